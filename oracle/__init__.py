@@ -1,0 +1,281 @@
+"""ctypes wrapper of the C oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs.  Never imported by the
+product package paper_1706_07772_b200/.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_HDR = os.path.join(_HERE, "oracle.h")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
+        subprocess.check_call(CFLAGS + ["-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_D = ctypes.POINTER(ctypes.c_double)
+
+
+class OrcParams(ctypes.Structure):
+    _fields_ = ([("ntypes", ctypes.c_int32)]
+                + [(f, _D) for f in ("r_sigma", "r_pi", "r_pipi", "gamma", "r_vdw", "eps", "alpha",
+                                     "gamma_w", "b131", "b132", "b133", "val", "val_boc")]
+                + [(f, _D) for f in ("p_bo1", "p_bo2", "p_bo3", "p_bo4", "p_bo5", "p_bo6")]
+                + [(f, ctypes.c_double) for f in ("p_boc1", "p_boc2", "p_vdw1", "coulomb_c")])
+
+
+class _P:
+    """Keeps the numpy buffers alive alongside the ctypes struct."""
+
+    def __init__(self, p):
+        self.keep = []
+        s = OrcParams()
+        s.ntypes = p.ntypes
+        for f in ("r_sigma", "r_pi", "r_pipi", "gamma", "r_vdw", "eps", "alpha", "gamma_w",
+                  "b131", "b132", "b133", "val", "val_boc", "p_bo1", "p_bo2", "p_bo3", "p_bo4",
+                  "p_bo5", "p_bo6"):
+            a = np.ascontiguousarray(getattr(p, f), dtype=np.float64).ravel()
+            self.keep.append(a)
+            setattr(s, f, a.ctypes.data_as(_D))
+        for f in ("p_boc1", "p_boc2", "p_vdw1", "coulomb_c"):
+            setattr(s, f, float(getattr(p, f)))
+        self.s = s
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.s)
+
+
+_lib = None
+V, I64, U64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64
+DBL, INT = ctypes.c_double, ctypes.c_int
+
+
+def _get():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        sig = {
+            "orc_wrap": (None, [I64, V, V, V]),
+            "orc_min_image": (DBL, [DBL, DBL]),
+            "orc_half_list_brute": (I64, [I64, V, V, DBL, V, V, I64]),
+            "orc_half_list_cells": (I64, [I64, V, V, DBL, V, V, I64]),
+            "orc_digest": (None, [I64, V, V, V, V]),
+            "orc_mix64_pub": (U64, [U64, U64]),
+            "orc_bo_raw": (None, [DBL, INT, INT, V, V]),
+            "orc_bonds": (I64, [I64, V, V, V, V, DBL, DBL, V, V, V, V, V, V, I64]),
+            "orc_delta": (None, [I64, V, V, V, V, V]),
+            "orc_bo_corr_pair": (None, [V, DBL, DBL, DBL, DBL, INT, INT, V, V, V]),
+            "orc_bo_correct": (None, [I64, V, V, V, V, V, V, V, V]),
+            "orc_taper": (None, [DBL, DBL, V, V]),
+            "orc_vdw": (None, [DBL, INT, INT, V, V, V]),
+            "orc_coulomb_kernel": (None, [DBL, INT, INT, V, V, V]),
+            "orc_pair": (None, [DBL, INT, INT, DBL, DBL, V, DBL, V, V]),
+            "orc_nonbonded": (None, [I64, V, V, V, V, V, DBL, V, V, V, V]),
+            "orc_atom_neighbors": (I64, [I64, I64, V, V, DBL, V, I64]),
+            "orc_atom_force": (None, [I64, I64, V, V, V, V, V, DBL, V, V]),
+            "orc_atom_bonds": (I64, [I64, I64, V, V, V, V, DBL, DBL, V, V, V, I64]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _a(x, dt):
+    return np.ascontiguousarray(x, dtype=dt)
+
+
+def _ptr(a):
+    return a.ctypes.data
+
+
+def wrap(pos, box):
+    pos, box = _a(pos, np.float64), _a(box, np.float64)
+    out = np.empty_like(pos)
+    _get().orc_wrap(len(pos), _ptr(pos), _ptr(box), _ptr(out))
+    return out
+
+
+def min_image(d, L):
+    return _get().orc_min_image(float(d), float(L))
+
+
+def half_list(pos, box, R, mode="cells"):
+    """Canonical half list (rowoff int64[n+1], col int32[P]): rows i asc, j>i asc."""
+    pos, box = _a(pos, np.float64), _a(box, np.float64)
+    n = len(pos)
+    fn = _get().orc_half_list_cells if mode == "cells" else _get().orc_half_list_brute
+    rowoff = np.empty(n + 1, np.int64)
+    cap = max(1, int(n * 260))
+    while True:
+        col = np.empty(cap, np.int32)
+        p = fn(n, _ptr(pos), _ptr(box), float(R), _ptr(rowoff), _ptr(col), cap)
+        if p <= cap:
+            return rowoff, col[:p].copy()
+        cap = int(p)
+
+
+def digest(n, rowoff, col):
+    cnt = np.empty(n, np.int64)
+    dig = np.empty(n, np.uint64)
+    _get().orc_digest(n, _ptr(_a(rowoff, np.int64)), _ptr(_a(col, np.int32)), _ptr(cnt), _ptr(dig))
+    return cnt, dig
+
+
+def mix64(a, b):
+    return _get().orc_mix64_pub(int(a), int(b))
+
+
+def bo_raw(r, ti, tj, params):
+    P = _P(params)
+    out = np.empty(4)
+    _get().orc_bo_raw(float(r), int(ti), int(tj), P.ref, _ptr(out))
+    return out
+
+
+def bo_corr_pair(raw, di, dboci, dj, dbocj, ti, tj, params):
+    P = _P(params)
+    raw = _a(raw, np.float64)
+    out, f = np.empty(4), np.empty(5)
+    _get().orc_bo_corr_pair(_ptr(raw), float(di), float(dboci), float(dj), float(dbocj), int(ti), int(tj),
+                            P.ref, _ptr(out), _ptr(f))
+    return out, f
+
+
+def bonds(pos, type_, box, params, r_bond, bo_cut, hrow, hcol):
+    """Full bond CSR: brow int64[n+1], bcol int32[B] (rows sorted by j), mirror int32[B]
+    (absolute entry index of the reverse bond), raw float64[B,4] (BO'sigma, BO'pi, BO'pipi, BO')."""
+    P = _P(params)
+    pos, box, type_ = _a(pos, np.float64), _a(box, np.float64), _a(type_, np.int32)
+    hrow, hcol = _a(hrow, np.int64), _a(hcol, np.int32)
+    n = len(pos)
+    brow = np.empty(n + 1, np.int64)
+    cap = max(16, 8 * n)
+    while True:
+        bcol = np.empty(cap, np.int32)
+        mir = np.empty(cap, np.int32)
+        raw = np.empty((cap, 4))
+        B = _get().orc_bonds(n, _ptr(pos), _ptr(type_), _ptr(box), P.ref, float(r_bond), float(bo_cut),
+                             _ptr(hrow), _ptr(hcol), _ptr(brow), _ptr(bcol), _ptr(mir), _ptr(raw), cap)
+        if B <= cap:
+            return brow, bcol[:B].copy(), mir[:B].copy(), raw[:B].copy()
+        cap = int(B)
+
+
+def delta(type_, params, brow, raw):
+    P = _P(params)
+    type_ = _a(type_, np.int32)
+    n = len(type_)
+    out = np.empty((n, 2))
+    _get().orc_delta(n, _ptr(type_), P.ref, _ptr(_a(brow, np.int64)), _ptr(_a(raw, np.float64)), _ptr(out))
+    return out
+
+
+def bo_correct(type_, params, brow, bcol, mirror, raw, dlt):
+    P = _P(params)
+    type_ = _a(type_, np.int32)
+    raw = _a(raw, np.float64)
+    out = np.empty_like(raw)
+    _get().orc_bo_correct(len(type_), _ptr(type_), P.ref, _ptr(_a(brow, np.int64)), _ptr(_a(bcol, np.int32)),
+                          _ptr(_a(mirror, np.int32)), _ptr(raw), _ptr(_a(dlt, np.float64)), _ptr(out))
+    return out
+
+
+def taper(r, R):
+    t, d = ctypes.c_double(), ctypes.c_double()
+    _get().orc_taper(float(r), float(R), ctypes.addressof(t), ctypes.addressof(d))
+    return t.value, d.value
+
+
+def vdw(r, ti, tj, params):
+    P = _P(params)
+    e, d = ctypes.c_double(), ctypes.c_double()
+    _get().orc_vdw(float(r), int(ti), int(tj), P.ref, ctypes.addressof(e), ctypes.addressof(d))
+    return e.value, d.value
+
+
+def coulomb_kernel(r, ti, tj, params):
+    P = _P(params)
+    e, d = ctypes.c_double(), ctypes.c_double()
+    _get().orc_coulomb_kernel(float(r), int(ti), int(tj), P.ref, ctypes.addressof(e), ctypes.addressof(d))
+    return e.value, d.value
+
+
+def pair(r, ti, tj, qi, qj, params, R):
+    """(E_vdW_pair, E_Coul_pair), dE/dr."""
+    P = _P(params)
+    e = np.empty(2)
+    d = ctypes.c_double()
+    _get().orc_pair(float(r), int(ti), int(tj), float(qi), float(qj), P.ref, float(R), _ptr(e),
+                    ctypes.addressof(d))
+    return e, d.value
+
+
+def nonbonded(pos, type_, q, box, params, R, hrow, hcol):
+    """E = [E_vdW, E_Coul], F (n,3)."""
+    P = _P(params)
+    pos, type_, q, box = _a(pos, np.float64), _a(type_, np.int32), _a(q, np.float64), _a(box, np.float64)
+    n = len(pos)
+    E = np.empty(2)
+    F = np.empty((n, 3))
+    _get().orc_nonbonded(n, _ptr(pos), _ptr(type_), _ptr(q), _ptr(box), P.ref, float(R),
+                         _ptr(_a(hrow, np.int64)), _ptr(_a(hcol, np.int32)), _ptr(E), _ptr(F))
+    return E, F
+
+
+def atom_neighbors(i, pos, box, R):
+    pos, box = _a(pos, np.float64), _a(box, np.float64)
+    out = np.empty(2048, np.int32)
+    m = _get().orc_atom_neighbors(int(i), len(pos), _ptr(pos), _ptr(box), float(R), _ptr(out), 2048)
+    assert m <= 2048
+    return out[:m].copy()
+
+
+def atom_force(i, pos, type_, q, box, params, R):
+    P = _P(params)
+    pos, type_, q, box = _a(pos, np.float64), _a(type_, np.int32), _a(q, np.float64), _a(box, np.float64)
+    F, Eh = np.empty(3), np.empty(2)
+    _get().orc_atom_force(int(i), len(pos), _ptr(pos), _ptr(type_), _ptr(q), _ptr(box), P.ref, float(R),
+                          _ptr(F), _ptr(Eh))
+    return F, Eh
+
+
+def atom_bonds(i, pos, type_, box, params, r_bond, bo_cut):
+    P = _P(params)
+    pos, type_, box = _a(pos, np.float64), _a(type_, np.int32), _a(box, np.float64)
+    part = np.empty(64, np.int32)
+    raw = np.empty((64, 4))
+    dl = np.empty(2)
+    m = _get().orc_atom_bonds(int(i), len(pos), _ptr(pos), _ptr(type_), _ptr(box), P.ref, float(r_bond),
+                              float(bo_cut), _ptr(part), _ptr(raw), _ptr(dl), 64)
+    assert m <= 64
+    return part[:m].copy(), raw[:m].copy(), dl
+
+
+def evaluate(system, params, cut, mode="cells"):
+    """Whole path in order: wrap -> list -> bonds -> Delta' -> corrected BO -> nonbonded."""
+    pos = wrap(system.pos, system.box)
+    hrow, hcol = half_list(pos, system.box, cut["r_nonb"], mode)
+    brow, bcol, mir, raw = bonds(pos, system.type, system.box, params, cut["r_bond"], cut["bo_cut"], hrow, hcol)
+    dlt = delta(system.type, params, brow, raw)
+    corr = bo_correct(system.type, params, brow, bcol, mir, raw, dlt)
+    E, F = nonbonded(pos, system.type, system.q, system.box, params, cut["r_nonb"], hrow, hcol)
+    return dict(pos=pos, hrow=hrow, hcol=hcol, brow=brow, bcol=bcol, mirror=mir, raw=raw, delta=dlt,
+                corr=corr, E=E, F=F)

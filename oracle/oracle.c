@@ -1,0 +1,448 @@
+/* ============================================================================
+ * CPU ORACLE for the ReaxFF list / bond-order / nonbonded hot path
+ * (arXiv:1706.07772, ReaxC-OMP).  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path
+ * (paper_1706_07772_b200/) never links, imports or executes it, and the two
+ * share no code, headers, tables or constants.
+ *
+ * Plain, slow, obviously correct: scalar IEEE fp64, compiled with
+ * -O2 -ffp-contract=off (no FMA contraction, no fast-math), glibc libm,
+ * single thread, every loop in the order the definition states.
+ *
+ * What it computes (the reading adopted in DESIGN.md):
+ *   O1 minimum image, half-open [-L/2, L/2)
+ *   O2 half neighbour list r^2 <= r_nonb^2            PAPER.md:152 (§3.3)
+ *   O3 uncorrected bond orders B1-B2, full bond list  PAPER.md:154-158 (§3.3); north_star
+ *   O4 Delta' per atom (B3)                           PAPER.md:37 (§2.1 over/under-coordination)
+ *   O5 corrected bond orders f1..f5 (B4-B8)           PAPER.md:160 (§3.3); north_star
+ *   O6 tapered shielded vdW + Coulomb (N1-N6),
+ *      Alg. 1/Alg. 2 pair loop with F_i += f, F_k -= f PAPER.md:87-110 (Alg. 1), 162-196 (Alg. 2)
+ *
+ * PARITY NOTE.  PAPER.md states no ReaxFF equations (it cites refs [6,7],
+ * PAPER.md:37); the functional forms B1-B8 / N1-N6 are the standard published
+ * ReaxFF forms as restated in SURVEY.md §8(c).  Every function below is pinned
+ * by tests (brute force, closed forms, special cases, finite differences,
+ * invariants), but whether these forms are what "the paper" computes is
+ * parity unpinned (no in-paper worked example exists).  DESIGN.md lists every
+ * reading taken.
+ * ==========================================================================*/
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "oracle.h"
+
+/* ---------------------------------------------------------------- a1 / O1 */
+
+/* a1: x <- x - L*floor(x/L); a result equal to L is mapped to 0. */
+void orc_wrap(int64_t n, const double* pos, const double box[3], double* out) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) {
+      double x = pos[3 * i + k], L = box[k];
+      double w = x - L * floor(x / L);
+      if (w >= L || w < 0.0) w = 0.0;
+      out[3 * i + k] = w;
+    }
+}
+
+/* O1: per axis d = x_j - x_i wrapped into [-L/2, L/2). */
+double orc_min_image(double d, double L) {
+  if (d >= 0.5 * L) d -= L;
+  else if (d < -0.5 * L) d += L;
+  return d;
+}
+
+/* r^2 = (dx*dx + dy*dy) + dz*dz, products separately rounded (no FMA). */
+static double orc_dist2(const double* pos, int64_t i, int64_t j, const double box[3], double d[3]) {
+  for (int k = 0; k < 3; ++k) d[k] = orc_min_image(pos[3 * j + k] - pos[3 * i + k], box[k]);
+  return (d[0] * d[0] + d[1] * d[1]) + d[2] * d[2];
+}
+
+/* ---------------------------------------------------------------- O2 list */
+
+/* Brute force: every unordered pair i<j with min-image r^2 <= R^2, emitted as
+ * canonical CSR (rows i ascending, j > i ascending).  This is the plain
+ * definition ("exactly the pairs with minimum-image distance <=
+ * r_nonb, each once with i<j").  Returns the pair count; writes at most cap. */
+int64_t orc_half_list_brute(int64_t n, const double* pos, const double box[3], double R,
+                            int64_t* rowoff, int32_t* col, int64_t cap) {
+  double R2 = R * R, d[3];
+  int64_t p = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    rowoff[i] = p;
+    for (int64_t j = i + 1; j < n; ++j)
+      if (orc_dist2(pos, i, j, box, d) <= R2) {
+        if (p < cap) col[p] = (int32_t)j;
+        ++p;
+      }
+  }
+  rowoff[n] = p;
+  return p;
+}
+
+static int cmp_i32(const void* a, const void* b) {
+  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x > y) - (x < y);
+}
+
+/* Cell-list version of the same set (O2): cells of side L/floor(L/(R(1+1e-9)))
+ * per axis (strictly wider than R, so rounding in floor(x/side) can never put
+ * two atoms within R more than one cell apart),
+ * the set of neighbour cells deduplicated (c0 has 2 cells per axis, so -1 and
+ * +1 name the same cell), candidate j > i kept iff r^2 <= R^2. */
+int64_t orc_half_list_cells(int64_t n, const double* pos, const double box[3], double R,
+                            int64_t* rowoff, int32_t* col, int64_t cap) {
+  int nc[3];
+  for (int k = 0; k < 3; ++k) {
+    nc[k] = (int)floor(box[k] / (R * (1.0 + 1e-9)));
+    if (nc[k] < 1) nc[k] = 1;
+  }
+  int64_t ncell = (int64_t)nc[0] * nc[1] * nc[2];
+  int64_t* head = (int64_t*)malloc(sizeof(int64_t) * ncell);
+  int64_t* next = (int64_t*)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+  int32_t* cell = (int32_t*)malloc(sizeof(int32_t) * 3 * (n > 0 ? n : 1));
+  int32_t* row = (int32_t*)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
+  for (int64_t c = 0; c < ncell; ++c) head[c] = -1;
+  for (int64_t i = n - 1; i >= 0; --i) {
+    int64_t c = 0;
+    for (int k = 2; k >= 0; --k) {
+      int ck = (int)floor(pos[3 * i + k] / (box[k] / nc[k]));
+      if (ck >= nc[k]) ck = nc[k] - 1;
+      if (ck < 0) ck = 0;
+      cell[3 * i + k] = ck;
+      c = c * nc[k] + ck;
+    }
+    next[i] = head[c];
+    head[c] = i;
+  }
+  double R2 = R * R, d[3];
+  int64_t p = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    rowoff[i] = p;
+    /* deduplicated neighbour cells */
+    int64_t nb[27];
+    int nnb = 0;
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          int cx = ((cell[3 * i] + dx) % nc[0] + nc[0]) % nc[0];
+          int cy = ((cell[3 * i + 1] + dy) % nc[1] + nc[1]) % nc[1];
+          int cz = ((cell[3 * i + 2] + dz) % nc[2] + nc[2]) % nc[2];
+          int64_t c = ((int64_t)cz * nc[1] + cy) * nc[0] + cx;
+          int dup = 0;
+          for (int m = 0; m < nnb; ++m) dup |= (nb[m] == c);
+          if (!dup) nb[nnb++] = c;
+        }
+    int64_t len = 0;
+    for (int m = 0; m < nnb; ++m)
+      for (int64_t j = head[nb[m]]; j >= 0; j = next[j])
+        if (j > i && orc_dist2(pos, i, j, box, d) <= R2) row[len++] = (int32_t)j;
+    qsort(row, (size_t)len, sizeof(int32_t), cmp_i32);
+    for (int64_t m = 0; m < len; ++m) {
+      if (p < cap) col[p] = row[m];
+      ++p;
+    }
+  }
+  rowoff[n] = p;
+  free(head); free(next); free(cell); free(row);
+  return p;
+}
+
+/* Per-atom digest for large configs: for each atom, the
+ * number of pairs it belongs to and sum of mix64(min,max) mod 2^64. */
+static uint64_t orc_mix64(uint64_t a, uint64_t b) {
+  uint64_t z = (a << 32) ^ b;
+  z ^= z >> 33; z *= 0xff51afd7ed558ccdull;
+  z ^= z >> 33; z *= 0xc4ceb9fe1a85ec53ull;
+  z ^= z >> 33;
+  return z;
+}
+void orc_digest(int64_t n, const int64_t* rowoff, const int32_t* col, int64_t* cnt, uint64_t* dig) {
+  for (int64_t i = 0; i < n; ++i) { cnt[i] = 0; dig[i] = 0; }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = rowoff[i]; p < rowoff[i + 1]; ++p) {
+      int64_t j = col[p];
+      uint64_t h = orc_mix64((uint64_t)(i < j ? i : j), (uint64_t)(i < j ? j : i));
+      cnt[i] += 1; cnt[j] += 1; dig[i] += h; dig[j] += h;
+    }
+}
+uint64_t orc_mix64_pub(uint64_t a, uint64_t b) { return orc_mix64(a, b); }
+
+/* ------------------------------------------------------------ O3 bond orders */
+
+/* B1-B2 for one pair at distance r (north_star: "uncorrected bond orders
+ * BO'sigma/pi/pipi", combining rule
+ * r0_ij = (r_i + r_j)/2, reading 9).  out = {BO'sigma, BO'pi, BO'pipi, BO'}. */
+void orc_bo_raw(double r, int ti, int tj, const orc_params* P, double out[4]) {
+  int nt = P->ntypes, tp = ti * nt + tj;
+  double r0s = 0.5 * (P->r_sigma[ti] + P->r_sigma[tj]);
+  double r0p = 0.5 * (P->r_pi[ti] + P->r_pi[tj]);
+  double r0pp = 0.5 * (P->r_pipi[ti] + P->r_pipi[tj]);
+  double bs = exp(P->p_bo1[tp] * pow(r / r0s, P->p_bo2[tp]));
+  double bp = exp(P->p_bo3[tp] * pow(r / r0p, P->p_bo4[tp]));
+  double bpp = exp(P->p_bo5[tp] * pow(r / r0pp, P->p_bo6[tp]));
+  out[0] = bs;
+  out[1] = bp;
+  out[2] = bpp;
+  out[3] = (bs + bp) + bpp; /* B2, summed in this order */
+}
+
+/* O3: for every canonical pair of the half list with r <= r_bond (r^2 <=
+ * r_bond^2), BO' from B1-B2; a bond iff BO' >= bo_cut (reading 2A).  Emits the
+ * FULL list (both i->j and j->i, "requires the bond list to be a
+ * full list with both i-j and j-i bonds available") as CSR with rows sorted by
+ * j, plus the mirror index.  bo: [B][4].  Returns B (entries);
+ * writes nothing past cap. */
+int64_t orc_bonds(int64_t n, const double* pos, const int32_t* type, const double box[3],
+                  const orc_params* P, double r_bond, double bo_cut, const int64_t* hrow,
+                  const int32_t* hcol, int64_t* brow, int32_t* bcol, int32_t* bmirror,
+                  double* bo, int64_t cap) {
+  double rb2 = r_bond * r_bond, d[3], v[4];
+  int64_t* deg = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+  /* pass 1: count kept bonds per atom */
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = hrow[i]; p < hrow[i + 1]; ++p) {
+      int64_t j = hcol[p];
+      double r2 = orc_dist2(pos, i, j, box, d);
+      if (r2 > rb2) continue;
+      orc_bo_raw(sqrt(r2), type[i], type[j], P, v);
+      if (v[3] >= bo_cut) { deg[i]++; deg[j]++; }
+    }
+  brow[0] = 0;
+  for (int64_t i = 0; i < n; ++i) brow[i + 1] = brow[i] + deg[i];
+  int64_t B = brow[n];
+  if (B > cap) { free(deg); return B; }
+  /* pass 2: fill.  Canonical pairs are visited in (i asc, j asc) order, so row
+   * i receives partners j < i (from earlier rows, ascending i) before its own
+   * partners j > i (ascending): every row ends sorted by j. */
+  int64_t* fill = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = hrow[i]; p < hrow[i + 1]; ++p) {
+      int64_t j = hcol[p];
+      double r2 = orc_dist2(pos, i, j, box, d);
+      if (r2 > rb2) continue;
+      orc_bo_raw(sqrt(r2), type[i], type[j], P, v);
+      if (v[3] < bo_cut) continue;
+      int64_t ei = brow[i] + fill[i]++, ej = brow[j] + fill[j]++;
+      bcol[ei] = (int32_t)j; bcol[ej] = (int32_t)i;
+      bmirror[ei] = (int32_t)ej; /* mirror = absolute entry index of j->i */
+      bmirror[ej] = (int32_t)ei;
+      for (int k = 0; k < 4; ++k) { bo[4 * ei + k] = v[k]; bo[4 * ej + k] = v[k]; }
+    }
+  free(deg); free(fill);
+  return B;
+}
+
+/* O4 / B3: Delta'_i = sum_j BO'_ij - Val_i and Delta'boc_i = sum_j BO'_ij - Val^boc_i,
+ * the sum over the kept bonds of row i in ascending j (readings 4, 6). */
+void orc_delta(int64_t n, const int32_t* type, const orc_params* P, const int64_t* brow,
+               const double* bo, double* delta) {
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int64_t e = brow[i]; e < brow[i + 1]; ++e) s += bo[4 * e + 3];
+    delta[2 * i] = s - P->val[type[i]];
+    delta[2 * i + 1] = s - P->val_boc[type[i]];
+  }
+}
+
+/* B4-B8 for one bond (i,j) given its BO' terms and the two atoms' Delta'.
+ * out = {BO, BOsigma, BOpi, BOpipi}; f (optional) = {f1, f2, f3, f4, f5}. */
+void orc_bo_corr_pair(const double raw[4], double di, double dboci, double dj, double dbocj,
+                      int ti, int tj, const orc_params* P, double out[4], double* f) {
+  int tp = ti * P->ntypes + tj;
+  double p1 = P->p_boc1, p2 = P->p_boc2;
+  double vi = P->val[ti], vj = P->val[tj];
+  double pboc3 = sqrt(P->b132[ti] * P->b132[tj]);
+  double pboc4 = sqrt(P->b131[ti] * P->b131[tj]);
+  double pboc5 = sqrt(P->b133[ti] * P->b133[tj]);
+  (void)tp;
+  double bo = raw[3];
+  double f2 = exp(-p1 * di) + exp(-p1 * dj);                                    /* B4 */
+  double f3 = -(1.0 / p2) * log(0.5 * (exp(-p2 * di) + exp(-p2 * dj)));         /* B5 */
+  double f1 = 0.5 * ((vi + f2) / (vi + f2 + f3) + (vj + f2) / (vj + f2 + f3));  /* B6 */
+  double f4 = 1.0 / (1.0 + exp(-pboc3 * (pboc4 * bo * bo - dboci) + pboc5));    /* B7 */
+  double f5 = 1.0 / (1.0 + exp(-pboc3 * (pboc4 * bo * bo - dbocj) + pboc5));
+  double BO = bo * f1 * f4 * f5;                                                /* B8 */
+  double BOpi = raw[1] * f1 * f1 * f4 * f5;
+  double BOpipi = raw[2] * f1 * f1 * f4 * f5;
+  out[0] = BO;
+  out[1] = BO - BOpi - BOpipi; /* reading 5 */
+  out[2] = BOpi;
+  out[3] = BOpipi;
+  if (f) { f[0] = f1; f[1] = f2; f[2] = f3; f[3] = f4; f[4] = f5; }
+}
+
+/* O5: B4-B8 once per unordered bond in canonical orientation (i < j, so f4
+ * uses Delta'boc_i and f5 uses Delta'boc_j) and mirrored to both entries, so
+ * BO_ij == BO_ji bitwise.  corr: [B][4]. */
+void orc_bo_correct(int64_t n, const int32_t* type, const orc_params* P, const int64_t* brow,
+                    const int32_t* bcol, const int32_t* bmirror, const double* bo,
+                    const double* delta, double* corr) {
+  double out[4];
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = brow[i]; e < brow[i + 1]; ++e) {
+      int64_t j = bcol[e];
+      if (j < i) continue;
+      orc_bo_corr_pair(&bo[4 * e], delta[2 * i], delta[2 * i + 1], delta[2 * j], delta[2 * j + 1],
+                       type[i], type[j], P, out, NULL);
+      int64_t em = bmirror[e];
+      for (int k = 0; k < 4; ++k) { corr[4 * e + k] = out[k]; corr[4 * em + k] = out[k]; }
+    }
+}
+
+/* -------------------------------------------------------------- O6 nonbonded */
+
+/* N1: 7th-order taper in x = r/R (inner radius 0, reading 14), and dTap/dr. */
+void orc_taper(double r, double R, double* tap, double* dtap) {
+  double x = r / R;
+  double x2 = x * x, x3 = x2 * x, x4 = x3 * x, x5 = x4 * x, x6 = x5 * x, x7 = x6 * x;
+  *tap = 1.0 - 35.0 * x4 + 84.0 * x5 - 70.0 * x6 + 20.0 * x7;
+  *dtap = -140.0 * x3 * (1.0 - x) * (1.0 - x) * (1.0 - x) / R;
+}
+
+/* N2-N4: shielded vdW (untapered) e_v and de_v/dr for one pair.
+ * Combining rules (reading 9): D = sqrt(eps_i eps_j), alpha = sqrt(alpha_i alpha_j),
+ * r_vdW = 2 sqrt(r_vdw_i r_vdw_j), gamma_w = sqrt(gamma_w_i gamma_w_j). */
+void orc_vdw(double r, int ti, int tj, const orc_params* P, double* ev, double* dev) {
+  double D = sqrt(P->eps[ti] * P->eps[tj]);
+  double alpha = sqrt(P->alpha[ti] * P->alpha[tj]);
+  double rvdw = 2.0 * sqrt(P->r_vdw[ti] * P->r_vdw[tj]);
+  double gw = sqrt(P->gamma_w[ti] * P->gamma_w[tj]);
+  double p = P->p_vdw1;
+  double sv = pow(r, p) + pow(gw, -p);
+  double f13 = pow(sv, 1.0 / p);                                   /* N2 */
+  double u = 1.0 - f13 / rvdw;
+  double e1 = exp(alpha * u), e2 = exp(0.5 * alpha * u);
+  *ev = D * (e1 - 2.0 * e2);                                       /* N3 */
+  double df13 = pow(sv, 1.0 / p - 1.0) * pow(r, p - 1.0);          /* d f13 / dr */
+  *dev = -D * (alpha / rvdw) * (e1 - e2) * df13;                   /* N4 (untapered part) */
+}
+
+/* N5 (untapered): shielded Coulomb kernel k(r) = S^(-1/3), S = r^3 + gamma_ij^-3,
+ * gamma_ij = sqrt(gamma_i gamma_j); returns k and dk/dr. */
+void orc_coulomb_kernel(double r, int ti, int tj, const orc_params* P, double* k, double* dk) {
+  double g = sqrt(P->gamma[ti] * P->gamma[tj]);
+  double S = r * r * r + pow(g, -3.0);
+  *k = pow(S, -1.0 / 3.0);
+  *dk = -r * r * pow(S, -4.0 / 3.0);
+}
+
+/* One Alg. 2 pair ("evdW, fvdW <- vdWaals(atom[i], atom[k]);
+ * eClmb, fClmb <- Coulomb(atom[i], atom[k])"): tapered energies and the total
+ * dE/dr.  e[0] = Tap*e_v, e[1] = C q_i q_j Tap S^(-1/3). */
+void orc_pair(double r, int ti, int tj, double qi, double qj, const orc_params* P, double R,
+              double e[2], double* dEdr) {
+  double tap, dtap, ev, dev, k, dk;
+  orc_taper(r, R, &tap, &dtap);
+  orc_vdw(r, ti, tj, P, &ev, &dev);
+  orc_coulomb_kernel(r, ti, tj, P, &k, &dk);
+  double cqq = P->coulomb_c * qi * qj;
+  e[0] = tap * ev;
+  e[1] = cqq * tap * k;
+  double dEv = dtap * ev + tap * dev;      /* N4 */
+  double dEc = cqq * (dtap * k + tap * dk); /* N5 */
+  *dEdr = dEv + dEc;
+}
+
+/* Neumaier compensated summation. */
+typedef struct { double s, c; } orc_ksum;
+static void ks_add(orc_ksum* a, double x) {
+  double t = a->s + x;
+  if (fabs(a->s) >= fabs(x)) a->c += (a->s - t) + x;
+  else a->c += (x - t) + a->s;
+  a->s = t;
+}
+
+/* O6: Alg. 1 / Alg. 2 over the canonical half list:
+ * E += e(i,k); f = g*d with g = (dE/dr)/r and d = minimum-image(x_k - x_i);
+ * gForce[i] += f; gForce[k] -= f (Alg. 2 line 12 read as "-=", reading 20).
+ * Energies use Neumaier sums in canonical pair order.  E = {E_vdW, E_Coul}. */
+void orc_nonbonded(int64_t n, const double* pos, const int32_t* type, const double* q,
+                   const double box[3], const orc_params* P, double R, const int64_t* hrow,
+                   const int32_t* hcol, double E[2], double* F) {
+  orc_ksum ev = {0, 0}, ec = {0, 0};
+  double d[3], e[2], dEdr;
+  for (int64_t i = 0; i < 3 * n; ++i) F[i] = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = hrow[i]; p < hrow[i + 1]; ++p) {
+      int64_t k = hcol[p];
+      double r = sqrt(orc_dist2(pos, i, k, box, d));
+      orc_pair(r, type[i], type[k], q[i], q[k], P, R, e, &dEdr);
+      ks_add(&ev, e[0]);
+      ks_add(&ec, e[1]);
+      double g = dEdr / r;
+      for (int m = 0; m < 3; ++m) {
+        F[3 * i + m] += g * d[m];
+        F[3 * k + m] -= g * d[m];
+      }
+    }
+  E[0] = ev.s + ev.c;
+  E[1] = ec.s + ec.c;
+}
+
+/* ------------------------------------------ per-atom brute force (large N) */
+
+/* All j != i with min-image r^2 <= R^2 (the FULL neighbour set of atom i),
+ * ascending; O(N).  Used to sample c3/c4 outputs one atom at a time. */
+int64_t orc_atom_neighbors(int64_t i, int64_t n, const double* pos, const double box[3], double R,
+                           int32_t* out, int64_t cap) {
+  double R2 = R * R, d[3];
+  int64_t m = 0;
+  for (int64_t j = 0; j < n; ++j)
+    if (j != i && orc_dist2(pos, i, j, box, d) <= R2) {
+      if (m < cap) out[m] = (int32_t)j;
+      ++m;
+    }
+  return m;
+}
+
+/* Force on atom i and its pair-energy share (1/2 of each of its pairs),
+ * brute force over all j.  F = sum_j g_ij d_ij (the F_i += f side of Alg. 1). */
+void orc_atom_force(int64_t i, int64_t n, const double* pos, const int32_t* type, const double* q,
+                    const double box[3], const orc_params* P, double R, double F[3], double Ehalf[2]) {
+  double R2 = R * R, d[3], e[2], dEdr;
+  orc_ksum a = {0, 0}, b = {0, 0};
+  F[0] = F[1] = F[2] = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    if (j == i) continue;
+    double r2 = orc_dist2(pos, i, j, box, d);
+    if (r2 > R2) continue;
+    double r = sqrt(r2);
+    orc_pair(r, type[i], type[j], q[i], q[j], P, R, e, &dEdr);
+    ks_add(&a, 0.5 * e[0]);
+    ks_add(&b, 0.5 * e[1]);
+    double g = dEdr / r;
+    for (int m = 0; m < 3; ++m) F[m] += g * d[m];
+  }
+  Ehalf[0] = a.s + a.c;
+  Ehalf[1] = b.s + b.c;
+}
+
+/* Bonds of atom i by brute force: partners (ascending), BO' terms, and the
+ * atom's Delta' — O(N) per call. */
+int64_t orc_atom_bonds(int64_t i, int64_t n, const double* pos, const int32_t* type,
+                       const double box[3], const orc_params* P, double r_bond, double bo_cut,
+                       int32_t* partner, double* raw, double* delta, int64_t cap) {
+  double rb2 = r_bond * r_bond, d[3], v[4];
+  int64_t m = 0;
+  double s = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    if (j == i) continue;
+    double r2 = orc_dist2(pos, i, j, box, d);
+    if (r2 > rb2) continue;
+    orc_bo_raw(sqrt(r2), type[i < j ? i : j], type[i < j ? j : i], P, v);
+    if (v[3] < bo_cut) continue;
+    if (m < cap) {
+      partner[m] = (int32_t)j;
+      for (int k = 0; k < 4; ++k) raw[4 * m + k] = v[k];
+    }
+    s += v[3];
+    ++m;
+  }
+  delta[0] = s - P->val[type[i]];
+  delta[1] = s - P->val_boc[type[i]];
+  return m;
+}
