@@ -1,0 +1,1025 @@
+// Device kernels of the ReaxFF hot path (arXiv:1706.07772 ReaxC-OMP kernels,
+// re-designed for B200).  Included once, by reax.cu.
+#pragma once
+#include "common.cuh"
+
+namespace rx {
+
+__constant__ WindowTables c_win;
+
+__device__ __forceinline__ void set_flag(Status* st, int f) { atomicOr(&st->flags, f); }
+
+// a1: x <- x - L floor(x/L), a result equal to L (or below 0 by rounding) -> 0.
+// Explicitly rounded operations keep it bit-identical to any IEEE scalar code.
+__device__ __forceinline__ double wrap_coord(double x, double L) {
+  double w = __dsub_rn(x, __dmul_rn(L, floor(__ddiv_rn(x, L))));
+  return (w >= L || w < 0.0) ? 0.0 : w;
+}
+
+// ===================================================================== scan
+// Exclusive prefix sum in 3 launches (block partials, top, final); T in/out.
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+template <typename TI>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_partial(const TI* in, int64_t n, long long* part) {
+  __shared__ long long red[32];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  long long s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    int64_t i = base + threadIdx.x + (int64_t)k * SCAN_THREADS;
+    if (i < n) s += (long long)in[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    long long v = red[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  }
+}
+
+// single block: exclusive scan of nparts partials in place; total -> part[nparts]
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_top(long long* part, int nparts) {
+  __shared__ long long warp_tot[32];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nparts; base += SCAN_THREADS) {
+    int i = base + threadIdx.x;
+    long long v = i < nparts ? part[i] : 0;
+    long long x = v;
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      long long t = warp_tot[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;
+    }
+    __syncthreads();
+    long long incl = x + (w > 0 ? warp_tot[w - 1] : 0) + carry;
+    if (i < nparts) part[i] = incl - v;
+    __syncthreads();
+    if (threadIdx.x == SCAN_THREADS - 1) carry = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[nparts] = carry;
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const TI* in, int64_t n, const long long* part, TO* out) {
+  __shared__ long long warp_tot[32];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // each thread owns SCAN_ITEMS consecutive elements
+  int64_t i0 = base + (int64_t)threadIdx.x * SCAN_ITEMS;
+  long long v[SCAN_ITEMS];
+  long long s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    v[k] = (i0 + k < n) ? (long long)in[i0 + k] : 0;
+    s += v[k];
+  }
+  long long x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    long long t = warp_tot[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_tot[lane] = t;
+  }
+  __syncthreads();
+  long long run = part[blockIdx.x] + x - s + (w > 0 ? warp_tot[w - 1] : 0);
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    if (i0 + k < n) out[i0 + k] = (TO)run;
+    run += v[k];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = (TO)part[gridDim.x];
+}
+
+// ================================================================ a1-a2 bin
+// wrap, validate, sub-cell id, histogram
+__global__ void k_bin(int n, const double* __restrict__ pos, const int* __restrict__ type, Grid g,
+                      int nt, int* __restrict__ cell_of, int* __restrict__ cell_cnt, Status* st) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c[3];
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double x = pos[3 * (int64_t)i + k];
+    bad |= !isfinite(x);
+    double w = isfinite(x) ? wrap_coord(x, g.L[k]) : 0.0;
+    int ck = (int)(w * g.inv_h[k]);
+    c[k] = ck >= g.nc[k] ? g.nc[k] - 1 : ck;
+  }
+  if (bad) set_flag(st, ST_NONFINITE_IN);
+  int t = type[i];
+  if (t < 0 || t >= nt) set_flag(st, ST_TYPE);
+  int cid = (c[2] * g.nc[1] + c[1]) * g.nc[0] + c[0];
+  cell_of[i] = cid;
+  atomicAdd(&cell_cnt[cid], 1);
+}
+
+// counting-sort scatter; cell_cnt returns to zero (ready for the next call)
+__global__ void k_scatter(int n, const int* __restrict__ cell_of, const int* __restrict__ cell_start,
+                          int* __restrict__ cell_cnt, int* __restrict__ perm) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = cell_of[i];
+  int r = atomicSub(&cell_cnt[c], 1) - 1;
+  perm[cell_start[c] + r] = i;
+}
+
+// Per cell (one warp): order the cell's atoms by original index (rank
+// sort in registers; deterministic), then gather the sorted arrays.
+__global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int* __restrict__ perm,
+                              const double* __restrict__ pos, const int* __restrict__ type, Grid g, int nt,
+                              int* __restrict__ iperm, double4* __restrict__ spos, float4* __restrict__ sloc,
+                              int* __restrict__ stype) {
+  int c = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  int lane = threadIdx.x & 31;
+  if (c >= ncell) return;
+  int a = cell_start[c], b = cell_start[c + 1], m = b - a;
+  if (m <= 32) {
+    int v = lane < m ? perm[a + lane] : 0x7fffffff;
+    int rank = 0;
+    for (int q = 0; q < m; ++q) rank += (__shfl_sync(0xffffffffu, v, q) < v);
+    __syncwarp();
+    if (lane < m) perm[a + rank] = v;
+  } else if (lane == 0) {  // rare (Poisson tail): serial insertion sort
+    for (int i = a + 1; i < b; ++i) {
+      int v = perm[i], j = i - 1;
+      while (j >= a && perm[j] > v) { perm[j + 1] = perm[j]; --j; }
+      perm[j + 1] = v;
+    }
+  }
+  __syncwarp();
+  int cc[3] = {c % g.nc[0], (c / g.nc[0]) % g.nc[1], c / (g.nc[0] * g.nc[1])};
+  for (int q = lane; q < m; q += 32) {
+    int s = a + q;
+    int i = perm[s];
+    double w[3];
+    float l[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double x = pos[3 * (int64_t)i + d];
+      w[d] = isfinite(x) ? wrap_coord(x, g.L[d]) : 0.0;
+      l[d] = (float)(w[d] - cc[d] * g.h[d]);
+    }
+    int t = type[i];
+    t = (t < 0 || t >= nt) ? 0 : t;  // flagged by k_bin; clamp keeps every table index valid
+    spos[s] = make_double4(w[0], w[1], w[2], 0.0);
+    sloc[s] = make_float4(l[0], l[1], l[2], __int_as_float(t));
+    stype[s] = t;
+    iperm[i] = s;
+  }
+}
+
+// ======================================================== window of a block
+// Shared-memory description of a home block's neighbour window.
+struct WinSmem {
+  int start[NWB];      // first sorted atom of each used window cell
+  int cnt[NWB];
+  int slot[NWB + 1];   // slot base (prefix of cnt)
+  double shift[NWB][3];// periodic image shift (0 or +-L) of each window cell
+  float off[NWB][3];   // cell origin relative to the block origin (fp32)
+  int home_ok[NHOME];  // home sub-cell exists (odd nc leaves the last block partial)
+};
+
+// Fill WinSmem for block b (all threads participate). Returns total slots.
+__device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restrict__ cell_start) {
+  // b = home block index
+  int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
+  int base[3] = {bx * HB, by * HB, bz * HB};
+  int nwu = c_win.nwu;
+  for (int k = threadIdx.x; k < nwu; k += blockDim.x) {
+    int wb = c_win.wu[k];
+    int wv[3] = {wb % WB, (wb / WB) % WB, wb / (WB * WB)};
+    int cc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      int u = base[a] + wv[a] - SR;          // unwrapped sub-cell
+      int m = u >= 0 ? u / g.nc[a] : -((-u + g.nc[a] - 1) / g.nc[a]);  // floor(u / nc)
+      cc[a] = u - m * g.nc[a];
+      W.shift[k][a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
+      W.off[k][a] = (float)((double)(u - base[a]) * g.h[a]);
+    }
+    int cid = (cc[2] * g.nc[1] + cc[1]) * g.nc[0] + cc[0];
+    int s0 = cell_start[cid];
+    W.start[k] = s0;
+    W.cnt[k] = cell_start[cid + 1] - s0;
+  }
+  if (threadIdx.x < NHOME) {
+    int h = threadIdx.x;
+    int hv[3] = {h % HB, (h / HB) % HB, h / (HB * HB)};
+    W.home_ok[h] = (base[0] + hv[0] < g.nc[0]) && (base[1] + hv[1] < g.nc[1]) && (base[2] + hv[2] < g.nc[2]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // warp 0: exclusive scan over <= 216 counts
+    int carry = 0;
+    for (int k0 = 0; k0 < nwu; k0 += 32) {
+      int k = k0 + threadIdx.x;
+      int v = k < nwu ? W.cnt[k] : 0;
+      int x = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((int)threadIdx.x >= o) x += y;
+      }
+      if (k < nwu) W.slot[k] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (threadIdx.x == 0) W.slot[nwu] = carry;
+  }
+  __syncthreads();
+  return W.slot[nwu];
+}
+
+// rows of the block: home sub-cell h, slot range [slot[home_k[h]], slot[home_k[h]+1])
+__device__ __forceinline__ bool row_of(const WinSmem& W, int r, int& h, int& si) {
+  for (h = 0; h < NHOME; ++h) {
+    if (!W.home_ok[h]) continue;
+    int k = c_win.home_k[h];
+    int c = W.cnt[k];
+    if (r < c) {
+      si = W.slot[k] + r;
+      return true;
+    }
+    r -= c;
+  }
+  return false;
+}
+
+// ========================================================= a3-a4 list build
+constexpr int NBR_THREADS = 256;
+
+struct NbrSmem {
+  WinSmem W;
+  float rcand2[NTP_MAX];
+};
+
+// One CTA per home block.  Candidates of the window are staged in shared
+// memory as fp32 coordinates relative to the block origin; each warp scans
+// one row (atom) against the forward runs of its sub-cell's half stencil and
+// its own cell (j after i), classifies r^2 in fp32 with a band of +-m around
+// R^2 that is ~50x wider than the fp32 error bound, settles the band with the
+// exact FMA-free fp64 test, and compacts accepted candidates with a ballot.
+__global__ void __launch_bounds__(NBR_THREADS) k_nbr_build(Grid g, const int* __restrict__ cell_start,
+    const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
+    uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
+    int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ NbrSmem S;
+  const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
+  float4* cand = reinterpret_cast<float4*>(dyn);                                // window_cap
+  int* cand_j = reinterpret_cast<int*>(cand + window_cap);                       // window_cap
+  unsigned char* cand_k = reinterpret_cast<unsigned char*>(cand_j + window_cap); // window_cap
+  const int nt = prm->nt;
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) S.rcand2[t] = prm->rcand2[t];
+  const float R2lo = prm->R2lo, R2hi = prm->R2hi, rcmax = prm->rcand2_max;
+  const double R2 = prm->R2;
+  int W = build_window(S.W, blk, g, cell_start);
+  const int nwu = c_win.nwu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  if (W > window_cap) {
+    if (threadIdx.x == 0) {
+      set_flag(st, ST_WIN_OVF);
+      atomicMax(&st->max_window, W);
+    }
+    // leave every row of the block empty so later kernels stay in bounds
+    for (int r = split * nwarp + warp;; r += nsplit * nwarp) {
+      int h, si;
+      if (!row_of(S.W, r, h, si)) break;
+      int s = S.W.start[c_win.home_k[h]] + (si - S.W.slot[c_win.home_k[h]]);
+      if (lane == 0) { nbr_len[s] = 0; bc_len[s] = 0; }
+    }
+    return;
+  }
+  for (int k = warp; k < nwu; k += nwarp) {
+    int s0 = S.W.start[k], c = S.W.cnt[k], b0 = S.W.slot[k];
+    float ox = S.W.off[k][0], oy = S.W.off[k][1], oz = S.W.off[k][2];
+    for (int a = lane; a < c; a += 32) {
+      float4 l = sloc[s0 + a];
+      cand[b0 + a] = make_float4(l.x + ox, l.y + oy, l.z + oz, l.w);
+      cand_j[b0 + a] = s0 + a;
+      cand_k[b0 + a] = (unsigned char)k;
+    }
+  }
+  __syncthreads();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int r = split * nwarp + warp;; r += nsplit * nwarp) {
+    int h, si;
+    if (!row_of(S.W, r, h, si)) break;
+    const int s = cand_j[si];
+    const float4 ri = cand[si];
+    const int ti = __float_as_int(ri.w);
+    int len = 0, nc = 0;
+    uint16_t* row = nbr + (int64_t)s * row_cap;
+    int* crow = bc + (int64_t)s * cand_cap;
+    const int nrun = c_win.nrun[h];
+    const int kh = c_win.home_k[h];
+    for (int q = 0; q <= nrun; ++q) {
+      int sa, sb;
+      if (q < nrun) {
+        sa = S.W.slot[c_win.run_a[h][q]];
+        sb = S.W.slot[c_win.run_b[h][q] + 1];
+      } else {  // own cell: partners after i (sorted order)
+        sa = si + 1;
+        sb = S.W.slot[kh + 1];
+      }
+      for (int b0 = sa; b0 < sb; b0 += 32) {
+        int slot = b0 + lane;
+        bool valid = slot < sb;
+        float4 c = valid ? cand[slot] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
+        float dx = c.x - ri.x, dy = c.y - ri.y, dz = c.z - ri.z;
+        float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        bool in = valid && r2 < R2lo;
+        bool band = valid && !in && r2 <= R2hi;
+        if (__any_sync(0xffffffffu, band)) {
+          if (band) {  // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
+            double4 xi = spos[s];
+            double4 xj = spos[cand_j[slot]];
+            int k = cand_k[slot];
+            double ex = __dadd_rn(__dsub_rn(xj.x, xi.x), S.W.shift[k][0]);
+            double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), S.W.shift[k][1]);
+            double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), S.W.shift[k][2]);
+            double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+            in = d2 <= R2;
+          }
+        }
+        unsigned m = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          int p = len + __popc(m & lt_mask);
+          if (p < row_cap) row[p] = (uint16_t)slot;
+        }
+        len += __popc(m);
+        if (__any_sync(0xffffffffu, in && r2 <= rcmax)) {  // rare: ~3 bond candidates per row
+          bool bcand = in && r2 <= S.rcand2[ti * nt + __float_as_int(c.w)];
+          unsigned mb = __ballot_sync(0xffffffffu, bcand);
+          if (bcand) {
+            int p = nc + __popc(mb & lt_mask);
+            if (p < cand_cap) crow[p] = cand_j[slot];
+          }
+          nc += __popc(mb);
+        }
+      }
+    }
+    if (lane == 0) {
+      nbr_len[s] = len < row_cap ? len : row_cap;
+      bc_len[s] = nc < cand_cap ? nc : cand_cap;
+      if (len > row_cap) { set_flag(st, ST_ROW_OVF); atomicMax(&st->max_row, len); }
+      if (nc > cand_cap) { set_flag(st, ST_CAND_OVF); atomicMax(&st->max_cand, nc); }
+    }
+  }
+}
+
+// =================================================== a4 bond orders (B1-B2)
+__device__ __forceinline__ double min_image(double d, double L) {
+  // same rule as the definition: [-L/2, L/2)
+  if (d >= 0.5 * L) return __dsub_rn(d, L);
+  if (d < -0.5 * L) return __dadd_rn(d, L);
+  return d;
+}
+
+// BO'sigma, BO'pi, BO'pipi, BO' at distance r:  exp(pa * (r/r0)^pb), with
+// (r/r0)^pb = exp(pb (ln r - ln r0)); one log shared by the three terms.
+__device__ __forceinline__ double4 bo_raw(double r, const BOPair& c) {
+  double lr = log(r);
+  double v[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v[k] = exp(c.pa[k] * exp(c.pb[k] * (lr - c.lr0[k])));
+  return make_double4(v[0], v[1], v[2], (v[0] + v[1]) + v[2]);
+}
+
+// Bond candidates are flattened across a warp: lane i owns atom a0+i, the
+// warp scans the candidate counts and every lane then evaluates one
+// (atom, candidate) pair per round: the exact FMA-free r^2 <= r_bond^2 test,
+// B1-B2, and BO' >= bo_cut.  Rejected candidates are marked -1 in place;
+// kept ones store BO' and are counted per atom (bdeg).
+__device__ __forceinline__ int warp_find(int incl, int t) {
+  // largest q with excl(q) <= t, where incl is the lane's inclusive prefix
+  int q = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    int v = __shfl_sync(0xffffffffu, incl, q + step - 1);
+    if (t >= v) q += step;
+  }
+  return q;
+}
+
+__global__ void k_bond_eval(int n, const double4* __restrict__ spos, const int* __restrict__ stype, Grid g,
+                            const DevParams* __restrict__ prm, int* __restrict__ bc, const int* __restrict__ bc_len,
+                            double4* __restrict__ bc_raw, int cand_cap, int* __restrict__ bdeg) {
+  __shared__ BOPair sbo[NTP_MAX];
+  const int nt = prm->nt;
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) sbo[t] = prm->bo[t];
+  __syncthreads();
+  const double rb2 = prm->rb2, bo_cut = prm->bo_cut;
+  const int lane = threadIdx.x & 31;
+  const int a0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
+  if (a0 >= n) return;
+  int a = a0 + lane;
+  int cnt = a < n ? bc_len[a] : 0;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int b0 = 0; b0 < total; b0 += 32) {
+    int t = b0 + lane;
+    int q = warp_find(incl, t);
+    int excl_q = __shfl_sync(0xffffffffu, incl - cnt, q);
+    if (t >= total) continue;
+    int s = a0 + q, k = t - excl_q;
+    int64_t slot = (int64_t)s * cand_cap + k;
+    int j = bc[slot];
+    double4 xi = spos[s], xj = spos[j];
+    double dx = min_image(__dsub_rn(xj.x, xi.x), g.L[0]);
+    double dy = min_image(__dsub_rn(xj.y, xi.y), g.L[1]);
+    double dz = min_image(__dsub_rn(xj.z, xi.z), g.L[2]);
+    double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    bool keep = false;
+    double4 v = make_double4(0, 0, 0, 0);
+    if (r2 <= rb2) {
+      v = bo_raw(__dsqrt_rn(r2), sbo[stype[s] * nt + stype[j]]);
+      keep = v.w >= bo_cut;
+    }
+    if (keep) {
+      bc_raw[slot] = v;
+      atomicAdd(&bdeg[s], 1);
+      atomicAdd(&bdeg[j], 1);
+    } else {
+      bc[slot] = -1;
+    }
+  }
+}
+
+// full list fill: each kept half bond reserves one slot in row i and one in
+// row j (the paper's "critical region only includes the reservation of a
+// slot", as an atomic decrement); bdeg returns to zero.  The
+// sort key (original partner index) is stored beside each entry.
+__global__ void k_bond_fill(int n, const int* __restrict__ bc, const int* __restrict__ bc_len,
+                            const double4* __restrict__ bc_raw, int cand_cap, const int* __restrict__ brow,
+                            const int* __restrict__ perm, int* __restrict__ bdeg, int* __restrict__ bcol,
+                            int* __restrict__ bkey, double* __restrict__ bo, long long bond_cap, Status* st) {
+  const int lane = threadIdx.x & 31;
+  const int a0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->bonds = brow[n];
+  if (a0 >= n) return;
+  int a = a0 + lane;
+  int cnt = a < n ? bc_len[a] : 0;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int b0 = 0; b0 < total; b0 += 32) {
+    int t = b0 + lane;
+    int q = warp_find(incl, t);
+    int excl_q = __shfl_sync(0xffffffffu, incl - cnt, q);
+    if (t >= total) continue;
+    int s = a0 + q;
+    int64_t slot = (int64_t)s * cand_cap + (t - excl_q);
+    int j = bc[slot];
+    if (j < 0) continue;
+    double4 v = bc_raw[slot];
+    long long e1 = (long long)brow[s] + atomicSub(&bdeg[s], 1) - 1;
+    long long e2 = (long long)brow[j] + atomicSub(&bdeg[j], 1) - 1;
+    // each side independently: every entry below the capacity is written
+    if (e1 < bond_cap) {
+      bcol[e1] = j;
+      bkey[e1] = perm[j];
+      double* p1 = bo + 8 * e1;
+      p1[0] = v.x; p1[1] = v.y; p1[2] = v.z; p1[3] = v.w;
+    }
+    if (e2 < bond_cap) {
+      bcol[e2] = s;
+      bkey[e2] = perm[s];
+      double* p2 = bo + 8 * e2;
+      p2[0] = v.x; p2[1] = v.y; p2[2] = v.z; p2[3] = v.w;
+    }
+    if (e1 >= bond_cap || e2 >= bond_cap) set_flag(st, ST_BOND_OVF);
+  }
+}
+
+// a5 (B3): each row sorted by original partner index (entries staged in
+// local memory, so the loads are independent), then Delta' = sum BO' - Val
+// in that order; the row owner is recorded per entry for k_bond_correct.
+constexpr int ROW_STAGE = 24;
+__global__ void k_bond_sort_delta(int n, const int* __restrict__ brow, const int* __restrict__ stype,
+                                  const DevParams* __restrict__ prm, int* __restrict__ bcol, int* __restrict__ bkey,
+                                  int* __restrict__ bown, double* __restrict__ bo, double2* __restrict__ delta,
+                                  long long bond_cap) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  int a = brow[s], b = brow[s + 1];
+  if (b > bond_cap) b = (int)bond_cap;
+  int d = b - a;
+  double sum = 0.0;
+  if (d > 0 && d <= ROW_STAGE) {
+    int key[ROW_STAGE], col[ROW_STAGE];
+    double4 v[ROW_STAGE];
+    for (int e = 0; e < d; ++e) {
+      key[e] = bkey[a + e];
+      col[e] = bcol[a + e];
+      const double* p = bo + 8 * (int64_t)(a + e);
+      v[e] = make_double4(p[0], p[1], p[2], p[3]);
+    }
+    for (int e = 0; e < d; ++e) {  // rank of each entry (keys are distinct)
+      int rank = 0;
+      for (int f = 0; f < d; ++f) rank += key[f] < key[e];
+      int o = a + rank;
+      bcol[o] = col[e];
+      bkey[o] = key[e];
+      bown[o] = s;
+      double* p = bo + 8 * (int64_t)o;
+      p[0] = v[e].x; p[1] = v[e].y; p[2] = v[e].z; p[3] = v[e].w;
+    }
+    for (int e = a; e < b; ++e) sum += bo[8 * (int64_t)e + 3];  // ascending partner order
+  } else if (d > ROW_STAGE) {  // rare: in-place insertion sort
+    for (int i = a + 1; i < b; ++i) {
+      int kv = bkey[i], cv = bcol[i];
+      double r0 = bo[8 * (int64_t)i], r1 = bo[8 * (int64_t)i + 1], r2 = bo[8 * (int64_t)i + 2], r3 = bo[8 * (int64_t)i + 3];
+      int j = i - 1;
+      while (j >= a && bkey[j] > kv) {
+        bkey[j + 1] = bkey[j];
+        bcol[j + 1] = bcol[j];
+        for (int q = 0; q < 4; ++q) bo[8 * (int64_t)(j + 1) + q] = bo[8 * (int64_t)j + q];
+        --j;
+      }
+      bkey[j + 1] = kv; bcol[j + 1] = cv;
+      bo[8 * (int64_t)(j + 1)] = r0; bo[8 * (int64_t)(j + 1) + 1] = r1;
+      bo[8 * (int64_t)(j + 1) + 2] = r2; bo[8 * (int64_t)(j + 1) + 3] = r3;
+    }
+    for (int e = a; e < b; ++e) {
+      bown[e] = s;
+      sum += bo[8 * (int64_t)e + 3];
+    }
+  }
+  int t = stype[s];
+  delta[s] = make_double2(sum - prm->val[t], sum - prm->val_boc[t]);
+}
+
+// a6 (B4-B8): one thread per full entry: mirror index and corrected bond
+// orders in canonical orientation (smaller original index first), so
+// BO_ij == BO_ji bitwise.
+__global__ void k_bond_correct(const int* __restrict__ brow, const int* __restrict__ perm,
+                               const int* __restrict__ stype, const DevParams* __restrict__ prm,
+                               const int* __restrict__ bcol, const int* __restrict__ bkey, const int* __restrict__ bown,
+                               int* __restrict__ bmir, double* __restrict__ bo, const double2* __restrict__ delta,
+                               long long bond_cap, const Status* __restrict__ st) {
+  __shared__ BOPair sbo[NTP_MAX];
+  __shared__ double sval[NT_MAX];
+  const int nt = prm->nt;
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) sbo[t] = prm->bo[t];
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) sval[t] = prm->val[t];
+  __syncthreads();
+  long long B = st->bonds < bond_cap ? st->bonds : bond_cap;
+  const double p1 = prm->p_boc1, p2 = prm->p_boc2, inv_p2 = 1.0 / p2;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
+    int s = bown[e];
+    int j = bcol[e];
+    int os = perm[s];
+    int em = -1;
+    for (int f = brow[j], fb = brow[j + 1]; f < fb && f < bond_cap; ++f)
+      if (bkey[f] == os) { em = f; break; }
+    bmir[e] = em;
+    bool first = os < bkey[e];
+    int ia = first ? s : j, ib = first ? j : s;
+    int ta = stype[ia], tb = stype[ib];
+    double2 da = delta[ia], db = delta[ib];
+    const BOPair& c = sbo[ta * nt + tb];
+    double* q = bo + 8 * e;
+    double bpi = q[1], bpp = q[2], bp = q[3];
+    double f2 = exp(-p1 * da.x) + exp(-p1 * db.x);
+    double f3 = -inv_p2 * log(0.5 * (exp(-p2 * da.x) + exp(-p2 * db.x)));
+    double va = sval[ta], vb = sval[tb];
+    double f1 = 0.5 * ((va + f2) / (va + f2 + f3) + (vb + f2) / (vb + f2 + f3));
+    double bb = c.pboc4 * bp * bp;
+    double f4 = 1.0 / (1.0 + exp(-c.pboc3 * (bb - da.y) + c.pboc5));
+    double f5 = 1.0 / (1.0 + exp(-c.pboc3 * (bb - db.y) + c.pboc5));
+    double f145 = f1 * f4 * f5;
+    double BO = bp * f145;
+    double BOpi = bpi * f1 * f145;
+    double BOpp = bpp * f1 * f145;
+    q[4] = BO;
+    q[5] = BO - BOpi - BOpp;
+    q[6] = BOpi;
+    q[7] = BOpp;
+  }
+}
+
+// ====================================================== a7-a8 nonbonded
+__global__ void k_nb_prep(int n, const double* __restrict__ q, const int* __restrict__ perm, double4* __restrict__ spos,
+                          double* __restrict__ sfx, double* __restrict__ sfy, double* __restrict__ sfz, Status* st) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double qs = q[perm[s]];
+  if (!isfinite(qs)) set_flag(st, ST_NONFINITE_IN);
+  spos[s].w = qs;
+  sfx[s] = 0.0;
+  sfy[s] = 0.0;
+  sfz[s] = 0.0;
+}
+
+struct NBConst {
+  double invR, p, inv_p, C;
+};
+
+// ---- branch-free fp64 math for the nonbonded pair (inputs in known, finite,
+// normal ranges; ~1-2 ulp).  Tables live in shared memory.
+constexpr int EXP_TBL = 64;    // 2^(j/64)
+constexpr int LOG_TBL = 128;   // {1/c_j, -log(1/c_j)}, c_j = 1 + (j + 1/2)/128
+
+// e^x for |x| < 700: x = k ln2/64 + r, |r| <= ln2/128; e^r - 1 by a degree-5
+// polynomial (error r^6/720 < 4e-17); 2^(k/64) = 2^(k>>6) * T[k & 63].
+__device__ __forceinline__ double fexp(double x, const double* __restrict__ T) {
+  const double L2E64 = 0x1.71547652b82fep+6;          // 64 / ln 2
+  const double SHIFT = 6755399441055744.0;             // 1.5 * 2^52
+  const double LN2_64_HI = 0x1.62e42fee00000p-7; // ln2_hi / 64 (fdlibm split)
+  const double LN2_64_LO = 0x1.a39ef35793c76p-39; // ln2_lo / 64
+  double t = fma(x, L2E64, SHIFT);
+  double kd = t - SHIFT;
+  int k = __double2loint(t);
+  double r = fma(kd, -LN2_64_HI, x);
+  r = fma(kd, -LN2_64_LO, r);
+  double q = fma(fma(fma(r, 1.0 / 120.0, 1.0 / 24.0), r, 1.0 / 6.0), r, 0.5);
+  double p = fma(q, r * r, r);
+  double tj = T[k & (EXP_TBL - 1)];
+  double y = fma(tj, p, tj);
+  return __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
+}
+
+// ln x for finite normal x > 0: x = 2^e m, m in [1,2); m/c_j = 1 + r with
+// |r| < 2^-8; log1p(r) by a degree-6 polynomial (error < 3e-18).
+__device__ __forceinline__ double flog(double x, const double2* __restrict__ LT) {
+  const double LN2_HI = 0x1.62e42fee00000p-1;
+  const double LN2_LO = 0x1.a39ef35793c76p-33;
+  int hi = __double2hiint(x);
+  int e = (hi >> 20) - 1023;
+  int j = (hi >> 13) & (LOG_TBL - 1);
+  double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(x));
+  double2 t = LT[j];
+  double r = fma(m, t.x, -1.0);
+  double q = fma(fma(fma(fma(r, -1.0 / 6.0, 1.0 / 5.0), r, -0.25), r, 1.0 / 3.0), r, -0.5);
+  double p = fma(q, r * r, r);
+  double ed = (double)e;
+  return fma(ed, LN2_HI, t.y) + fma(ed, LN2_LO, p);
+}
+
+// approximate seeds from the MUFU unit, then one Halley-type correction:
+// (1-e)^(-1/2) = 1 + e/2 + 3e^2/8 + ..., (1-e)^(-1/3) = 1 + e/3 + 2e^2/9 + ...,
+// 1/(1-e) = 1 + e + e^2: relative error ~ (2^-22)^3
+__device__ __forceinline__ double frsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x * y, y, 1.0);
+  return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+__device__ __forceinline__ double frcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  return fma(y * e, 1.0 + e, y);
+}
+__device__ __forceinline__ double frcbrt(double x) {
+  float xf = (float)x, yf;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(xf));
+  yf *= -1.0f / 3.0f;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(yf));
+  double y = (double)yf;
+  double e = fma(-x * y, y * y, 1.0);
+  return fma(y * e, fma(e, 2.0 / 9.0, 1.0 / 3.0), y);
+}
+
+// device self-test of the nonbonded math (tests/test_math_gpu.py)
+__global__ void k_selftest_math(int n, const double* __restrict__ x, double* __restrict__ out,
+                                const DevParams* __restrict__ prm) {
+  __shared__ double ET[EXP_TBL];
+  __shared__ double2 LT[LOG_TBL];
+  for (int t = threadIdx.x; t < EXP_TBL; t += blockDim.x) ET[t] = prm->exp_tbl[t];
+  for (int t = threadIdx.x; t < LOG_TBL; t += blockDim.x) LT[t] = make_double2(prm->log_tbl[2 * t], prm->log_tbl[2 * t + 1]);
+  __syncthreads();
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = x[i];
+  out[5 * (int64_t)i + 0] = fexp(v, ET);
+  out[5 * (int64_t)i + 1] = v > 0 ? flog(v, LT) : 0.0;
+  out[5 * (int64_t)i + 2] = v > 0 ? frsqrt(v) : 0.0;
+  out[5 * (int64_t)i + 3] = v > 0 ? frcp(v) : 0.0;
+  out[5 * (int64_t)i + 4] = v > 0 ? frcbrt(v) : 0.0;
+}
+
+// One Alg. 2 pair (N1-N5): tapered shielded vdW + Coulomb; returns energies
+// and g = (dE/dr)/r so that F_i += g d, F_j -= g d.
+__device__ __forceinline__ void nb_pair(double r2, double qiqj, const NBPair& c, const NBConst& k,
+                                        const double* __restrict__ ET, const double2* __restrict__ LT,
+                                        double& ev, double& ec, double& g) {
+  double rinv = frsqrt(r2);
+  double r = r2 * rinv;
+  // N1 taper: 1 + x^4 (-35 + x (84 + x (-70 + 20 x))), dTap/dr = -140 x^3 (1-x)^3 / R
+  double x = r * k.invR;
+  double x2 = x * x, x3 = x2 * x;
+  double tap = fma(x2 * x2, fma(x, fma(x, fma(x, 20.0, -70.0), 84.0), -35.0), 1.0);
+  double omx = 1.0 - x;
+  double dtap = (-140.0 * k.invR) * x3 * (omx * omx * omx);
+  // N2-N4 shielded vdW: r^p = exp(p ln r), f13 = (r^p + gw^-p)^(1/p)
+  double lr = 0.5 * flog(r2, LT);
+  double rp = fexp(k.p * lr, ET);
+  double sv = rp + c.gwmp;
+  double f13 = fexp(flog(sv, LT) * k.inv_p, ET);
+  double u = fma(-f13, c.inv_rvdw, 1.0);
+  double e2 = fexp(c.ahalf * u, ET);      // e^{alpha u / 2}
+  double e1 = e2 * e2;                    // e^{alpha u}
+  double evu = c.D * fma(-2.0, e2, e1);
+  // d f13/dr = sv^(1/p - 1) r^(p-1) = (f13 / sv) (r^p / r)
+  double df13 = (f13 * frcp(sv)) * (rp * rinv);
+  double devu = -c.Dadr * (e1 - e2) * df13;
+  // N5 shielded Coulomb: S^(-1/3), S = r^3 + gamma^-3; S^(-4/3) = (S^(-1/3))^4
+  double S = fma(r2, r, c.g3);
+  double cb = frcbrt(S);
+  double cb2 = cb * cb;
+  double ecu = qiqj * cb;
+  double decu = -qiqj * r2 * (cb2 * cb2);
+  ev = tap * evu;
+  ec = tap * ecu;
+  double dE = fma(dtap, evu + ecu, tap * (devu + decu));
+  g = dE * rinv;
+}
+
+constexpr int NB_THREADS = 256;
+
+struct NBSmem {
+  WinSmem W;
+  double red[2][NB_THREADS / 32];
+};
+
+// One CTA per home block (Alg. 2, re-designed): a warp per
+// row i streams its half-list entries (lanes over j); F_i stays in registers
+// and is warp-reduced once per row; F_j is accumulated in a shared-memory
+// window (the block's private force array, the GPU form of the paper's
+// thread-private tprivForce) and flushed to the global sorted force array
+// once per block.  Energies: per-block partials reduced later in fixed order.
+__global__ void __launch_bounds__(NB_THREADS, 3) k_nonbonded(Grid g, const int* __restrict__ cell_start,
+    const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
+    const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
+    double* __restrict__ sfx, double* __restrict__ sfy, double* __restrict__ sfz, double* __restrict__ epart,
+    int nsplit, Status* st) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ NBSmem S;
+  const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
+  const int nt = prm->nt;
+  double* ET = reinterpret_cast<double*>(dyn);                  // exp table
+  double2* LT = reinterpret_cast<double2*>(ET + EXP_TBL);       // log table
+  NBPair* pc = reinterpret_cast<NBPair*>(LT + LOG_TBL);         // nt*nt pair constants
+  double* fx = reinterpret_cast<double*>(pc + nt * nt);        // F window (block-private force array)
+  double* fy = fx + window_cap;
+  double* fz = fy + window_cap;
+  int* slot_j = reinterpret_cast<int*>(fz + window_cap);       // slot -> sorted atom
+  unsigned char* slot_k = reinterpret_cast<unsigned char*>(slot_j + window_cap);  // slot -> window cell
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) pc[t] = prm->nb[t];
+  for (int t = threadIdx.x; t < EXP_TBL; t += blockDim.x) ET[t] = prm->exp_tbl[t];
+  for (int t = threadIdx.x; t < LOG_TBL; t += blockDim.x) LT[t] = make_double2(prm->log_tbl[2 * t], prm->log_tbl[2 * t + 1]);
+  NBConst kc;
+  kc.invR = prm->invR; kc.p = prm->p_vdw; kc.inv_p = prm->inv_p; kc.C = prm->C;
+  int W = build_window(S.W, blk, g, cell_start);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  if (W > window_cap) {
+    if (threadIdx.x == 0) {
+      set_flag(st, ST_WIN_OVF);
+      atomicMax(&st->max_window, W);
+      epart[2 * blockIdx.x] = 0.0;
+      epart[2 * blockIdx.x + 1] = 0.0;
+    }
+    return;
+  }
+  const int nwu = c_win.nwu;
+  for (int k = warp; k < nwu; k += nwarp) {
+    int s0 = S.W.start[k], c = S.W.cnt[k], b0 = S.W.slot[k];
+    for (int a = lane; a < c; a += 32) {
+      slot_j[b0 + a] = s0 + a;
+      slot_k[b0 + a] = (unsigned char)k;
+    }
+  }
+  for (int t = threadIdx.x; t < W; t += blockDim.x) {
+    fx[t] = 0.0; fy[t] = 0.0; fz[t] = 0.0;
+  }
+  __syncthreads();
+  double ev_acc = 0.0, ec_acc = 0.0;
+  for (int r = split * nwarp + warp;; r += nsplit * nwarp) {
+    int h, si;
+    if (!row_of(S.W, r, h, si)) break;
+    const int s = slot_j[si];
+    const double4 xi = spos[s];
+    const int ti = stype[s];
+    const double cqi = kc.C * xi.w;
+    const int len = nbr_len[s];
+    const uint16_t* row = nbr + (int64_t)s * row_cap;
+    double fix = 0.0, fiy = 0.0, fiz = 0.0;
+    for (int b0 = 0; b0 < len; b0 += 32) {
+      int e = b0 + lane;
+      if (e < len) {
+        int slot = row[e];
+        int j = slot_j[slot];
+        int k = slot_k[slot];
+        double4 xj = spos[j];
+        int tj = stype[j];
+        double dx = (xj.x - xi.x) + S.W.shift[k][0];
+        double dy = (xj.y - xi.y) + S.W.shift[k][1];
+        double dz = (xj.z - xi.z) + S.W.shift[k][2];
+        double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double ev, ec, gg;
+        nb_pair(r2, cqi * xj.w, pc[ti * nt + tj], kc, ET, LT, ev, ec, gg);
+        ev_acc += ev;
+        ec_acc += ec;
+        double gx = gg * dx, gy = gg * dy, gz = gg * dz;
+        fix += gx; fiy += gy; fiz += gz;
+        atomicAdd(&fx[slot], -gx);
+        atomicAdd(&fy[slot], -gy);
+        atomicAdd(&fz[slot], -gz);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      fix += __shfl_xor_sync(0xffffffffu, fix, o);
+      fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
+      fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&fx[si], fix);
+      atomicAdd(&fy[si], fiy);
+      atomicAdd(&fz[si], fiz);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < W; t += blockDim.x) {
+    double a = fx[t], b = fy[t], c = fz[t];
+    if (a != 0.0 || b != 0.0 || c != 0.0) {
+      int j = slot_j[t];
+      atomicAdd(&sfx[j], a);
+      atomicAdd(&sfy[j], b);
+      atomicAdd(&sfz[j], c);
+    }
+  }
+  // deterministic block energy partial
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ev_acc += __shfl_xor_sync(0xffffffffu, ev_acc, o);
+    ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
+  }
+  if (lane == 0) {
+    S.red[0][warp] = ev_acc;
+    S.red[1][warp] = ec_acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < nwarp; ++w) { a += S.red[0][w]; b += S.red[1][w]; }
+    epart[2 * blockIdx.x] = a;
+    epart[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// un-permute: force[i] = F_sorted[iperm[i]]
+__global__ void k_finalize_forces(int n, const int* __restrict__ iperm, const double* __restrict__ sfx,
+                                  const double* __restrict__ sfy, const double* __restrict__ sfz,
+                                  double* __restrict__ force, Status* st) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int s = iperm[i];
+  double a = sfx[s], b = sfy[s], c = sfz[s];
+  if (!(isfinite(a) && isfinite(b) && isfinite(c))) set_flag(st, ST_NONFINITE_OUT);
+  force[3 * (int64_t)i] = a;
+  force[3 * (int64_t)i + 1] = b;
+  force[3 * (int64_t)i + 2] = c;
+}
+
+// fixed-order energy reduction over block partials (one CTA)
+constexpr int FIN_THREADS = 1024;
+__global__ void __launch_bounds__(FIN_THREADS) k_finalize_energy(int nblock, const double* __restrict__ epart,
+                                                                 double* __restrict__ energy, Status* st) {
+  __shared__ double red[2][FIN_THREADS / 32];
+  double a = 0.0, b = 0.0;
+  for (int t = threadIdx.x; t < nblock; t += FIN_THREADS) {
+    a += epart[2 * t];
+    b += epart[2 * t + 1];
+  }
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) { red[0][w] = a; red[1][w] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < FIN_THREADS / 32; ++k) { x += red[0][k]; y += red[1][k]; }
+    energy[0] = x;
+    energy[1] = y;
+    if (!(isfinite(x) && isfinite(y))) set_flag(st, ST_NONFINITE_OUT);
+  }
+}
+
+// ================================================================= export
+__device__ __forceinline__ uint64_t mix64(uint64_t a, uint64_t b) {
+  uint64_t z = (a << 32) ^ b;
+  z ^= z >> 33; z *= 0xff51afd7ed558ccdull;
+  z ^= z >> 33; z *= 0xc4ceb9fe1a85ec53ull;
+  z ^= z >> 33;
+  return z;
+}
+
+// mode 0: write pairs at exp_off[s] + e;  mode 1: per-atom count / digest
+__global__ void __launch_bounds__(NBR_THREADS) k_export_pairs(Grid g, const int* __restrict__ cell_start,
+    const int* __restrict__ perm, const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap,
+    int window_cap, const long long* __restrict__ off, int mode, int* __restrict__ pi, int* __restrict__ pj,
+    unsigned long long* __restrict__ cnt, unsigned long long* __restrict__ dig) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ WinSmem W;
+  int* slot_j = reinterpret_cast<int*>(dyn);
+  int nW = build_window(W, blockIdx.x, g, cell_start);
+  if (nW > window_cap) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int k = warp; k < c_win.nwu; k += nwarp)
+    for (int a = lane; a < W.cnt[k]; a += 32) slot_j[W.slot[k] + a] = W.start[k] + a;
+  __syncthreads();
+  for (int r = warp;; r += nwarp) {
+    int h, si;
+    if (!row_of(W, r, h, si)) break;
+    int s = slot_j[si];
+    int len = nbr_len[s];
+    int oi = perm[s];
+    for (int e = lane; e < len; e += 32) {
+      int oj = perm[slot_j[nbr[(int64_t)s * row_cap + e]]];
+      int a = oi < oj ? oi : oj, b = oi < oj ? oj : oi;
+      if (mode == 0) {
+        long long o = off[s] + e;
+        pi[o] = a;
+        pj[o] = b;
+      } else {
+        unsigned long long hsh = mix64((uint64_t)a, (uint64_t)b);
+        atomicAdd(&cnt[a], 1ull); atomicAdd(&cnt[b], 1ull);
+        atomicAdd(&dig[a], hsh); atomicAdd(&dig[b], hsh);
+      }
+    }
+  }
+}
+
+__global__ void k_export_bond_deg(int n, const int* __restrict__ iperm, const int* __restrict__ brow, int* __restrict__ deg) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int s = iperm[i];
+  deg[i] = brow[s + 1] - brow[s];
+}
+
+__global__ void k_export_bonds(int n, const int* __restrict__ iperm, const int* __restrict__ perm,
+                               const int* __restrict__ brow, const int* __restrict__ bcol, const int* __restrict__ bmir,
+                               const double* __restrict__ bo, const double2* __restrict__ delta,
+                               const long long* __restrict__ orow, int64_t* __restrict__ out_row, int* __restrict__ out_col,
+                               int* __restrict__ out_mir, double* __restrict__ out_bo, double* __restrict__ out_delta) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (out_row) out_row[i] = orow[i];
+  if (i == n) return;
+  int s = iperm[i];
+  long long o0 = orow[i];
+  for (int e = brow[s]; e < brow[s + 1]; ++e) {
+    long long o = o0 + (e - brow[s]);
+    int j = bcol[e];
+    if (out_col) out_col[o] = perm[j];
+    if (out_mir) {
+      int em = bmir[e];
+      out_mir[o] = (int)(orow[perm[j]] + (em - brow[j]));
+    }
+    if (out_bo)
+      for (int q = 0; q < 8; ++q) out_bo[8 * o + q] = bo[8 * (int64_t)e + q];
+  }
+  if (out_delta) {
+    out_delta[2 * (int64_t)i] = delta[s].x;
+    out_delta[2 * (int64_t)i + 1] = delta[s].y;
+  }
+}
+
+}  // namespace rx

@@ -1,0 +1,918 @@
+// libreax: C ABI + host orchestration of the B200 ReaxFF hot path.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared -Xcompiler -fPIC
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/reax.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace rx;
+
+namespace {
+
+constexpr size_t ALIGN = 256;
+constexpr int MAX_SPLIT = 8;
+// CTAs per home block for the window kernels: small systems (c0/c1) have too
+// few home blocks to fill 148 SMs, so each block's rows are split over
+// several CTAs (each builds the same window)
+int choose_split(int nblock) {
+  int target = 148 * 8;
+  int s = (target + nblock - 1) / std::max(nblock, 1);
+  return std::max(1, std::min(MAX_SPLIT, s));
+}
+constexpr int TPB = 256;
+
+inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
+inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+// ------------------------------------------------------------ window tables
+bool forward_offset(int ox, int oy, int oz) {
+  return oz > 0 || (oz == 0 && (oy > 0 || (oy == 0 && ox > 0)));
+}
+
+WindowTables make_tables() {
+  WindowTables T;
+  memset(&T, 0, sizeof(T));
+  bool used[NWB] = {false};
+  for (int h = 0; h < NHOME; ++h) {
+    int hv[3] = {h % HB, (h / HB) % HB, h / (HB * HB)};
+    for (int oz = -SR; oz <= SR; ++oz)
+      for (int oy = -SR; oy <= SR; ++oy)
+        for (int ox = -SR; ox <= SR; ++ox) {
+          if (!(forward_offset(ox, oy, oz) || (ox == 0 && oy == 0 && oz == 0))) continue;
+          int w = (hv[0] + SR + ox) + WB * ((hv[1] + SR + oy) + WB * (hv[2] + SR + oz));
+          used[w] = true;
+        }
+  }
+  T.nwu = 0;
+  for (int w = 0; w < NWB; ++w) {
+    T.widx[w] = -1;
+    if (used[w]) {
+      T.widx[w] = T.nwu;
+      T.wu[T.nwu++] = w;
+    }
+  }
+  for (int h = 0; h < NHOME; ++h) {
+    int hv[3] = {h % HB, (h / HB) % HB, h / (HB * HB)};
+    auto wk = [&](int ox, int oy, int oz) {
+      return T.widx[(hv[0] + SR + ox) + WB * ((hv[1] + SR + oy) + WB * (hv[2] + SR + oz))];
+    };
+    T.home_k[h] = wk(0, 0, 0);
+    std::vector<std::pair<int, int>> runs;
+    for (int oz = 0; oz <= SR; ++oz)
+      for (int oy = -SR; oy <= SR; ++oy) {
+        int oxa = -SR, oxb = SR;
+        if (oz == 0 && oy < 0) continue;
+        if (oz == 0 && oy == 0) oxa = 1;
+        runs.push_back({wk(oxa, oy, oz), wk(oxb, oy, oz)});
+      }
+    std::sort(runs.begin(), runs.end());
+    std::vector<std::pair<int, int>> merged;
+    for (auto& r : runs) {
+      if (!merged.empty() && merged.back().second + 1 == r.first) merged.back().second = r.second;
+      else merged.push_back(r);
+    }
+    T.nrun[h] = (int)merged.size();
+    for (size_t q = 0; q < merged.size(); ++q) {
+      T.run_a[h][q] = merged[q].first;
+      T.run_b[h][q] = merged[q].second;
+    }
+  }
+  return T;
+}
+
+std::mutex g_tab_mu;
+bool g_tab_done[64] = {false};
+
+cudaError_t ensure_tables() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  if (dev < 64 && g_tab_done[dev]) return cudaSuccess;
+  WindowTables T = make_tables();
+  e = cudaMemcpyToSymbol(c_win, &T, sizeof(T));
+  if (e == cudaSuccess && dev < 64) g_tab_done[dev] = true;
+  return e;
+}
+
+// ------------------------------------------------------------------- grid
+bool make_grid(const double box[3], double R, Grid& g) {
+  for (int k = 0; k < 3; ++k) {
+    double L = box[k];
+    // sub-cell side strictly >= R/2 with a relative margin, so rounding in
+    // floor(x/h) never separates two atoms within R by more than SR cells
+    int nc = (int)std::floor(L / (0.5 * R * (1.0 + 1e-10)));
+    if (nc < 1) nc = 1;
+    g.nc[k] = nc;
+    g.nb[k] = (nc + HB - 1) / HB;
+    g.L[k] = L;
+    g.h[k] = L / nc;
+    g.inv_h[k] = nc / L;
+  }
+  long long ncell = (long long)g.nc[0] * g.nc[1] * g.nc[2];
+  long long nblock = (long long)g.nb[0] * g.nb[1] * g.nb[2];
+  if (ncell > (1LL << 30)) return false;
+  g.ncell = (int)ncell;
+  g.nblock = (int)nblock;
+  return true;
+}
+
+bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
+
+// --------------------------------------------------------- validation (a1)
+reax_status check_box_cut(const double box[3], const reax_cutoffs* cut) {
+  if (!box || !cut) return REAX_ERR_ARG;
+  if (!(finite_pos(cut->r_nonb) && finite_pos(cut->r_bond))) return REAX_ERR_CUTOFF;
+  if (cut->r_bond > cut->r_nonb) return REAX_ERR_CUTOFF;
+  if (!(cut->bo_cut > 0.0 && cut->bo_cut < 1.0)) return REAX_ERR_CUTOFF;
+  for (int k = 0; k < 3; ++k) {
+    // strictly greater than 2 r_nonb: every pair within r_nonb then has exactly
+    // one periodic image within r_nonb (reading 18)
+    if (!std::isfinite(box[k]) || !(box[k] > 2.0 * cut->r_nonb)) return REAX_ERR_BOX;
+  }
+  return REAX_OK;
+}
+
+// host copy of B1-B2 for the conservative candidate radius (bisection)
+double host_bo_prime(double r, const reax_params* p, int ti, int tj) {
+  int nt = p->ntypes, tp = ti * nt + tj;
+  double r0s = 0.5 * (p->r_sigma[ti] + p->r_sigma[tj]);
+  double r0p = 0.5 * (p->r_pi[ti] + p->r_pi[tj]);
+  double r0pp = 0.5 * (p->r_pipi[ti] + p->r_pipi[tj]);
+  return std::exp(p->p_bo1[tp] * std::pow(r / r0s, p->p_bo2[tp])) +
+         std::exp(p->p_bo3[tp] * std::pow(r / r0p, p->p_bo4[tp])) +
+         std::exp(p->p_bo5[tp] * std::pow(r / r0pp, p->p_bo6[tp]));
+}
+
+reax_status build_params(const reax_params* p, const reax_cutoffs* cut, DevParams& d) {
+  if (!p) return REAX_ERR_ARG;
+  int nt = p->ntypes;
+  if (nt < 1 || nt > REAX_MAX_TYPES) return REAX_ERR_PARAM;
+  const double* per_type[] = {p->r_sigma, p->r_pi, p->r_pipi, p->gamma, p->r_vdw, p->eps, p->alpha,
+                              p->gamma_w, p->b131, p->b132, p->b133, p->val, p->val_boc};
+  for (auto a : per_type) {
+    if (!a) return REAX_ERR_ARG;
+    for (int t = 0; t < nt; ++t)
+      if (!std::isfinite(a[t])) return REAX_ERR_PARAM;
+  }
+  const double* per_pair[] = {p->p_bo1, p->p_bo2, p->p_bo3, p->p_bo4, p->p_bo5, p->p_bo6, p->De};
+  for (auto a : per_pair) {
+    if (!a) return REAX_ERR_ARG;
+    for (int t = 0; t < nt * nt; ++t) {
+      if (!std::isfinite(a[t])) return REAX_ERR_PARAM;
+      if (a[t] != a[(t % nt) * nt + t / nt]) return REAX_ERR_PARAM;  // symmetric
+    }
+  }
+  for (int t = 0; t < nt; ++t) {
+    if (!(p->r_sigma[t] > 0 && p->r_pi[t] > 0 && p->r_pipi[t] > 0 && p->gamma[t] > 0 && p->r_vdw[t] > 0 &&
+          p->eps[t] >= 0 && p->alpha[t] >= 0 && p->gamma_w[t] > 0 && p->b131[t] >= 0 && p->b132[t] >= 0 &&
+          p->b133[t] >= 0 && p->val[t] > 0))
+      return REAX_ERR_PARAM;
+  }
+  if (!(std::isfinite(p->p_boc1) && std::isfinite(p->p_boc2) && p->p_boc2 != 0.0 && p->p_vdw1 > 0 &&
+        std::isfinite(p->p_vdw1) && std::isfinite(p->coulomb_c)))
+    return REAX_ERR_PARAM;
+  memset(&d, 0, sizeof(d));
+  d.nt = nt;
+  d.R = cut->r_nonb;
+  d.R2 = cut->r_nonb * cut->r_nonb;
+  d.rb2 = cut->r_bond * cut->r_bond;
+  d.bo_cut = cut->bo_cut;
+  d.p_vdw = p->p_vdw1;
+  d.inv_p = 1.0 / p->p_vdw1;
+  d.invR = 1.0 / cut->r_nonb;
+  d.C = p->coulomb_c;
+  d.p_boc1 = p->p_boc1;
+  d.p_boc2 = p->p_boc2;
+  // fp32 band: the fp32 r^2 error is < 3e-4 A^2 for |d| < 16 A;
+  // the band is +-0.02 A^2 (scaled with R^2 for other cutoffs)
+  double m = 0.02 * (d.R2 / 100.0);
+  d.R2lo = (float)(d.R2 - m);
+  d.R2hi = (float)(d.R2 + m);
+  d.rcand2_max = -1.0f;
+  for (int t = 0; t < nt; ++t) {
+    d.val[t] = p->val[t];
+    d.val_boc[t] = p->val_boc[t];
+  }
+  // tables of the nonbonded's exp/log (x86 long double: 64-bit mantissa)
+  for (int j = 0; j < 64; ++j) d.exp_tbl[j] = (double)exp2l((long double)j / 64.0L);
+  for (int j = 0; j < 128; ++j) {
+    long double cj = 1.0L + ((long double)j + 0.5L) / 128.0L;
+    double inv = (double)(1.0L / cj);
+    d.log_tbl[2 * j] = inv;
+    d.log_tbl[2 * j + 1] = (double)(-logl((long double)inv));
+  }
+  for (int a = 0; a < nt; ++a)
+    for (int b = 0; b < nt; ++b) {
+      int tp = a * nt + b;
+      NBPair& c = d.nb[tp];
+      double D = std::sqrt(p->eps[a] * p->eps[b]);
+      double alpha = std::sqrt(p->alpha[a] * p->alpha[b]);
+      double rvdw = 2.0 * std::sqrt(p->r_vdw[a] * p->r_vdw[b]);
+      double gw = std::sqrt(p->gamma_w[a] * p->gamma_w[b]);
+      double g = std::sqrt(p->gamma[a] * p->gamma[b]);
+      c.D = D;
+      c.ahalf = 0.5 * alpha;
+      c.Dadr = D * alpha / rvdw;
+      c.inv_rvdw = 1.0 / rvdw;
+      c.gwmp = std::pow(gw, -p->p_vdw1);
+      c.g3 = 1.0 / (g * g * g);
+      BOPair& o = d.bo[tp];
+      o.lr0[0] = std::log(0.5 * (p->r_sigma[a] + p->r_sigma[b]));
+      o.lr0[1] = std::log(0.5 * (p->r_pi[a] + p->r_pi[b]));
+      o.lr0[2] = std::log(0.5 * (p->r_pipi[a] + p->r_pipi[b]));
+      o.pa[0] = p->p_bo1[tp]; o.pa[1] = p->p_bo3[tp]; o.pa[2] = p->p_bo5[tp];
+      o.pb[0] = p->p_bo2[tp]; o.pb[1] = p->p_bo4[tp]; o.pb[2] = p->p_bo6[tp];
+      o.pboc3 = std::sqrt(p->b132[a] * p->b132[b]);
+      o.pboc4 = std::sqrt(p->b131[a] * p->b131[b]);
+      o.pboc5 = std::sqrt(p->b133[a] * p->b133[b]);
+      // conservative candidate radius: BO' is decreasing in r when p_bo(1,3,5) <= 0
+      // and p_bo(2,4,6) >= 0; otherwise fall back to r_bond
+      bool mono = p->p_bo1[tp] <= 0 && p->p_bo3[tp] <= 0 && p->p_bo5[tp] <= 0 && p->p_bo2[tp] >= 0 &&
+                  p->p_bo4[tp] >= 0 && p->p_bo6[tp] >= 0;
+      double rc = cut->r_bond;
+      if (mono) {
+        double lo = 1e-3, hi = cut->r_bond;
+        if (host_bo_prime(hi, p, a, b) < cut->bo_cut) {
+          if (host_bo_prime(lo, p, a, b) < cut->bo_cut) {
+            rc = 0.0;
+          } else {
+            for (int it = 0; it < 200; ++it) {
+              double mid = 0.5 * (lo + hi);
+              if (host_bo_prime(mid, p, a, b) >= cut->bo_cut) lo = mid; else hi = mid;
+            }
+            rc = std::min(cut->r_bond, hi * (1.0 + 1e-6) + 1e-6);
+          }
+        }
+      }
+      d.rcand2[tp] = rc > 0.0 ? (float)(rc * rc + m) : -1.0f;
+      d.rcand2_max = std::max(d.rcand2_max, d.rcand2[tp]);
+    }
+  return REAX_OK;
+}
+
+// ------------------------------------------------------------ capacities
+void resolve_caps(int64_t n, const double box[3], const reax_cutoffs* cut, const reax_capacity* in,
+                  reax_capacity& c) {
+  reax_capacity z = {0, 0, 0, 0};
+  if (!in) in = &z;
+  double vol = box[0] * box[1] * box[2];
+  double rho = vol > 0 ? (double)n / vol : 0.0;
+  double R = cut->r_nonb;
+  double mean = 2.0 * M_PI / 3.0 * rho * R * R * R;
+  int rc = (int)std::ceil(2.0 * mean + 96.0);
+  rc = (rc + 31) / 32 * 32;
+  c.row_cap = in->row_cap > 0 ? in->row_cap : std::min(rc, 65535);
+  c.cand_cap = in->cand_cap > 0 ? in->cand_cap : 16;
+  c.bond_cap = in->bond_cap > 0 ? in->bond_cap : std::max<int64_t>(8 * n, 64);
+  c.window_cap = in->window_cap > 0 ? in->window_cap : 2048;
+}
+
+struct Layout {
+  size_t off[40];
+  size_t total;
+};
+
+// assigns WS pointers relative to base (base may be null to size)
+size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* w) {
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + std::max<size_t>(bytes, 1));
+    return base ? base + r : nullptr;
+  };
+  size_t N = (size_t)std::max<int64_t>(n, 1);
+  size_t nscan = (size_t)nblk(std::max<int64_t>(std::max<int64_t>(N + 1, (int64_t)g.ncell + 1), 1), SCAN_TILE) + 2;
+  WS t;
+  t.cell_cnt = (int*)take(sizeof(int) * (g.ncell + 1));
+  t.cell_start = (int*)take(sizeof(int) * (g.ncell + 1));
+  t.cell_of = (int*)take(sizeof(int) * N);
+  t.perm = (int*)take(sizeof(int) * N);
+  t.iperm = (int*)take(sizeof(int) * N);
+  t.spos = (double4*)take(sizeof(double4) * N);
+  t.sloc = (float4*)take(sizeof(float4) * N);
+  t.stype = (int*)take(sizeof(int) * N);
+  t.nbr = (uint16_t*)take(sizeof(uint16_t) * N * (size_t)c.row_cap);
+  t.nbr_len = (int*)take(sizeof(int) * N);
+  t.bc = (int*)take(sizeof(int) * N * (size_t)c.cand_cap);
+  t.bc_len = (int*)take(sizeof(int) * N);
+  t.bkey = (int*)take(sizeof(int) * (size_t)c.bond_cap);
+  t.bown = (int*)take(sizeof(int) * (size_t)c.bond_cap);
+  t.bc_raw = (double4*)take(sizeof(double4) * N * (size_t)c.cand_cap);
+  t.bdeg = (int*)take(sizeof(int) * (N + 1));
+  t.brow = (int*)take(sizeof(int) * (N + 1));
+  t.bcol = (int*)take(sizeof(int) * (size_t)c.bond_cap);
+  t.bmir = (int*)take(sizeof(int) * (size_t)c.bond_cap);
+  t.bo = (double*)take(sizeof(double) * 8 * (size_t)c.bond_cap);
+  t.delta = (double2*)take(sizeof(double2) * N);
+  t.sfx = (double*)take(sizeof(double) * N);
+  t.sfy = (double*)take(sizeof(double) * N);
+  t.sfz = (double*)take(sizeof(double) * N);
+  t.epart = (double*)take(sizeof(double) * 2 * MAX_SPLIT * (size_t)std::max(g.nblock, 1));
+  t.scan_tmp = (long long*)take(sizeof(long long) * nscan);
+  t.exp_off = (long long*)take(sizeof(long long) * (N + 1));
+  t.prm = (DevParams*)take(sizeof(DevParams));
+  t.st = (Status*)take(sizeof(Status));
+  t.h_pos = (double*)take(sizeof(double) * 3 * N);
+  t.h_type = (int*)take(sizeof(int) * N);
+  t.h_q = (double*)take(sizeof(double) * N);
+  t.h_force = (double*)take(sizeof(double) * 3 * N);
+  t.h_energy = (double*)take(sizeof(double) * 2);
+  if (w) *w = t;
+  return o;
+}
+
+}  // namespace
+
+// ===================================================================== ctx
+struct reax_ctx {
+  bool bound = false;
+  char* ws_base = nullptr;
+  size_t ws_bytes = 0;
+  WS w{};
+  Grid g{};
+  int64_t n = 0;
+  reax_capacity cap{};
+  reax_cutoffs cut{};
+  // pinned host
+  Status* h_st = nullptr;
+  DevParams* h_prm = nullptr;
+  bool prm_valid = false;  // device copy matches *h_prm
+  std::vector<double> prm_key;  // raw reax_params + cutoffs of the last successful build
+  // state
+  bool lists_ok = false;
+  bool bonds_ok = false;
+  const double* last_pos = nullptr;
+  const int* last_type = nullptr;
+  double last_box[3] = {0, 0, 0};
+  bool async = false;
+  reax_capacity need{};
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending[REAX_NKERNELS];
+  double ms_acc[REAX_NKERNELS] = {0};
+  int64_t launches_acc[REAX_NKERNELS] = {0};
+  int launches_step = 0;
+  int launches_cur = 0;
+  int nsplit = 1;
+};
+
+namespace {
+
+reax_status cuda_err(cudaError_t e) { return e == cudaSuccess ? REAX_OK : REAX_ERR_CUDA; }
+
+cudaEvent_t take_event(reax_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct Timer {
+  reax_ctx* c;
+  int k;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  int l0;
+  Timer(reax_ctx* c_, int k_, cudaStream_t s_) : c(c_), k(k_), s(s_) {
+    l0 = c->launches_cur;
+    if (c->timing) {
+      a = take_event(c);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~Timer() {
+    c->launches_acc[k] += c->launches_cur - l0;
+    if (c->timing) {
+      cudaEvent_t b = take_event(c);
+      cudaEventRecord(b, s);
+      c->ev_pending[k].push_back({a, b});
+    }
+  }
+};
+
+#define LAUNCH(ctx) (++(ctx)->launches_cur)
+
+template <typename TI, typename TO>
+cudaError_t scan(reax_ctx* c, const TI* in, int64_t n, TO* out, cudaStream_t s) {
+  int nparts = nblk(n, SCAN_TILE);
+  if (n <= 0) return cudaMemsetAsync(out, 0, sizeof(TO), s);
+  k_scan_partial<TI><<<nparts, SCAN_THREADS, 0, s>>>(in, n, c->w.scan_tmp);
+  LAUNCH(c);
+  k_scan_top<<<1, SCAN_THREADS, 0, s>>>(c->w.scan_tmp, nparts);
+  LAUNCH(c);
+  k_scan_final<TI, TO><<<nparts, SCAN_THREADS, 0, s>>>(in, n, c->w.scan_tmp, out);
+  LAUNCH(c);
+  return cudaGetLastError();
+}
+
+reax_status read_status(reax_ctx* c, cudaStream_t s, bool sync) {
+  cudaError_t e = cudaMemcpyAsync(c->h_st, c->w.st, sizeof(Status), cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  if (!sync) return REAX_OK;
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  int f = c->h_st->flags;
+  if (f == 0) return REAX_OK;
+  if (f & (ST_ROW_OVF | ST_CAND_OVF | ST_BOND_OVF | ST_WIN_OVF)) {
+    c->need = c->cap;
+    if (f & ST_ROW_OVF) c->need.row_cap = std::max(c->cap.row_cap, (c->h_st->max_row + 32) / 32 * 32);
+    if (f & ST_CAND_OVF) c->need.cand_cap = std::max(c->cap.cand_cap, c->h_st->max_cand + 4);
+    if (f & ST_BOND_OVF) c->need.bond_cap = std::max<int64_t>(c->cap.bond_cap, c->h_st->bonds + 64);
+    if (f & ST_WIN_OVF) c->need.window_cap = std::max(c->cap.window_cap, (c->h_st->max_window + 255) / 256 * 256);
+    c->lists_ok = c->bonds_ok = false;
+    cudaMemsetAsync(c->w.st, 0, sizeof(Status), s);
+    return REAX_ERR_CAPACITY;
+  }
+  cudaMemsetAsync(c->w.st, 0, sizeof(Status), s);
+  if (f & ST_TYPE) { c->lists_ok = c->bonds_ok = false; return REAX_ERR_ARG; }
+  return REAX_ERR_NONFINITE;
+}
+
+// raw parameter values (and cutoffs) as a flat key: rebuilding the tables
+// (incl. the host bisection) only when something changed keeps per-call host
+// cost to a memcmp, and keeps CUDA-graph capture free of synchronisation
+bool params_key(const reax_params* p, const reax_cutoffs* cut, std::vector<double>& k) {
+  if (!p || p->ntypes < 1 || p->ntypes > REAX_MAX_TYPES) return false;
+  int nt = p->ntypes;
+  k.clear();
+  k.push_back(nt);
+  const double* per_type[] = {p->r_sigma, p->r_pi, p->r_pipi, p->gamma, p->r_vdw, p->eps, p->alpha,
+                              p->gamma_w, p->b131, p->b132, p->b133, p->val, p->val_boc};
+  for (auto a : per_type) {
+    if (!a) return false;
+    k.insert(k.end(), a, a + nt);
+  }
+  const double* per_pair[] = {p->p_bo1, p->p_bo2, p->p_bo3, p->p_bo4, p->p_bo5, p->p_bo6, p->De};
+  for (auto a : per_pair) {
+    if (!a) return false;
+    k.insert(k.end(), a, a + nt * nt);
+  }
+  double g[] = {p->p_boc1, p->p_boc2, p->p_vdw1, p->coulomb_c, cut->r_nonb, cut->r_bond, cut->bo_cut};
+  k.insert(k.end(), g, g + 7);
+  return true;
+}
+
+reax_status upload_params(reax_ctx* c, const reax_params* p, const reax_cutoffs* cut, cudaStream_t s) {
+  std::vector<double> key;
+  if (!params_key(p, cut, key)) return p ? REAX_ERR_PARAM : REAX_ERR_ARG;
+  if (c->prm_valid && key.size() == c->prm_key.size() &&
+      memcmp(key.data(), c->prm_key.data(), key.size() * sizeof(double)) == 0)
+    return REAX_OK;
+  DevParams d;
+  reax_status r = build_params(p, cut, d);
+  if (r != REAX_OK) return r;
+  if (c->prm_valid && memcmp(&d, c->h_prm, sizeof(DevParams)) == 0) return REAX_OK;
+  // the pinned staging buffer may still be read by an earlier async copy
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  memcpy(c->h_prm, &d, sizeof(DevParams));
+  e = cudaMemcpyAsync(c->w.prm, c->h_prm, sizeof(DevParams), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  c->prm_valid = true;
+  c->prm_key.swap(key);
+  return REAX_OK;
+}
+
+size_t nbr_smem(int wcap) { return (size_t)wcap * (sizeof(float4) + sizeof(int) + 1) + 64; }
+size_t nb_smem(int wcap, int nt = NT_MAX) { return sizeof(double) * (EXP_TBL + 2 * LOG_TBL) + sizeof(NBPair) * nt * nt + (size_t)wcap * (3 * sizeof(double) + sizeof(int) + 1) + 64; }
+size_t exp_smem(int wcap) { return (size_t)wcap * sizeof(int) + 64; }
+
+reax_status check_common(reax_ctx* c, int64_t n, const double box[3], const reax_cutoffs* cut) {
+  if (!c) return REAX_ERR_ARG;
+  if (!c->bound) return REAX_ERR_STATE;
+  reax_status r = check_box_cut(box, cut);
+  if (r != REAX_OK) return r;
+  if (n != c->n) return REAX_ERR_STATE;
+  if (cut->r_nonb != c->cut.r_nonb) return REAX_ERR_STATE;
+  Grid g;
+  if (!make_grid(box, cut->r_nonb, g)) return REAX_ERR_BOX;
+  for (int k = 0; k < 3; ++k)
+    if (g.nc[k] != c->g.nc[k]) return REAX_ERR_STATE;
+  c->g = g;  // same topology; box lengths may differ slightly
+  return REAX_OK;
+}
+
+reax_status do_build_lists(reax_ctx* c, int64_t n, const double* pos, const int* type, const double box[3],
+                           const reax_params* prm, const reax_cutoffs* cut, cudaStream_t s) {
+  reax_status r = check_common(c, n, box, cut);
+  if (r != REAX_OK) return r;
+  if (n > 0 && (!pos || !type)) return REAX_ERR_ARG;
+  r = upload_params(c, prm, cut, s);
+  if (r != REAX_OK) return r;
+  c->cut = *cut;
+  c->lists_ok = c->bonds_ok = false;
+  const Grid& g = c->g;
+  WS& w = c->w;
+  int N = (int)n;
+  if (N > 0) {
+    {
+      Timer t(c, 0, s);
+      k_bin<<<nblk(N, TPB), TPB, 0, s>>>(N, pos, type, g, prm->ntypes, w.cell_of, w.cell_cnt, w.st);
+      LAUNCH(c);
+      scan<int, int>(c, w.cell_cnt, g.ncell, w.cell_start, s);
+      k_scatter<<<nblk(N, TPB), TPB, 0, s>>>(N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
+      LAUNCH(c);
+      k_cell_gather<<<nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s>>>(g.ncell, w.cell_start, w.perm, pos, type, g,
+                                                                 prm->ntypes, w.iperm, w.spos, w.sloc, w.stype);
+      LAUNCH(c);
+    }
+    {
+      Timer t(c, 1, s);
+      k_nbr_build<<<g.nblock * c->nsplit, NBR_THREADS, nbr_smem(c->cap.window_cap), s>>>(
+          g, w.cell_start, w.sloc, w.spos, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, w.bc, w.bc_len,
+          c->cap.cand_cap, c->cap.window_cap, c->nsplit, w.st);
+      LAUNCH(c);
+    }
+    {
+      Timer t(c, 2, s);
+      k_bond_eval<<<nblk(N, TPB), TPB, 0, s>>>(N, w.spos, w.stype, g, w.prm, w.bc, w.bc_len, w.bc_raw,
+                                              c->cap.cand_cap, w.bdeg);
+      LAUNCH(c);
+      scan<int, int>(c, w.bdeg, N, w.brow, s);
+      k_bond_fill<<<nblk(N, TPB), TPB, 0, s>>>(N, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.brow, w.perm, w.bdeg,
+                                              w.bcol, w.bkey, w.bo, c->cap.bond_cap, w.st);
+      LAUNCH(c);
+      k_bond_sort_delta<<<nblk(N, 128), 128, 0, s>>>(N, w.brow, w.stype, w.prm, w.bcol, w.bkey, w.bown, w.bo, w.delta,
+                                                    c->cap.bond_cap);
+      LAUNCH(c);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  c->last_pos = pos;
+  c->last_type = type;
+  memcpy(c->last_box, box, sizeof(c->last_box));
+  r = read_status(c, s, !c->async);
+  if (r != REAX_OK) return r;
+  c->lists_ok = true;
+  return REAX_OK;
+}
+
+reax_status do_bond_orders(reax_ctx* c, const reax_params* prm, const reax_cutoffs* cut, cudaStream_t s) {
+  if (!c) return REAX_ERR_ARG;
+  if (!c->bound || !c->lists_ok) return REAX_ERR_STATE;
+  reax_status r = upload_params(c, prm, cut, s);
+  if (r != REAX_OK) return r;
+  int N = (int)c->n;
+  if (N > 0) {
+    Timer t(c, 3, s);
+    k_bond_correct<<<148 * 8, TPB, 0, s>>>(c->w.brow, c->w.perm, c->w.stype, c->w.prm, c->w.bcol, c->w.bkey,
+                                           c->w.bown, c->w.bmir, c->w.bo, c->w.delta, c->cap.bond_cap, c->w.st);
+    LAUNCH(c);
+  }
+  if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
+  c->bonds_ok = true;
+  return REAX_OK;
+}
+
+reax_status do_nonbonded(reax_ctx* c, int64_t n, const double* pos, const int* type, const double* q,
+                         const double box[3], const reax_params* prm, const reax_cutoffs* cut, double* force,
+                         double* energy, cudaStream_t s) {
+  reax_status r = check_common(c, n, box, cut);
+  if (r != REAX_OK) return r;
+  if (!c->lists_ok) return REAX_ERR_STATE;
+  if (pos != c->last_pos || type != c->last_type || memcmp(box, c->last_box, sizeof(c->last_box)) != 0)
+    return REAX_ERR_STATE;
+  if (!energy || (n > 0 && (!q || !force))) return REAX_ERR_ARG;
+  r = upload_params(c, prm, cut, s);
+  if (r != REAX_OK) return r;
+  const Grid& g = c->g;
+  WS& w = c->w;
+  int N = (int)n;
+  if (N == 0) {
+    if (cudaMemsetAsync(energy, 0, 2 * sizeof(double), s) != cudaSuccess) return REAX_ERR_CUDA;
+    return REAX_OK;
+  }
+  {
+    Timer t(c, 5, s);
+    k_nb_prep<<<nblk(N, TPB), TPB, 0, s>>>(N, q, w.perm, w.spos, w.sfx, w.sfy, w.sfz, w.st);
+    LAUNCH(c);
+  }
+  {
+    Timer t(c, 4, s);
+    k_nonbonded<<<g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, prm->ntypes), s>>>(
+        g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy,
+        w.sfz, w.epart, c->nsplit, w.st);
+    LAUNCH(c);
+  }
+  {
+    Timer t(c, 5, s);
+    k_finalize_forces<<<nblk(N, TPB), TPB, 0, s>>>(N, w.iperm, w.sfx, w.sfy, w.sfz, force, w.st);
+    LAUNCH(c);
+    k_finalize_energy<<<1, FIN_THREADS, 0, s>>>(g.nblock * c->nsplit, w.epart, energy, w.st);
+    LAUNCH(c);
+  }
+  if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
+  return read_status(c, s, !c->async);
+}
+
+}  // namespace
+
+// ==================================================================== ABI
+extern "C" {
+
+const char* reax_status_str(reax_status s) {
+  switch (s) {
+    case REAX_OK: return "ok";
+    case REAX_ERR_ARG: return "invalid argument";
+    case REAX_ERR_BOX: return "box length must be finite and > 2 r_nonb";
+    case REAX_ERR_CUTOFF: return "invalid cutoffs (need 0 < r_bond <= r_nonb, 0 < bo_cut < 1)";
+    case REAX_ERR_PARAM: return "invalid parameter table";
+    case REAX_ERR_CAPACITY: return "workspace capacity exceeded (see reax_required)";
+    case REAX_ERR_NONFINITE: return "non-finite input or output";
+    case REAX_ERR_CUDA: return "CUDA error";
+    case REAX_ERR_STATE: return "invalid call sequence or binding";
+  }
+  return "unknown";
+}
+
+reax_status reax_create(reax_ctx** out) {
+  if (!out) return REAX_ERR_ARG;
+  *out = nullptr;
+  if (ensure_tables() != cudaSuccess) return REAX_ERR_CUDA;
+  reax_ctx* c = new reax_ctx();
+  if (cudaHostAlloc((void**)&c->h_st, sizeof(Status), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->h_prm, sizeof(DevParams), cudaHostAllocDefault) != cudaSuccess) {
+    if (c->h_st) cudaFreeHost(c->h_st);
+    delete c;
+    return REAX_ERR_CUDA;
+  }
+  memset(c->h_st, 0, sizeof(Status));
+  *out = c;
+  return REAX_OK;
+}
+
+reax_status reax_destroy(reax_ctx* c) {
+  if (!c) return REAX_ERR_ARG;
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (int k = 0; k < REAX_NKERNELS; ++k)
+    for (auto& p : c->ev_pending[k]) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+  if (c->h_st) cudaFreeHost(c->h_st);
+  if (c->h_prm) cudaFreeHost(c->h_prm);
+  delete c;
+  return REAX_OK;
+}
+
+reax_status reax_workspace_bytes(int64_t n, const double box[3], const reax_cutoffs* cut, const reax_capacity* cap,
+                                 size_t* bytes, reax_capacity* cap_out) {
+  if (!bytes || n < 0 || n >= (1LL << 31) - 1) return REAX_ERR_ARG;
+  reax_status r = check_box_cut(box, cut);
+  if (r != REAX_OK) return r;
+  Grid g;
+  if (!make_grid(box, cut->r_nonb, g)) return REAX_ERR_BOX;
+  reax_capacity c;
+  resolve_caps(n, box, cut, cap, c);
+  *bytes = layout(n, g, c, nullptr, nullptr);
+  if (cap_out) *cap_out = c;
+  return REAX_OK;
+}
+
+reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n, const double box[3],
+                                const reax_cutoffs* cut, const reax_capacity* cap) {
+  if (!ctx || !ws || n < 0 || n >= (1LL << 31) - 1) return REAX_ERR_ARG;
+  reax_status r = check_box_cut(box, cut);
+  if (r != REAX_OK) return r;
+  Grid g;
+  if (!make_grid(box, cut->r_nonb, g)) return REAX_ERR_BOX;
+  reax_capacity c;
+  resolve_caps(n, box, cut, cap, c);
+  if (c.row_cap > 65535 || c.window_cap > 65535 || c.cand_cap < 1) return REAX_ERR_ARG;
+  size_t need = layout(n, g, c, nullptr, nullptr);
+  if (bytes < need) return REAX_ERR_CAPACITY;
+  if (((uintptr_t)ws) % ALIGN != 0) return REAX_ERR_ARG;
+  // shared memory limits of the window kernels
+  int dev = 0, maxsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  size_t s1 = nbr_smem(c.window_cap) + sizeof(NbrSmem), s2 = nb_smem(c.window_cap) + sizeof(NBSmem);
+  if ((size_t)maxsm < s1 || (size_t)maxsm < s2) return REAX_ERR_CAPACITY;
+  if (cudaFuncSetAttribute(k_nbr_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nbr_smem(c.window_cap)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_nonbonded, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nb_smem(c.window_cap)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_export_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exp_smem(c.window_cap)) != cudaSuccess)
+    return REAX_ERR_CUDA;
+  ctx->ws_base = (char*)ws;
+  ctx->ws_bytes = bytes;
+  layout(n, g, c, ctx->ws_base, &ctx->w);
+  ctx->g = g;
+  ctx->n = n;
+  ctx->cap = c;
+  ctx->nsplit = choose_split(g.nblock);
+  ctx->cut = *cut;
+  ctx->prm_valid = false;
+  ctx->lists_ok = ctx->bonds_ok = false;
+  // zero the counters that kernels keep self-cleaning
+  cudaError_t e = cudaMemset(ctx->w.cell_cnt, 0, sizeof(int) * (g.ncell + 1));
+  if (e == cudaSuccess) e = cudaMemset(ctx->w.bdeg, 0, sizeof(int) * (std::max<int64_t>(n, 1) + 1));
+  if (e == cudaSuccess) e = cudaMemset(ctx->w.st, 0, sizeof(Status));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  ctx->bound = true;
+  return REAX_OK;
+}
+
+reax_status reax_required(const reax_ctx* ctx, reax_capacity* need) {
+  if (!ctx || !need) return REAX_ERR_ARG;
+  *need = ctx->need;
+  return REAX_OK;
+}
+
+reax_status reax_build_lists(reax_ctx* ctx, int64_t n, const double* pos, const int32_t* type, const double box[3],
+                             const reax_params* params, const reax_cutoffs* cut, void* stream) {
+  if (ctx) ctx->launches_cur = 0;
+  reax_status r = do_build_lists(ctx, n, pos, type, box, params, cut, (cudaStream_t)stream);
+  return r;
+}
+
+reax_status reax_bond_orders(reax_ctx* ctx, const reax_params* params, const reax_cutoffs* cut, void* stream) {
+  return do_bond_orders(ctx, params, cut, (cudaStream_t)stream);
+}
+
+reax_status reax_nonbonded(reax_ctx* ctx, int64_t n, const double* pos, const int32_t* type, const double* q,
+                           const double box[3], const reax_params* params, const reax_cutoffs* cut, double* force,
+                           double* energy, void* stream) {
+  return do_nonbonded(ctx, n, pos, type, q, box, params, cut, force, energy, (cudaStream_t)stream);
+}
+
+reax_status reax_step(reax_ctx* ctx, int64_t n, const double* pos, const int32_t* type, const double* q,
+                      const double box[3], const reax_params* params, const reax_cutoffs* cut, double* force,
+                      double* energy, void* stream) {
+  if (!ctx) return REAX_ERR_ARG;
+  ctx->launches_cur = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  reax_status r = do_build_lists(ctx, n, pos, type, box, params, cut, s);
+  if (r != REAX_OK) return r;
+  r = do_bond_orders(ctx, params, cut, s);
+  if (r != REAX_OK) return r;
+  r = do_nonbonded(ctx, n, pos, type, q, box, params, cut, force, energy, s);
+  ctx->launches_step = ctx->launches_cur;
+  return r;
+}
+
+reax_status reax_step_host(reax_ctx* ctx, int64_t n, const double* pos, const int32_t* type, const double* q,
+                           const double box[3], const reax_params* params, const reax_cutoffs* cut, double* force,
+                           double* energy, void* stream) {
+  if (!ctx) return REAX_ERR_ARG;
+  if (!ctx->bound) return REAX_ERR_STATE;
+  if (n != ctx->n) return REAX_ERR_STATE;
+  if (!energy || (n > 0 && (!pos || !type || !q || !force))) return REAX_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  WS& w = ctx->w;
+  if (n > 0) {
+    if (cudaMemcpyAsync(w.h_pos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(w.h_type, type, sizeof(int) * n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(w.h_q, q, sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return REAX_ERR_CUDA;
+  }
+  reax_status r = reax_step(ctx, n, w.h_pos, w.h_type, w.h_q, box, params, cut, w.h_force, w.h_energy, stream);
+  if (r != REAX_OK) return r;
+  if (n > 0 && cudaMemcpyAsync(force, w.h_force, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return REAX_ERR_CUDA;
+  if (cudaMemcpyAsync(energy, w.h_energy, sizeof(double) * 2, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return REAX_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  return REAX_OK;
+}
+
+reax_status reax_set_async(reax_ctx* ctx, int enable) {
+  if (!ctx) return REAX_ERR_ARG;
+  ctx->async = enable != 0;
+  return REAX_OK;
+}
+
+reax_status reax_check(reax_ctx* ctx, void* stream) {
+  if (!ctx) return REAX_ERR_ARG;
+  if (!ctx->bound) return REAX_ERR_STATE;
+  return read_status(ctx, (cudaStream_t)stream, true);
+}
+
+reax_status reax_set_timing(reax_ctx* ctx, int enable) {
+  if (!ctx) return REAX_ERR_ARG;
+  ctx->timing = enable != 0;
+  return REAX_OK;
+}
+
+reax_status reax_kernel_ms(reax_ctx* ctx, double ms[REAX_NKERNELS], int64_t launches[REAX_NKERNELS], int reset) {
+  if (!ctx) return REAX_ERR_ARG;
+  for (int k = 0; k < REAX_NKERNELS; ++k) {
+    for (auto& p : ctx->ev_pending[k]) {
+      if (cudaEventSynchronize(p.second) != cudaSuccess) return REAX_ERR_CUDA;
+      float t = 0.f;
+      cudaEventElapsedTime(&t, p.first, p.second);
+      ctx->ms_acc[k] += t;
+      ctx->ev_pool.push_back(p.first);
+      ctx->ev_pool.push_back(p.second);
+    }
+    ctx->ev_pending[k].clear();
+    if (ms) ms[k] = ctx->ms_acc[k];
+    if (launches) launches[k] = ctx->launches_acc[k];
+    if (reset) {
+      ctx->ms_acc[k] = 0;
+      ctx->launches_acc[k] = 0;
+    }
+  }
+  return REAX_OK;
+}
+
+int32_t reax_launches_per_step(const reax_ctx* ctx) { return ctx ? ctx->launches_step : 0; }
+
+reax_status reax_selftest_math(reax_ctx* ctx, int64_t n, const double* x, double* out, const reax_params* params,
+                               const reax_cutoffs* cut, void* stream) {
+  if (!ctx || n < 0 || (n > 0 && (!x || !out))) return REAX_ERR_ARG;
+  if (!ctx->bound) return REAX_ERR_STATE;
+  cudaStream_t s = (cudaStream_t)stream;
+  reax_status r = upload_params(ctx, params, cut, s);
+  if (r != REAX_OK) return r;
+  if (n > 0) k_selftest_math<<<nblk(n, TPB), TPB, 0, s>>>((int)n, x, out, ctx->w.prm);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  return REAX_OK;
+}
+
+reax_status reax_pair_count(reax_ctx* ctx, int64_t* n_half_pairs, int64_t* n_bond_entries, void* stream) {
+  if (!ctx) return REAX_ERR_ARG;
+  if (!ctx->bound || !ctx->lists_ok) return REAX_ERR_STATE;
+  cudaStream_t s = (cudaStream_t)stream;
+  int N = (int)ctx->n;
+  long long P = 0;
+  int B = 0;
+  if (N > 0) {
+    if (scan<int, long long>(ctx, ctx->w.nbr_len, N, ctx->w.exp_off, s) != cudaSuccess) return REAX_ERR_CUDA;
+    if (cudaMemcpyAsync(&P, ctx->w.exp_off + N, sizeof(long long), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(&B, ctx->w.brow + N, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return REAX_ERR_CUDA;
+  }
+  if (n_half_pairs) *n_half_pairs = P;
+  if (n_bond_entries) *n_bond_entries = B;
+  return REAX_OK;
+}
+
+reax_status reax_export_pairs(reax_ctx* ctx, int32_t* pi, int32_t* pj, void* stream) {
+  if (!ctx || !pi || !pj) return REAX_ERR_ARG;
+  if (!ctx->bound || !ctx->lists_ok) return REAX_ERR_STATE;
+  cudaStream_t s = (cudaStream_t)stream;
+  int N = (int)ctx->n;
+  if (N == 0) return REAX_OK;
+  if (scan<int, long long>(ctx, ctx->w.nbr_len, N, ctx->w.exp_off, s) != cudaSuccess) return REAX_ERR_CUDA;
+  k_export_pairs<<<ctx->g.nblock, NBR_THREADS, exp_smem(ctx->cap.window_cap), s>>>(
+      ctx->g, ctx->w.cell_start, ctx->w.perm, ctx->w.nbr, ctx->w.nbr_len, ctx->cap.row_cap, ctx->cap.window_cap,
+      ctx->w.exp_off, 0, pi, pj, nullptr, nullptr);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  return REAX_OK;
+}
+
+reax_status reax_export_nbr_digest(reax_ctx* ctx, int64_t* cnt, uint64_t* dig, void* stream) {
+  if (!ctx || !cnt || !dig) return REAX_ERR_ARG;
+  if (!ctx->bound || !ctx->lists_ok) return REAX_ERR_STATE;
+  cudaStream_t s = (cudaStream_t)stream;
+  int N = (int)ctx->n;
+  if (N == 0) return REAX_OK;
+  if (cudaMemsetAsync(cnt, 0, sizeof(int64_t) * N, s) != cudaSuccess ||
+      cudaMemsetAsync(dig, 0, sizeof(uint64_t) * N, s) != cudaSuccess)
+    return REAX_ERR_CUDA;
+  k_export_pairs<<<ctx->g.nblock, NBR_THREADS, exp_smem(ctx->cap.window_cap), s>>>(
+      ctx->g, ctx->w.cell_start, ctx->w.perm, ctx->w.nbr, ctx->w.nbr_len, ctx->cap.row_cap, ctx->cap.window_cap,
+      nullptr, 1, nullptr, nullptr, (unsigned long long*)cnt, (unsigned long long*)dig);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  return REAX_OK;
+}
+
+reax_status reax_export_bonds(reax_ctx* ctx, int64_t* brow, int32_t* bcol, int32_t* mirror, double* bo, double* delta,
+                              void* stream) {
+  if (!ctx) return REAX_ERR_ARG;
+  if (!ctx->bound || !ctx->lists_ok) return REAX_ERR_STATE;
+  if (bo && !ctx->bonds_ok) return REAX_ERR_STATE;
+  cudaStream_t s = (cudaStream_t)stream;
+  int N = (int)ctx->n;
+  if (N == 0) {
+    if (brow && cudaMemsetAsync(brow, 0, sizeof(int64_t), s) != cudaSuccess) return REAX_ERR_CUDA;
+    return cudaStreamSynchronize(s) == cudaSuccess ? REAX_OK : REAX_ERR_CUDA;
+  }
+  WS& w = ctx->w;
+  // original-order row offsets; bc_len is free scratch outside a step
+  k_export_bond_deg<<<nblk(N, TPB), TPB, 0, s>>>(N, w.iperm, w.brow, w.bc_len);
+  if (scan<int, long long>(ctx, w.bc_len, N, w.exp_off, s) != cudaSuccess) return REAX_ERR_CUDA;
+  k_export_bonds<<<nblk(N + 1, TPB), TPB, 0, s>>>(N, w.iperm, w.perm, w.brow, w.bcol, w.bmir, w.bo, w.delta,
+                                                 w.exp_off, brow, bcol, mirror, bo, delta);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  return REAX_OK;
+}
+
+}  // extern "C"

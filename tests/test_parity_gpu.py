@@ -1,0 +1,179 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle, element by
+element on the same seeded inputs (north_star tolerances: pair and bond sets
+exact, BO 1e-12 abs, energies 1e-10 rel, forces 1e-8 (1+|F|))."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+from gpu_helpers import (CUT, TOL_F, assert_energy_force, full_parity, gpu_run, pair_keys_gpu,
+                         pair_keys_oracle)
+
+pytestmark = pytest.mark.gpu
+
+
+def test_c0_full(params, c0):
+    full_parity(c0, params)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_tiny_random_boxes(params, seed):
+    rng = np.random.default_rng(100 + seed)
+    box = rng.uniform(20.05, 26.0, 3)
+    n = int(rng.integers(2, 300))
+    full_parity(gen.make_system(n, box, 4000 + seed), params)
+
+
+def test_ragged_sizes_and_dense_small_box(params):
+    for n, box in ((1, (21, 21, 21)), (2, (20.5, 30, 22)), (33, (25, 21, 40)), (1000, (21.5, 21.5, 21.5))):
+        s = gen.make_system(n, box, 77 + n)
+        full_parity(s, params)
+
+
+def test_exact_cutoff_pairs(params):
+    # atoms placed exactly on sub-cell faces and at exactly r = R and r = r_bond
+    L = 30.0
+    pos = np.array([[0.0, 0.0, 0.0], [10.0, 0.0, 0.0], [20.0, 0.0, 0.0], [29.999999999999996, 1, 1],
+                    [9.999999999999998, 1, 1], [5.0, 5.0, 5.0], [5.0, 15.0, 5.0], [5.0, 5.0, 15.0],
+                    [1.0, 2.0, 3.0], [1.0 + 6.0, 2.0 + 8.0, 3.0], [15.0, 15.0, 15.0], [16.3, 15.0, 15.0]])
+    typ = np.array([0, 1, 2, 3] * 3, np.int32)
+    q = np.linspace(-0.4, 0.4, 12)
+    s = gen.System(pos, typ, q - q.mean(), np.array([L, L, L]))
+    ctx, ref, F, E = full_parity(s, params)
+    assert len(ref["hcol"]) > 0 and len(ref["bcol"]) > 0
+
+
+def test_positions_outside_box_are_wrapped(params):
+    s = gen.make_system(500, (22.0, 23.0, 24.0), 9)
+    k = np.random.default_rng(0).integers(-3, 4, size=s.pos.shape)
+    shifted = s.pos + k * s.box
+    ref = oracle.evaluate(gen.System(shifted, s.type, s.q, s.box), params, CUT)
+    ctx, F, E = gpu_run(s, params, pos_override=shifted)
+    n = len(s.pos)
+    assert np.array_equal(pair_keys_gpu(ctx, n), pair_keys_oracle(ref["hrow"], ref["hcol"], n))
+    assert_energy_force(E, F, ref["E"], ref["F"])
+
+
+def test_empty_system(params):
+    s = gen.System(np.zeros((0, 3)), np.zeros(0, np.int32), np.zeros(0), np.array([25.0, 25.0, 25.0]))
+    ctx, F, E = gpu_run(s, params)
+    assert F.shape == (0, 3) and E.tolist() == [0.0, 0.0]
+    assert ctx.pair_count() == (0, 0)
+
+
+def test_c1_full(params):
+    full_parity(gen.make_config(1), params)
+
+
+def test_async_mode_matches(params):
+    s = gen.make_config(1)
+    _, F1, E1 = gpu_run(s, params)
+    _, F2, E2 = gpu_run(s, params, async_=True)
+    assert np.array_equal(E1, E2)   # energies are reduced in a fixed order
+    assert np.all(np.abs(F1 - F2) <= 1e-12 * (1 + np.abs(F1)))
+
+
+def test_cuda_graph_replay_matches(params):
+    import paper_1706_07772_b200 as rx
+    s = gen.make_config(1)
+    dev = torch.device("cuda:0")
+    ctx = rx.Reax(len(s.pos), s.box, params, CUT, device=dev)
+    pos = torch.from_numpy(s.pos).to(dev)
+    typ = torch.from_numpy(s.type).to(dev)
+    q = torch.from_numpy(s.q).to(dev)
+    F0, E0 = ctx.step(pos, typ, q)
+    torch.cuda.synchronize()
+    F0, E0 = F0.cpu().numpy(), E0.cpu().numpy()
+    ctx.set_async(True)
+    F = torch.empty((len(s.pos), 3), dtype=torch.float64, device=dev)
+    E = torch.empty(2, dtype=torch.float64, device=dev)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        ctx.step(pos, typ, q, F, E)  # warm-up on the capture stream
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ctx.step(pos, typ, q, F, E)
+    F.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    ctx.check()
+    assert np.array_equal(E.cpu().numpy(), E0)
+    assert np.all(np.abs(F.cpu().numpy() - F0) <= 1e-12 * (1 + np.abs(F0)))
+
+
+def test_capacity_regrow(params):
+    s = gen.make_config(0)
+    ref = oracle.evaluate(s, params, CUT)
+    ctx, F, E = gpu_run(s, params, capacity=dict(row_cap=64, cand_cap=2, bond_cap=100, window_cap=256))
+    assert ctx.cap.row_cap >= 64 and ctx.cap.window_cap > 256
+    assert_energy_force(E, F, ref["E"], ref["F"])
+    n = len(s.pos)
+    assert np.array_equal(pair_keys_gpu(ctx, n), pair_keys_oracle(ref["hrow"], ref["hcol"], n))
+
+
+def test_repeat_steps_deterministic(params):
+    import paper_1706_07772_b200 as rx
+    s = gen.make_config(1)
+    dev = torch.device("cuda:0")
+    ctx = rx.Reax(len(s.pos), s.box, params, CUT, device=dev)
+    pos = torch.from_numpy(s.pos).to(dev)
+    typ = torch.from_numpy(s.type).to(dev)
+    q = torch.from_numpy(s.q).to(dev)
+    out = [ctx.step(pos, typ, q) for _ in range(3)]
+    torch.cuda.synchronize()
+    E = [o[1].cpu().numpy() for o in out]
+    assert np.array_equal(E[0], E[1]) and np.array_equal(E[1], E[2])
+    F = [o[0].cpu().numpy() for o in out]
+    assert np.all(np.abs(F[0] - F[2]) <= 1e-12 * (1 + np.abs(F[0])))
+
+
+@pytest.mark.slow
+def test_c2_full(params):
+    full_parity(gen.make_config(2), params)
+
+
+def _sampled(k, params, nsample, seed=0):
+    s = gen.make_config(k)
+    ctx, F, E = gpu_run(s, params)
+    n = len(s.pos)
+    rng = np.random.default_rng(seed)
+    idx = np.concatenate([[0, n - 1], rng.choice(n, nsample, replace=False)])
+    cnt, dig = [t.cpu().numpy() for t in ctx.export_digest()]
+    brow, bcol, mir, bo, dl = [t.cpu().numpy() for t in ctx.export_bonds()]
+    for i in idx:
+        nb = oracle.atom_neighbors(i, s.pos, s.box, CUT["r_nonb"])
+        assert cnt[i] == len(nb), (i, cnt[i], len(nb))
+        h = 0
+        for j in nb:
+            h = (h + oracle.mix64(min(i, j), max(i, j))) % (1 << 64)
+        assert int(np.uint64(dig[i].view(np.uint64))) == h
+        Fo, _ = oracle.atom_force(i, s.pos, s.type, s.q, s.box, params, CUT["r_nonb"])
+        assert np.all(np.abs(F[i] - Fo) <= TOL_F * (1 + np.abs(Fo))), (i, F[i], Fo)
+        part, raw, dli = oracle.atom_bonds(i, s.pos, s.type, s.box, params, CUT["r_bond"], CUT["bo_cut"])
+        seg = slice(brow[i], brow[i + 1])
+        assert bcol[seg].tolist() == part.tolist()
+        assert np.max(np.abs(bo[seg, :4] - raw), initial=0) <= 1e-12
+        assert np.all(np.abs(dl[i] - dli) <= 1e-12)
+        for e, j in zip(range(brow[i], brow[i + 1]), part):
+            _, _, dlj = oracle.atom_bonds(j, s.pos, s.type, s.box, params, CUT["r_bond"], CUT["bo_cut"])
+            a, b = (i, j) if i < j else (j, i)
+            da, db = (dli, dlj) if i < j else (dlj, dli)
+            corr, _ = oracle.bo_corr_pair(bo[e, :4], da[0], da[1], db[0], db[1], s.type[a], s.type[b], params)
+            assert np.all(np.abs(bo[e, 4:] - corr) <= 1e-12)
+    # properties at any size: Newton's third law, mirror symmetry of the bond list
+    assert np.all(np.abs(F.sum(0)) <= 1e-11 * np.abs(F).sum())
+    assert np.array_equal(bo[mir], bo)
+    return E
+
+
+@pytest.mark.slow
+def test_c3_sampled(params):
+    _sampled(3, params, 40)
+
+
+@pytest.mark.slow
+def test_c4_sampled(params):
+    _sampled(4, params, 24)
