@@ -151,7 +151,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--graph", action="store_true", help="also time CUDA-graph replay (extra key)")
+    ap.add_argument("--no-graph", action="store_true", help="direct launches instead of CUDA-graph replay")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3   # timing rule: W >= 3
@@ -200,8 +200,40 @@ def main():
         flush.fill_(1.0)
         ctx.step(pos, typ, q, F, E)
     ctx.check()
-    ctx.set_timing(True)
-    ctx.kernel_ms(reset=True)
+    launches = ctx.launches_per_step()
+    graph = tgraph = None
+    if not args.no_graph:
+        # the whole step as one CUDA graph (c1 is launch-bound with direct launches)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            ctx.step(pos, typ, q, F, E)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            ctx.step(pos, typ, q, F, E)
+        # same step with the library's per-kernel CUDA events captured as
+        # external event nodes (read back after each replay)
+        ctx.set_timing(True)
+        ctx.kernel_ms(reset=True)
+        tgraph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(tgraph):
+            ctx.step(pos, typ, q, F, E)
+        ctx.set_timing(False)
+        for _ in range(2):
+            graph.replay()
+            tgraph.replay()
+        torch.cuda.synchronize()
+
+    def one_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            ctx.step(pos, typ, q, F, E)
+
+    # pass 1 (value): K steps back to back, L2 flushed between them, each
+    # bracketed by CUDA events on the launching stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
@@ -209,43 +241,44 @@ def main():
     for k in range(args.steps):
         flush.fill_(float(k))          # L2 flush between timed steps (outside the events)
         ev[k][0].record()
-        ctx.step(pos, typ, q, F, E)
+        one_step()
         ev[k][1].record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ctx.check()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    kms = ctx.kernel_ms(reset=True)
-    ctx.set_timing(False)
+    # pass 2 (kernel breakdown): the same K steps with per-kernel events live
+    kms_acc = {k: 0.0 for k in rx.KERNEL_GROUPS}
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if tgraph is None:
+        ctx.set_timing(True)
+        ctx.kernel_ms(reset=True)
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        ev2[k][0].record()
+        if tgraph is not None:
+            tgraph.replay()
+        else:
+            ctx.step(pos, typ, q, F, E)
+        ev2[k][1].record()
+        if tgraph is not None:
+            ev2[k][1].synchronize()
+            for name, (ms, _) in ctx.kernel_ms(peek=True).items():
+                kms_acc[name] += ms
+    torch.cuda.synchronize()
+    if tgraph is None:
+        kms_acc = {name: ms for name, (ms, _) in ctx.kernel_ms(reset=True).items()}
+        ctx.set_timing(False)
+    ctx.check()
+    pass2_ms = sum(a.elapsed_time(b) for a, b in ev2) / args.steps
+    kms = {name: (kms_acc[name], args.steps) for name in kms_acc}
     tot_ms = sum(step_ms)
     t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_ms_max = float(t.item())
     value = n * args.steps * world / (tot_ms_max * 1e-3)
-    launches = ctx.launches_per_step()
-
-    graph_ms = None
-    if args.graph:
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            ctx.step(pos, typ, q, F, E)
-        torch.cuda.current_stream().wait_stream(side)
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            ctx.step(pos, typ, q, F, E)
-        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        for k in range(args.steps):
-            flush.fill_(float(k))
-            gev[k][0].record()
-            g.replay()
-            gev[k][1].record()
-        torch.cuda.synchronize()
-        ctx.check()
-        graph_ms = sum(a.elapsed_time(b) for a, b in gev) / args.steps
 
     e2e = None
     if not args.no_e2e:
@@ -274,9 +307,11 @@ def main():
     clocks = sample_clocks_stop(clk)
 
     nb_ms, nb_launches = kms["nonbonded"]
+    nb_launches = args.steps
     nb_avg_s = nb_ms / max(nb_launches, 1) * 1e-3
     achieved = W_NB_DP_PER_PAIR * P / nb_avg_s
     nbr_ms, nbr_launches = kms["nbr"]
+    nbr_launches = args.steps
     nbr_avg_s = nbr_ms / max(nbr_launches, 1) * 1e-3
     nbr_bytes = n * NBR_BYTES_PER_ATOM_FIXED + P * NBR_BYTES_PER_PAIR + 2.9 * n * NBR_BYTES_PER_BONDCAND
     hbm_peak = None
@@ -297,7 +332,8 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config, c), "n_atoms": n, "half_pairs": P, "bond_entries": B,
                    "evals_timed": args.steps, "lists": "rebuilt every step", "l2": "flushed (512 MB write) between timed steps",
-                   "parallelism": "replicas" if world > 1 else "single GPU"},
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "launch": "direct launches" if args.no_graph else "CUDA graph replay of reax_step (async mode)"},
         "ns_per_atom_step": 1e9 / value * world if value else None,
         "roofline": {"bound": "alu", "kernel": "k_nonbonded (a7)", "achieved": achieved / 1e12, "peak": peak_dfma / 1e12,
                      "unit": "T FP64-pipe thread-instructions/s", "frac": achieved / peak_dfma,
@@ -310,15 +346,13 @@ def main():
              "bytes_per_launch": nbr_bytes},
         ],
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kms.items()},
+        "timing_pass_ms_per_step": pass2_ms,
         "kernel_share": {k: v[0] / step_total_ms for k, v in kms.items()} if step_total_ms else None,
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,
         "e2e": e2e,
         "clocks": clocks,
     }
-    if graph_ms is not None:
-        line["graph_ms_per_step"] = graph_ms
-        line["graph_value"] = n / (graph_ms * 1e-3)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         evals = 3 if args.config <= 1 else 1
         v, dt, nn = run_cpu_oracle(args.config if args.config <= 2 else 1, evals)

@@ -162,7 +162,10 @@ reax_status reax_check(reax_ctx* ctx, void* stream);
 #define REAX_NKERNELS 6
 reax_status reax_set_timing(reax_ctx* ctx, int enable);
 /* Accumulated milliseconds and launch counts per kernel group since the last
- * reset (synchronises the last recorded events). */
+ * reset (synchronises the last recorded events).  reset = 0: accumulate and
+ * keep; 1: return and clear; 2 (peek): return the times of the currently
+ * recorded events without consuming them, for CUDA-graph replays (events
+ * captured in a graph are external event nodes re-recorded by each replay). */
 reax_status reax_kernel_ms(reax_ctx* ctx, double ms[REAX_NKERNELS], int64_t launches[REAX_NKERNELS],
                            int reset);
 /* Number of device kernels launched by the last reax_step. */

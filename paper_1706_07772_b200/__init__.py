@@ -17,7 +17,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libreax.so")
+LIB_PATH = os.environ.get("REAX_LIBRARY", os.path.join(_HERE, "libreax.so"))
 
 OK, ERR_ARG, ERR_BOX, ERR_CUTOFF, ERR_PARAM, ERR_CAPACITY, ERR_NONFINITE, ERR_CUDA, ERR_STATE = range(9)
 KERNEL_GROUPS = ("bin", "nbr", "bonds", "bond_orders", "nonbonded", "other")
@@ -264,10 +264,10 @@ class Reax:
     def set_timing(self, enable: bool):
         _check(self.lib.reax_set_timing(self.ctx, int(bool(enable))), "reax_set_timing")
 
-    def kernel_ms(self, reset=False):
+    def kernel_ms(self, reset=False, peek=False):
         ms = (ctypes.c_double * 6)()
         nl = (ctypes.c_int64 * 6)()
-        _check(self.lib.reax_kernel_ms(self.ctx, ms, nl, int(reset)), "reax_kernel_ms")
+        _check(self.lib.reax_kernel_ms(self.ctx, ms, nl, 2 if peek else int(reset)), "reax_kernel_ms")
         return {k: (ms[i], nl[i]) for i, k in enumerate(KERNEL_GROUPS)}
 
     def launches_per_step(self) -> int:

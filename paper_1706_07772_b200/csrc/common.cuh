@@ -18,6 +18,8 @@ constexpr int WB = HB + 2 * SR;   // 6
 constexpr int NWB = WB * WB * WB; // 216
 constexpr int NHOME = HB * HB * HB;
 constexpr int MAX_RUNS = 16;
+constexpr int NWU_MAX = 136;   // used window cells (130 for HB = 2, SR = 2; checked at table build)
+constexpr int NMW = (NWB + 31) / 32;  // mask words over used window cells
 constexpr int NT_MAX = 16;
 constexpr int NTP_MAX = NT_MAX * NT_MAX;
 
@@ -29,6 +31,10 @@ struct WindowTables {
   int nrun[NHOME];               // forward runs of home sub-cell h (own cell excluded)
   int run_a[NHOME][MAX_RUNS];    // first used-list index of the run
   int run_b[NHOME][MAX_RUNS];    // last used-list index of the run (inclusive)
+  int nrun1[NHOME];              // un-merged forward runs (one per (oy, oz)) of home sub-cell h
+  int run1_a[NHOME][MAX_RUNS];
+  int run1_b[NHOME][MAX_RUNS];
+  unsigned mask[NHOME][NMW];     // bit k: used cell k is in home sub-cell h's half stencil or is h itself
 };
 
 struct Grid {
@@ -120,9 +126,17 @@ struct WS {
   double* sfx;       // n
   double* sfy;       // n
   double* sfz;       // n
-  double* epart;     // nblock * 2
+  double2* erow;     // n   per-row (E_vdW, E_Coul)
+  double* epart;     // energy reduction partials
+  unsigned* ticket;  // last-block counter of the energy reduction
+  int* ucol;         // bond_cap  unsorted full-list entries (fill order)
+  int* ukey;         // bond_cap
+  int* uown;         // bond_cap
+  double4* uraw;     // bond_cap
   long long* scan_tmp;  // scan partials
   long long* exp_off;   // n + 1 (export scratch)
+  unsigned long long* lb_status;  // look-back scan tile status
+  unsigned* lb_ticket;            // look-back scan tile ticket
   DevParams* prm;
   Status* st;
   double* h_pos;     // staging for reax_step_host

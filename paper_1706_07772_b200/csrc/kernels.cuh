@@ -116,10 +116,93 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const TI* in, int64
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = (TO)part[gridDim.x];
 }
 
+// Single-pass exclusive scan (decoupled look-back): tiles get ids from a
+// ticket counter (forward progress), publish their aggregate, then look back
+// over predecessors until an inclusive prefix is found.  status[] and the
+// ticket must be zero on entry (the producing kernel clears them).
+constexpr int LB_THREADS = 512;
+constexpr int LB_ITEMS = 8;
+constexpr int LB_TILE = LB_THREADS * LB_ITEMS;
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_MASK = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(LB_THREADS) k_scan_lookback(const int* __restrict__ in, int n, int* __restrict__ out,
+                                                              unsigned long long* __restrict__ status,
+                                                              unsigned* __restrict__ ticket) {
+  __shared__ int tile_id;
+  __shared__ long long warp_tot[LB_THREADS / 32];
+  __shared__ long long excl_tile;
+  if (threadIdx.x == 0) tile_id = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int t = tile_id;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i0 = (int64_t)t * LB_TILE + (int64_t)threadIdx.x * LB_ITEMS;
+  int v[LB_ITEMS];
+  long long sum = 0;
+#pragma unroll
+  for (int q = 0; q < LB_ITEMS; ++q) {
+    v[q] = (i0 + q < n) ? in[i0 + q] : 0;
+    sum += v[q];
+  }
+  long long x = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    long long y = lane < LB_THREADS / 32 ? warp_tot[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long z = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += z;
+    }
+    if (lane < LB_THREADS / 32) warp_tot[lane] = y;
+    long long agg = __shfl_sync(0xffffffffu, y, LB_THREADS / 32 - 1);
+    if (lane == 0) {
+      volatile unsigned long long* vs = status;
+      if (t == 0) {
+        vs[0] = LB_PRE | (unsigned long long)agg;
+        excl_tile = 0;
+      } else {
+        vs[t] = LB_AGG | (unsigned long long)agg;
+        long long acc = 0;
+        int p = t - 1;
+        for (;;) {
+          unsigned long long s;
+          do { s = vs[p]; } while ((s >> 62) == 0);
+          acc += (long long)(s & LB_MASK);
+          if ((s >> 62) == 2) break;
+          --p;
+        }
+        __threadfence();
+        vs[t] = LB_PRE | (unsigned long long)(acc + agg);
+        excl_tile = acc;
+      }
+      if (t == (int)gridDim.x - 1) *ticket = 0u;  // ready for the next call
+    }
+  }
+  __syncthreads();
+  long long run = excl_tile + x - sum + (w > 0 ? warp_tot[w - 1] : 0);
+#pragma unroll
+  for (int q = 0; q < LB_ITEMS; ++q) {
+    if (i0 + q < n) out[i0 + q] = (int)run;
+    run += v[q];
+  }
+  if (t == (int)gridDim.x - 1 && threadIdx.x == LB_THREADS - 1) out[n] = (int)(excl_tile + warp_tot[LB_THREADS / 32 - 1]);
+}
+
+// clears a look-back status array (run by the kernel before the scan)
+__device__ __forceinline__ void clear_status(unsigned long long* status, int ntiles) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ntiles) status[i] = 0ull;
+}
+
 // ================================================================ a1-a2 bin
 // wrap, validate, sub-cell id, histogram
 __global__ void k_bin(int n, const double* __restrict__ pos, const int* __restrict__ type, Grid g,
-                      int nt, int* __restrict__ cell_of, int* __restrict__ cell_cnt, Status* st) {
+                      int nt, int* __restrict__ cell_of, int* __restrict__ cell_cnt, Status* st,
+                      unsigned long long* __restrict__ scan_status, int scan_tiles) {
+  clear_status(scan_status, scan_tiles);
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int c[3];
@@ -198,12 +281,12 @@ __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int
 // ======================================================== window of a block
 // Shared-memory description of a home block's neighbour window.
 struct WinSmem {
-  int start[NWB];      // first sorted atom of each used window cell
-  int cnt[NWB];
-  int slot[NWB + 1];   // slot base (prefix of cnt)
-  double shift[NWB][3];// periodic image shift (0 or +-L) of each window cell
-  float off[NWB][3];   // cell origin relative to the block origin (fp32)
-  int home_ok[NHOME];  // home sub-cell exists (odd nc leaves the last block partial)
+  int start[NWU_MAX];       // first sorted atom of each used window cell
+  int cnt[NWU_MAX];
+  int slot[NWU_MAX + 1];    // slot base (prefix of cnt)
+  double shift[NWU_MAX][3]; // periodic image shift (0 or +-L) of each window cell
+  int home_ok[NHOME];       // home sub-cell exists (odd nc leaves the last block partial)
+  int has_shift;            // some window cell is a periodic image
 };
 
 // Fill WinSmem for block b (all threads participate). Returns total slots.
@@ -212,6 +295,7 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
   int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
   int base[3] = {bx * HB, by * HB, bz * HB};
   int nwu = c_win.nwu;
+  int my_shift = 0;
   for (int k = threadIdx.x; k < nwu; k += blockDim.x) {
     int wb = c_win.wu[k];
     int wv[3] = {wb % WB, (wb / WB) % WB, wb / (WB * WB)};
@@ -222,7 +306,7 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
       int m = u >= 0 ? u / g.nc[a] : -((-u + g.nc[a] - 1) / g.nc[a]);  // floor(u / nc)
       cc[a] = u - m * g.nc[a];
       W.shift[k][a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
-      W.off[k][a] = (float)((double)(u - base[a]) * g.h[a]);
+      my_shift |= (m != 0);
     }
     int cid = (cc[2] * g.nc[1] + cc[1]) * g.nc[0] + cc[0];
     int s0 = cell_start[cid];
@@ -234,7 +318,8 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
     int hv[3] = {h % HB, (h / HB) % HB, h / (HB * HB)};
     W.home_ok[h] = (base[0] + hv[0] < g.nc[0]) && (base[1] + hv[1] < g.nc[1]) && (base[2] + hv[2] < g.nc[2]);
   }
-  __syncthreads();
+  const int any_shift = __syncthreads_or(my_shift);
+  if (threadIdx.x == 0) W.has_shift = any_shift;
   if (threadIdx.x < 32) {  // warp 0: exclusive scan over <= 216 counts
     int carry = 0;
     for (int k0 = 0; k0 < nwu; k0 += 32) {
@@ -254,6 +339,16 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
   return W.slot[nwu];
 }
 
+// window cell holding slot t: largest k with W.slot[k] <= t (binary search)
+__device__ __forceinline__ int cell_of_slot(const WinSmem& W, int nwu, int t) {
+  int lo = 0, hi = nwu - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (W.slot[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 // rows of the block: home sub-cell h, slot range [slot[home_k[h]], slot[home_k[h]+1])
 __device__ __forceinline__ bool row_of(const WinSmem& W, int r, int& h, int& si) {
   for (h = 0; h < NHOME; ++h) {
@@ -269,30 +364,51 @@ __device__ __forceinline__ bool row_of(const WinSmem& W, int r, int& h, int& si)
   return false;
 }
 
+__device__ __forceinline__ int warp_find(int incl, int t) {
+  // largest q with excl(q) <= t, where incl is the lane's inclusive prefix
+  int q = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    int v = __shfl_sync(0xffffffffu, incl, q + step - 1);
+    if (t >= v) q += step;
+  }
+  return q;
+}
+
 // ========================================================= a3-a4 list build
 constexpr int NBR_THREADS = 256;
+constexpr int MAX_BLOCK_ROWS = 1024;
 
 struct NbrSmem {
   WinSmem W;
   float rcand2[NTP_MAX];
+  int rowtab[MAX_BLOCK_ROWS];   // row r of the block -> (window slot << 3) | home sub-cell
+  int nrows;
+  int next_row;
 };
 
-// One CTA per home block.  Candidates of the window are staged in shared
-// memory as fp32 coordinates relative to the block origin; each warp scans
-// one row (atom) against the forward runs of its sub-cell's half stencil and
-// its own cell (j after i), classifies r^2 in fp32 with a band of +-m around
-// R^2 that is ~50x wider than the fp32 error bound, settles the band with the
-// exact FMA-free fp64 test, and compacts accepted candidates with a ballot.
-__global__ void __launch_bounds__(NBR_THREADS) k_nbr_build(Grid g, const int* __restrict__ cell_start,
+// One CTA per (home block, split).  Candidates of the window are staged in
+// shared memory as fp32 coordinates relative to the block origin.  A warp
+// takes one row (atom) at a time.  Its candidate stream is the concatenation
+// of intervals, one per lane: the forward runs of its sub-cell's half stencil
+// (rows of cells along x), each trimmed to the cells whose x-extent meets
+// [x_i - w, x_i + w] with w = sqrt(R^2 - d_yz^2) (d_yz: distance from atom i to
+// the run's y-z cross-section, so no partner is ever trimmed), plus its own
+// cell after i.  Lanes walk the stream 32 candidates at a time: r^2 in fp32
+// against a band of +-m around R^2 (~70x the fp32 error bound), the band
+// settled by the exact FMA-free fp64 test; accepted window slots are
+// compacted with a ballot and stored coalesced.  Bond candidates (r^2 below the
+// conservative BO' = bo_cut radius) are compacted the same way.
+__global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int* __restrict__ cell_start,
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
     int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NbrSmem S;
   const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
-  float4* cand = reinterpret_cast<float4*>(dyn);                                // window_cap
-  int* cand_j = reinterpret_cast<int*>(cand + window_cap);                       // window_cap
-  unsigned char* cand_k = reinterpret_cast<unsigned char*>(cand_j + window_cap); // window_cap
+  float4* cand = reinterpret_cast<float4*>(dyn);                                // window_cap + 32
+  int* cand_j = reinterpret_cast<int*>(cand + window_cap + 32);                  // window_cap + 32
+  unsigned char* cand_k = reinterpret_cast<unsigned char*>(cand_j + window_cap + 32);
   const int nt = prm->nt;
   for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) S.rcand2[t] = prm->rcand2[t];
   const float R2lo = prm->R2lo, R2hi = prm->R2hi, rcmax = prm->rcand2_max;
@@ -300,87 +416,157 @@ __global__ void __launch_bounds__(NBR_THREADS) k_nbr_build(Grid g, const int* __
   int W = build_window(S.W, blk, g, cell_start);
   const int nwu = c_win.nwu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  if (threadIdx.x == 0) {   // row table of the block (rows in home sub-cell order)
+    int r = 0;
+    for (int h = 0; h < NHOME; ++h) {
+      if (!S.W.home_ok[h]) continue;
+      const int kk = c_win.home_k[h], a = S.W.slot[kk], c = S.W.cnt[kk];
+      for (int q = 0; q < c; ++q, ++r)
+        if (r < MAX_BLOCK_ROWS) S.rowtab[r] = ((a + q) << 3) | h;
+    }
+    S.nrows = r;
+    S.next_row = 0;
+  }
+  __syncthreads();
+  const int nrows = S.nrows;
   if (W > window_cap) {
     if (threadIdx.x == 0) {
       set_flag(st, ST_WIN_OVF);
       atomicMax(&st->max_window, W);
     }
     // leave every row of the block empty so later kernels stay in bounds
-    for (int r = split * nwarp + warp;; r += nsplit * nwarp) {
-      int h, si;
-      if (!row_of(S.W, r, h, si)) break;
-      int s = S.W.start[c_win.home_k[h]] + (si - S.W.slot[c_win.home_k[h]]);
-      if (lane == 0) { nbr_len[s] = 0; bc_len[s] = 0; }
+    for (int h = 0; h < NHOME; ++h) {
+      if (!S.W.home_ok[h]) continue;
+      const int kk = c_win.home_k[h];
+      for (int q = threadIdx.x; q < S.W.cnt[kk]; q += blockDim.x) {
+        nbr_len[S.W.start[kk] + q] = 0;
+        bc_len[S.W.start[kk] + q] = 0;
+      }
     }
     return;
   }
-  for (int k = warp; k < nwu; k += nwarp) {
-    int s0 = S.W.start[k], c = S.W.cnt[k], b0 = S.W.slot[k];
-    float ox = S.W.off[k][0], oy = S.W.off[k][1], oz = S.W.off[k][2];
-    for (int a = lane; a < c; a += 32) {
-      float4 l = sloc[s0 + a];
-      cand[b0 + a] = make_float4(l.x + ox, l.y + oy, l.z + oz, l.w);
-      cand_j[b0 + a] = s0 + a;
-      cand_k[b0 + a] = (unsigned char)k;
-    }
+  // staging, flattened over slots so that all global loads are in flight at once
+#pragma unroll 4
+  for (int t = threadIdx.x; t < W; t += blockDim.x) {
+    const int k = cell_of_slot(S.W, nwu, t);
+    const int j = S.W.start[k] + (t - S.W.slot[k]);
+    const int wb = c_win.wu[k];
+    // cell origin relative to the block origin: (w - SR) h per axis
+    const float ox = (float)((wb % WB - SR) * g.h[0]);
+    const float oy = (float)((wb / WB % WB - SR) * g.h[1]);
+    const float oz = (float)((wb / (WB * WB) - SR) * g.h[2]);
+    const float4 l = sloc[j];
+    cand[t] = make_float4(l.x + ox, l.y + oy, l.z + oz, l.w);
+    cand_j[t] = j;
+    cand_k[t] = (unsigned char)k;
   }
+  if (threadIdx.x < 32) cand[W + threadIdx.x] = make_float4(1e30f, 1e30f, 1e30f, 0.f);  // sentinel
   __syncthreads();
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int r = split * nwarp + warp;; r += nsplit * nwarp) {
+  const unsigned lt_mask = (1u << lane) - 1u, le_mask = lt_mask | (1u << lane);
+  const float R2mid = 0.5f * (R2lo + R2hi), R2half = 0.5f * (R2hi - R2lo);
+  const float Rt = sqrtf(R2hi) + 1e-3f;                 // trimming radius (conservative)
+  const float hx = (float)g.h[0], hy = (float)g.h[1], hz = (float)g.h[2], ihx = 1.0f / hx;
+  for (;;) {
+    int m = 0;
+    if (lane == 0) m = atomicAdd(&S.next_row, 1);
+    m = __shfl_sync(0xffffffffu, m, 0);
+    const int r = split + m * nsplit;
+    if (r >= nrows) break;
     int h, si;
-    if (!row_of(S.W, r, h, si)) break;
+    if (r < MAX_BLOCK_ROWS) {
+      const int rt = S.rowtab[r];
+      h = rt & 7;
+      si = rt >> 3;
+    } else {   // pathological density: beyond the table
+      row_of(S.W, r, h, si);
+    }
     const int s = cand_j[si];
     const float4 ri = cand[si];
     const int ti = __float_as_int(ri.w);
+    const int kh = c_win.home_k[h];
+    // ---- intervals: lane q < nrun trims run q, lane nrun takes the own cell
+    const int nrun = c_win.nrun1[h];
+    int ia = 0, il = 0;
+    if (lane < nrun) {
+      const int ka = c_win.run1_a[h][lane], kb = c_win.run1_b[h][lane];
+      const int wba = c_win.wu[ka];
+      const int wxa = wba % WB - SR;                   // x cell offset (block frame) of the run's first cell
+      const float oy = (float)((wba / WB % WB - SR) * g.h[1]);
+      const float oz = (float)((wba / (WB * WB) - SR) * g.h[2]);
+      const float dy = fmaxf(0.f, fmaxf(oy - ri.y, ri.y - (oy + hy)));
+      const float dz = fmaxf(0.f, fmaxf(oz - ri.z, ri.z - (oz + hz)));
+      const float w2 = Rt * Rt - (dy * dy + dz * dz);
+      if (w2 >= 0.f) {
+        const float w = sqrtf(w2) + 1e-3f;
+        // cells c (block frame) with [c hx, (c+1) hx] meeting [x - w, x + w]
+        const int c0 = max(wxa, (int)floorf((ri.x - w) * ihx));
+        const int c1 = min(wxa + (kb - ka), (int)floorf((ri.x + w) * ihx));
+        if (c0 <= c1) {
+          ia = S.W.slot[ka + (c0 - wxa)];
+          il = S.W.slot[ka + (c1 - wxa) + 1] - ia;
+        }
+      }
+    } else if (lane == nrun) {
+      ia = si + 1;
+      il = S.W.slot[kh + 1] - ia;
+    }
+    // compact the non-empty intervals, then exclusive offsets
+    const unsigned ne = __ballot_sync(0xffffffffu, il > 0);
+    int inc = il;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, inc, 31);
+    const int start_q = inc - il;                       // stream position where my interval starts
+    // compacted interval table: lane t holds the t-th non-empty interval's
+    // (start position, slot - position shift); intervals keep their order
+    const unsigned src = __fns(ne, 0, lane + 1);      // lane of the (lane+1)-th set bit
+    const int srcl = src < 32 ? (int)src : 0;
+    const int cstart = __shfl_sync(0xffffffffu, start_q, srcl);
+    const int cshift = __shfl_sync(0xffffffffu, ia - start_q, srcl);
+    const int nint = __popc(ne);
     int len = 0, nc = 0;
     uint16_t* row = nbr + (int64_t)s * row_cap;
     int* crow = bc + (int64_t)s * cand_cap;
-    const int nrun = c_win.nrun[h];
-    const int kh = c_win.home_k[h];
-    for (int q = 0; q <= nrun; ++q) {
-      int sa, sb;
-      if (q < nrun) {
-        sa = S.W.slot[c_win.run_a[h][q]];
-        sb = S.W.slot[c_win.run_b[h][q] + 1];
-      } else {  // own cell: partners after i (sorted order)
-        sa = si + 1;
-        sb = S.W.slot[kh + 1];
+    for (int p0 = 0; p0 < total; p0 += 32) {
+      // interval of each lane: the intervals starting inside this chunk mark
+      // their start position; lane l belongs to the latest start <= p0 + l
+      const int rel = cstart - p0;
+      const bool here = lane < nint && rel >= 0 && rel < 32;
+      const unsigned M = __reduce_or_sync(0xffffffffu, here ? (1u << rel) : 0u);
+      const int before = __popc(__ballot_sync(0xffffffffu, lane < nint && rel < 0));
+      const int q = before + __popc(M & le_mask) - 1;
+      const int p = p0 + lane;
+      const int slot = p + __shfl_sync(0xffffffffu, cshift, q);
+      const bool valid = p < total;
+      const float4 c = cand[valid ? slot : W];   // W: sentinel
+      const float dx = c.x - ri.x, dy = c.y - ri.y, dz = c.z - ri.z;
+      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      bool in = r2 < R2lo;
+      const bool band = fabsf(r2 - R2mid) <= R2half && !in;
+      if (__any_sync(0xffffffffu, band)) {
+        if (band) {  // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
+          double4 xi = spos[s];
+          double4 xj = spos[cand_j[slot]];
+          int k = cand_k[slot];
+          double ex = __dadd_rn(__dsub_rn(xj.x, xi.x), S.W.shift[k][0]);
+          double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), S.W.shift[k][1]);
+          double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), S.W.shift[k][2]);
+          double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+          in = d2 <= R2;
+        }
       }
-      for (int b0 = sa; b0 < sb; b0 += 32) {
-        int slot = b0 + lane;
-        bool valid = slot < sb;
-        float4 c = valid ? cand[slot] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
-        float dx = c.x - ri.x, dy = c.y - ri.y, dz = c.z - ri.z;
-        float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        bool in = valid && r2 < R2lo;
-        bool band = valid && !in && r2 <= R2hi;
-        if (__any_sync(0xffffffffu, band)) {
-          if (band) {  // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
-            double4 xi = spos[s];
-            double4 xj = spos[cand_j[slot]];
-            int k = cand_k[slot];
-            double ex = __dadd_rn(__dsub_rn(xj.x, xi.x), S.W.shift[k][0]);
-            double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), S.W.shift[k][1]);
-            double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), S.W.shift[k][2]);
-            double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
-            in = d2 <= R2;
-          }
-        }
-        unsigned m = __ballot_sync(0xffffffffu, in);
-        if (in) {
-          int p = len + __popc(m & lt_mask);
-          if (p < row_cap) row[p] = (uint16_t)slot;
-        }
-        len += __popc(m);
-        if (__any_sync(0xffffffffu, in && r2 <= rcmax)) {  // rare: ~3 bond candidates per row
-          bool bcand = in && r2 <= S.rcand2[ti * nt + __float_as_int(c.w)];
-          unsigned mb = __ballot_sync(0xffffffffu, bcand);
-          if (bcand) {
-            int p = nc + __popc(mb & lt_mask);
-            if (p < cand_cap) crow[p] = cand_j[slot];
-          }
-          nc += __popc(mb);
-        }
+      const unsigned mk = __ballot_sync(0xffffffffu, in);
+      const int pp = len + __popc(mk & lt_mask);
+      if (in && pp < row_cap) row[pp] = (uint16_t)slot;
+      len += __popc(mk);
+      if (__any_sync(0xffffffffu, in && r2 <= rcmax)) {  // rare: ~3 bond candidates per row
+        const bool bcand = in && r2 <= S.rcand2[ti * nt + __float_as_int(c.w)];
+        const unsigned mb = __ballot_sync(0xffffffffu, bcand);
+        const int pc = nc + __popc(mb & lt_mask);
+        if (bcand && pc < cand_cap) crow[pc] = cand_j[slot];
+        nc += __popc(mb);
       }
     }
     if (lane == 0) {
@@ -415,20 +601,11 @@ __device__ __forceinline__ double4 bo_raw(double r, const BOPair& c) {
 // (atom, candidate) pair per round: the exact FMA-free r^2 <= r_bond^2 test,
 // B1-B2, and BO' >= bo_cut.  Rejected candidates are marked -1 in place;
 // kept ones store BO' and are counted per atom (bdeg).
-__device__ __forceinline__ int warp_find(int incl, int t) {
-  // largest q with excl(q) <= t, where incl is the lane's inclusive prefix
-  int q = 0;
-#pragma unroll
-  for (int step = 16; step >= 1; step >>= 1) {
-    int v = __shfl_sync(0xffffffffu, incl, q + step - 1);
-    if (t >= v) q += step;
-  }
-  return q;
-}
-
 __global__ void k_bond_eval(int n, const double4* __restrict__ spos, const int* __restrict__ stype, Grid g,
                             const DevParams* __restrict__ prm, int* __restrict__ bc, const int* __restrict__ bc_len,
-                            double4* __restrict__ bc_raw, int cand_cap, int* __restrict__ bdeg) {
+                            double4* __restrict__ bc_raw, int cand_cap, int* __restrict__ bdeg,
+                            unsigned long long* __restrict__ scan_status, int scan_tiles) {
+  clear_status(scan_status, scan_tiles);
   __shared__ BOPair sbo[NTP_MAX];
   const int nt = prm->nt;
   for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) sbo[t] = prm->bo[t];
@@ -480,8 +657,9 @@ __global__ void k_bond_eval(int n, const double4* __restrict__ spos, const int* 
 // sort key (original partner index) is stored beside each entry.
 __global__ void k_bond_fill(int n, const int* __restrict__ bc, const int* __restrict__ bc_len,
                             const double4* __restrict__ bc_raw, int cand_cap, const int* __restrict__ brow,
-                            const int* __restrict__ perm, int* __restrict__ bdeg, int* __restrict__ bcol,
-                            int* __restrict__ bkey, double* __restrict__ bo, long long bond_cap, Status* st) {
+                            const int* __restrict__ perm, int* __restrict__ bdeg, int* __restrict__ ucol,
+                            int* __restrict__ ukey, int* __restrict__ uown, double4* __restrict__ uraw,
+                            long long bond_cap, Status* st) {
   const int lane = threadIdx.x & 31;
   const int a0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
   if (blockIdx.x == 0 && threadIdx.x == 0) st->bonds = brow[n];
@@ -507,76 +685,47 @@ __global__ void k_bond_fill(int n, const int* __restrict__ bc, const int* __rest
     long long e1 = (long long)brow[s] + atomicSub(&bdeg[s], 1) - 1;
     long long e2 = (long long)brow[j] + atomicSub(&bdeg[j], 1) - 1;
     // each side independently: every entry below the capacity is written
-    if (e1 < bond_cap) {
-      bcol[e1] = j;
-      bkey[e1] = perm[j];
-      double* p1 = bo + 8 * e1;
-      p1[0] = v.x; p1[1] = v.y; p1[2] = v.z; p1[3] = v.w;
-    }
-    if (e2 < bond_cap) {
-      bcol[e2] = s;
-      bkey[e2] = perm[s];
-      double* p2 = bo + 8 * e2;
-      p2[0] = v.x; p2[1] = v.y; p2[2] = v.z; p2[3] = v.w;
-    }
+    if (e1 < bond_cap) { ucol[e1] = j; ukey[e1] = perm[j]; uown[e1] = s; uraw[e1] = v; }
+    if (e2 < bond_cap) { ucol[e2] = s; ukey[e2] = perm[s]; uown[e2] = j; uraw[e2] = v; }
     if (e1 >= bond_cap || e2 >= bond_cap) set_flag(st, ST_BOND_OVF);
   }
 }
 
-// a5 (B3): each row sorted by original partner index (entries staged in
-// local memory, so the loads are independent), then Delta' = sum BO' - Val
-// in that order; the row owner is recorded per entry for k_bond_correct.
-constexpr int ROW_STAGE = 24;
-__global__ void k_bond_sort_delta(int n, const int* __restrict__ brow, const int* __restrict__ stype,
-                                  const DevParams* __restrict__ prm, int* __restrict__ bcol, int* __restrict__ bkey,
-                                  int* __restrict__ bown, double* __restrict__ bo, double2* __restrict__ delta,
-                                  long long bond_cap) {
+// a5 (B3): rows in ascending original-partner order.  One thread per entry
+// (grid-stride over the filled entries): its rank inside its row is the
+// number of smaller keys; it moves the entry to that position of the sorted
+// arrays.  Then one thread per atom sums BO' in that order: Delta'.
+__global__ void k_bond_rank(const int* __restrict__ brow, const int* __restrict__ ucol, const int* __restrict__ ukey,
+                            const int* __restrict__ uown, const double4* __restrict__ uraw, int* __restrict__ bcol,
+                            int* __restrict__ bkey, int* __restrict__ bown, double* __restrict__ bo, long long bond_cap,
+                            const Status* __restrict__ st) {
+  long long B = st->bonds < bond_cap ? st->bonds : bond_cap;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
+    int s = uown[e];
+    int key = ukey[e];
+    int a = brow[s], b = brow[s + 1];
+    if (b > bond_cap) b = (int)bond_cap;
+    int rank = 0;
+    for (int f = a; f < b; ++f) rank += ukey[f] < key;
+    long long o = a + rank;
+    bcol[o] = ucol[e];
+    bkey[o] = key;
+    bown[o] = s;
+    double4 v = uraw[e];
+    double* p = bo + 8 * o;
+    p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w;
+  }
+}
+
+__global__ void k_bond_delta(int n, const int* __restrict__ brow, const int* __restrict__ stype,
+                             const DevParams* __restrict__ prm, const double* __restrict__ bo,
+                             double2* __restrict__ delta, long long bond_cap) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   int a = brow[s], b = brow[s + 1];
   if (b > bond_cap) b = (int)bond_cap;
-  int d = b - a;
   double sum = 0.0;
-  if (d > 0 && d <= ROW_STAGE) {
-    int key[ROW_STAGE], col[ROW_STAGE];
-    double4 v[ROW_STAGE];
-    for (int e = 0; e < d; ++e) {
-      key[e] = bkey[a + e];
-      col[e] = bcol[a + e];
-      const double* p = bo + 8 * (int64_t)(a + e);
-      v[e] = make_double4(p[0], p[1], p[2], p[3]);
-    }
-    for (int e = 0; e < d; ++e) {  // rank of each entry (keys are distinct)
-      int rank = 0;
-      for (int f = 0; f < d; ++f) rank += key[f] < key[e];
-      int o = a + rank;
-      bcol[o] = col[e];
-      bkey[o] = key[e];
-      bown[o] = s;
-      double* p = bo + 8 * (int64_t)o;
-      p[0] = v[e].x; p[1] = v[e].y; p[2] = v[e].z; p[3] = v[e].w;
-    }
-    for (int e = a; e < b; ++e) sum += bo[8 * (int64_t)e + 3];  // ascending partner order
-  } else if (d > ROW_STAGE) {  // rare: in-place insertion sort
-    for (int i = a + 1; i < b; ++i) {
-      int kv = bkey[i], cv = bcol[i];
-      double r0 = bo[8 * (int64_t)i], r1 = bo[8 * (int64_t)i + 1], r2 = bo[8 * (int64_t)i + 2], r3 = bo[8 * (int64_t)i + 3];
-      int j = i - 1;
-      while (j >= a && bkey[j] > kv) {
-        bkey[j + 1] = bkey[j];
-        bcol[j + 1] = bcol[j];
-        for (int q = 0; q < 4; ++q) bo[8 * (int64_t)(j + 1) + q] = bo[8 * (int64_t)j + q];
-        --j;
-      }
-      bkey[j + 1] = kv; bcol[j + 1] = cv;
-      bo[8 * (int64_t)(j + 1)] = r0; bo[8 * (int64_t)(j + 1) + 1] = r1;
-      bo[8 * (int64_t)(j + 1) + 2] = r2; bo[8 * (int64_t)(j + 1) + 3] = r3;
-    }
-    for (int e = a; e < b; ++e) {
-      bown[e] = s;
-      sum += bo[8 * (int64_t)e + 3];
-    }
-  }
+  for (int e = a; e < b; ++e) sum += bo[8 * (int64_t)e + 3];
   int t = stype[s];
   delta[s] = make_double2(sum - prm->val[t], sum - prm->val_boc[t]);
 }
@@ -769,10 +918,19 @@ __device__ __forceinline__ void nb_pair(double r2, double qiqj, const NBPair& c,
 }
 
 constexpr int NB_THREADS = 256;
+#ifndef NB_ILP
+#define NB_ILP 1
+#endif
+#ifndef NB_MINB
+#define NB_MINB 3
+#endif
 
+constexpr int NB_MAX_ROWS = 256;   // rows of one (block, split) work unit
 struct NBSmem {
   WinSmem W;
-  double red[2][NB_THREADS / 32];
+  int next_row;
+  int order[NB_MAX_ROWS];        // row window slots, longest row first
+  int rlen[NB_MAX_ROWS];
 };
 
 // One CTA per home block (Alg. 2, re-designed): a warp per
@@ -781,10 +939,10 @@ struct NBSmem {
 // window (the block's private force array, the GPU form of the paper's
 // thread-private tprivForce) and flushed to the global sorted force array
 // once per block.  Energies: per-block partials reduced later in fixed order.
-__global__ void __launch_bounds__(NB_THREADS, 3) k_nonbonded(Grid g, const int* __restrict__ cell_start,
+__global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const int* __restrict__ cell_start,
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
-    double* __restrict__ sfx, double* __restrict__ sfy, double* __restrict__ sfz, double* __restrict__ epart,
+    double* __restrict__ sfx, double* __restrict__ sfy, double* __restrict__ sfz, double2* __restrict__ erow,
     int nsplit, Status* st) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
@@ -809,27 +967,67 @@ __global__ void __launch_bounds__(NB_THREADS, 3) k_nonbonded(Grid g, const int* 
     if (threadIdx.x == 0) {
       set_flag(st, ST_WIN_OVF);
       atomicMax(&st->max_window, W);
-      epart[2 * blockIdx.x] = 0.0;
-      epart[2 * blockIdx.x + 1] = 0.0;
     }
     return;
   }
   const int nwu = c_win.nwu;
-  for (int k = warp; k < nwu; k += nwarp) {
-    int s0 = S.W.start[k], c = S.W.cnt[k], b0 = S.W.slot[k];
-    for (int a = lane; a < c; a += 32) {
-      slot_j[b0 + a] = s0 + a;
-      slot_k[b0 + a] = (unsigned char)k;
-    }
-  }
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
+    const int k = cell_of_slot(S.W, nwu, t);
+    slot_j[t] = S.W.start[k] + (t - S.W.slot[k]);
+    slot_k[t] = (unsigned char)k;
     fx[t] = 0.0; fy[t] = 0.0; fz[t] = 0.0;
   }
+  // this CTA's rows: split, split + nsplit, ... of the block (home sub-cell
+  // order), ranked longest first (rows are 90-370 pairs): longest-processing-
+  // time-first keeps the warps busy until the flush barrier
+  int nrows_blk = 0;
+  for (int h = 0; h < NHOME; ++h)
+    if (S.W.home_ok[h]) nrows_blk += S.W.cnt[c_win.home_k[h]];
+  const int nrows = nrows_blk > split ? (nrows_blk - split + nsplit - 1) / nsplit : 0;
+  const int nsorted = nrows < NB_MAX_ROWS ? nrows : NB_MAX_ROWS;
+  if (threadIdx.x == 0) S.next_row = 0;
+  constexpr int RPT = NB_MAX_ROWS / NB_THREADS;   // rows per thread in the ranking
+  int my_row[RPT], my_len[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int t = threadIdx.x + u * NB_THREADS;
+    my_row[u] = 0; my_len[u] = 0;
+    if (t < nsorted) {
+      int h, si;
+      row_of(S.W, split + t * nsplit, h, si);
+      my_row[u] = si;
+      my_len[u] = nbr_len[slot_j[si]];
+      S.rlen[t] = my_len[u];
+    }
+  }
   __syncthreads();
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int me = threadIdx.x + u * NB_THREADS;
+    if (me < nsorted) {
+      int rank = 0;
+      for (int t = 0; t < nsorted; ++t) {
+        const int lt = S.rlen[t];
+        rank += (lt > my_len[u]) || (lt == my_len[u] && t < me);
+      }
+      S.order[rank] = my_row[u];
+    }
+  }
+  __syncthreads();
+  const bool has_shift = S.W.has_shift != 0;
   double ev_acc = 0.0, ec_acc = 0.0;
-  for (int r = split * nwarp + warp;; r += nsplit * nwarp) {
-    int h, si;
-    if (!row_of(S.W, r, h, si)) break;
+  for (;;) {
+    int m = 0;
+    if (lane == 0) m = atomicAdd(&S.next_row, 1);
+    m = __shfl_sync(0xffffffffu, m, 0);
+    if (m >= nrows) break;
+    int si;
+    if (m < nsorted) {
+      si = S.order[m];
+    } else {
+      int h;
+      row_of(S.W, split + m * nsplit, h, si);
+    }
     const int s = slot_j[si];
     const double4 xi = spos[s];
     const int ti = stype[s];
@@ -837,27 +1035,64 @@ __global__ void __launch_bounds__(NB_THREADS, 3) k_nonbonded(Grid g, const int* 
     const int len = nbr_len[s];
     const uint16_t* row = nbr + (int64_t)s * row_cap;
     double fix = 0.0, fiy = 0.0, fiz = 0.0;
-    for (int b0 = 0; b0 < len; b0 += 32) {
-      int e = b0 + lane;
+    // software pipeline: the next chunk's neighbour data is loaded while the
+    // current chunk is evaluated; NB_ILP independent pairs per lane per chunk
+    int slot_n[NB_ILP], k_n[NB_ILP], tj_n[NB_ILP];
+    double4 xj_n[NB_ILP];
+#pragma unroll
+    for (int u = 0; u < NB_ILP; ++u) {
+      const int e = u * 32 + lane;
+      slot_n[u] = 0; k_n[u] = 0; tj_n[u] = 0; xj_n[u] = make_double4(0, 0, 0, 0);
       if (e < len) {
-        int slot = row[e];
-        int j = slot_j[slot];
-        int k = slot_k[slot];
-        double4 xj = spos[j];
-        int tj = stype[j];
-        double dx = (xj.x - xi.x) + S.W.shift[k][0];
-        double dy = (xj.y - xi.y) + S.W.shift[k][1];
-        double dz = (xj.z - xi.z) + S.W.shift[k][2];
-        double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        double ev, ec, gg;
-        nb_pair(r2, cqi * xj.w, pc[ti * nt + tj], kc, ET, LT, ev, ec, gg);
-        ev_acc += ev;
-        ec_acc += ec;
-        double gx = gg * dx, gy = gg * dy, gz = gg * dz;
-        fix += gx; fiy += gy; fiz += gz;
-        atomicAdd(&fx[slot], -gx);
-        atomicAdd(&fy[slot], -gy);
-        atomicAdd(&fz[slot], -gz);
+        slot_n[u] = row[e];
+        const int j = slot_j[slot_n[u]];
+        k_n[u] = slot_k[slot_n[u]];
+        xj_n[u] = spos[j];
+        tj_n[u] = stype[j];
+      }
+    }
+    for (int b0 = 0; b0 < len; b0 += 32 * NB_ILP) {
+      int slot[NB_ILP], kk[NB_ILP], tj[NB_ILP];
+      double4 xj[NB_ILP];
+#pragma unroll
+      for (int u = 0; u < NB_ILP; ++u) {
+        slot[u] = slot_n[u]; kk[u] = k_n[u]; tj[u] = tj_n[u]; xj[u] = xj_n[u];
+        const int en = b0 + 32 * NB_ILP + u * 32 + lane;
+        if (en < len) {
+          slot_n[u] = row[en];
+          const int j = slot_j[slot_n[u]];
+          k_n[u] = slot_k[slot_n[u]];
+          xj_n[u] = spos[j];
+          tj_n[u] = stype[j];
+        }
+      }
+      double ev[NB_ILP], ec[NB_ILP], gg[NB_ILP], dx[NB_ILP], dy[NB_ILP], dz[NB_ILP];
+#pragma unroll
+      for (int u = 0; u < NB_ILP; ++u) {
+        const bool act = b0 + u * 32 + lane < len;
+        dx[u] = xj[u].x - xi.x;
+        dy[u] = xj[u].y - xi.y;
+        dz[u] = xj[u].z - xi.z;
+        if (has_shift) {   // block-uniform
+          dx[u] += S.W.shift[kk[u]][0];
+          dy[u] += S.W.shift[kk[u]][1];
+          dz[u] += S.W.shift[kk[u]][2];
+        }
+        double r2 = act ? fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u])) : 1.0;
+        nb_pair(r2, cqi * xj[u].w, pc[ti * nt + tj[u]], kc, ET, LT, ev[u], ec[u], gg[u]);
+        if (!act) { ev[u] = 0.0; ec[u] = 0.0; gg[u] = 0.0; }
+      }
+#pragma unroll
+      for (int u = 0; u < NB_ILP; ++u) {
+        if (b0 + u * 32 + lane < len) {
+          ev_acc += ev[u];
+          ec_acc += ec[u];
+          double gx = gg[u] * dx[u], gy = gg[u] * dy[u], gz = gg[u] * dz[u];
+          fix += gx; fiy += gy; fiz += gz;
+          atomicAdd(&fx[slot[u]], -gx);
+          atomicAdd(&fy[slot[u]], -gy);
+          atomicAdd(&fz[slot[u]], -gz);
+        }
       }
     }
 #pragma unroll
@@ -866,11 +1101,19 @@ __global__ void __launch_bounds__(NB_THREADS, 3) k_nonbonded(Grid g, const int* 
       fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
       fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ev_acc += __shfl_xor_sync(0xffffffffu, ev_acc, o);
+      ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
+    }
     if (lane == 0) {
       atomicAdd(&fx[si], fix);
       atomicAdd(&fy[si], fiy);
       atomicAdd(&fz[si], fiz);
+      erow[s] = make_double2(ev_acc, ec_acc);   // per-row energy: reduced later in row order
     }
+    ev_acc = 0.0;
+    ec_acc = 0.0;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
@@ -881,23 +1124,6 @@ __global__ void __launch_bounds__(NB_THREADS, 3) k_nonbonded(Grid g, const int* 
       atomicAdd(&sfy[j], b);
       atomicAdd(&sfz[j], c);
     }
-  }
-  // deterministic block energy partial
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ev_acc += __shfl_xor_sync(0xffffffffu, ev_acc, o);
-    ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
-  }
-  if (lane == 0) {
-    S.red[0][warp] = ev_acc;
-    S.red[1][warp] = ec_acc;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int w = 0; w < nwarp; ++w) { a += S.red[0][w]; b += S.red[1][w]; }
-    epart[2 * blockIdx.x] = a;
-    epart[2 * blockIdx.x + 1] = b;
   }
 }
 
@@ -915,15 +1141,20 @@ __global__ void k_finalize_forces(int n, const int* __restrict__ iperm, const do
   force[3 * (int64_t)i + 2] = c;
 }
 
-// fixed-order energy reduction over block partials (one CTA)
-constexpr int FIN_THREADS = 1024;
-__global__ void __launch_bounds__(FIN_THREADS) k_finalize_energy(int nblock, const double* __restrict__ epart,
-                                                                 double* __restrict__ energy, Status* st) {
+// fixed-order energy reduction over the per-row energies: each CTA sums a
+// fixed contiguous range, the last CTA to finish sums the CTA partials in
+// index order (bitwise reproducible)
+constexpr int FIN_THREADS = 512;
+constexpr int FIN_ITEMS = 16;
+__global__ void __launch_bounds__(FIN_THREADS) k_finalize_energy(int n, const double2* __restrict__ erow,
+    double* __restrict__ part, unsigned* __restrict__ ticket, double* __restrict__ energy, Status* st) {
   __shared__ double red[2][FIN_THREADS / 32];
+  __shared__ bool last;
   double a = 0.0, b = 0.0;
-  for (int t = threadIdx.x; t < nblock; t += FIN_THREADS) {
-    a += epart[2 * t];
-    b += epart[2 * t + 1];
+  int64_t base = (int64_t)blockIdx.x * FIN_THREADS * FIN_ITEMS;
+  for (int q = 0; q < FIN_ITEMS; ++q) {
+    int64_t i = base + (int64_t)q * FIN_THREADS + threadIdx.x;
+    if (i < n) { double2 v = erow[i]; a += v.x; b += v.y; }
   }
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -936,8 +1167,23 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_energy(int nblock, con
   if (threadIdx.x == 0) {
     double x = 0.0, y = 0.0;
     for (int k = 0; k < FIN_THREADS / 32; ++k) { x += red[0][k]; y += red[1][k]; }
+    part[2 * blockIdx.x] = x;
+    part[2 * blockIdx.x + 1] = y;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (unsigned k = 0; k < gridDim.x; ++k) {
+      x += ((volatile double*)part)[2 * k];
+      y += ((volatile double*)part)[2 * k + 1];
+    }
     energy[0] = x;
     energy[1] = y;
+    *ticket = 0u;   // ready for the next call
     if (!(isfinite(x) && isfinite(y))) set_flag(st, ST_NONFINITE_OUT);
   }
 }

@@ -24,7 +24,9 @@ constexpr int MAX_SPLIT = 8;
 // few home blocks to fill 148 SMs, so each block's rows are split over
 // several CTAs (each builds the same window)
 int choose_split(int nblock) {
-  int target = 148 * 8;
+  int per_sm = 8;
+  if (const char* e = getenv("REAX_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));   // tuning experiments
+  int target = 148 * per_sm;
   int s = (target + nblock - 1) / std::max(nblock, 1);
   return std::max(1, std::min(MAX_SPLIT, s));
 }
@@ -60,12 +62,20 @@ WindowTables make_tables() {
       T.wu[T.nwu++] = w;
     }
   }
+  if (T.nwu > NWU_MAX) abort();   // compile-time geometry constants are inconsistent
   for (int h = 0; h < NHOME; ++h) {
     int hv[3] = {h % HB, (h / HB) % HB, h / (HB * HB)};
     auto wk = [&](int ox, int oy, int oz) {
       return T.widx[(hv[0] + SR + ox) + WB * ((hv[1] + SR + oy) + WB * (hv[2] + SR + oz))];
     };
     T.home_k[h] = wk(0, 0, 0);
+    for (int oz = -SR; oz <= SR; ++oz)
+      for (int oy = -SR; oy <= SR; ++oy)
+        for (int ox = -SR; ox <= SR; ++ox) {
+          if (!(forward_offset(ox, oy, oz) || (ox == 0 && oy == 0 && oz == 0))) continue;
+          int kk = wk(ox, oy, oz);
+          T.mask[h][kk / 32] |= 1u << (kk % 32);
+        }
     std::vector<std::pair<int, int>> runs;
     for (int oz = 0; oz <= SR; ++oz)
       for (int oy = -SR; oy <= SR; ++oy) {
@@ -74,6 +84,11 @@ WindowTables make_tables() {
         if (oz == 0 && oy == 0) oxa = 1;
         runs.push_back({wk(oxa, oy, oz), wk(oxb, oy, oz)});
       }
+    T.nrun1[h] = (int)runs.size();
+    for (size_t q = 0; q < runs.size(); ++q) {
+      T.run1_a[h][q] = runs[q].first;
+      T.run1_b[h][q] = runs[q].second;
+    }
     std::sort(runs.begin(), runs.end());
     std::vector<std::pair<int, int>> merged;
     for (auto& r : runs) {
@@ -317,9 +332,18 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
   t.sfx = (double*)take(sizeof(double) * N);
   t.sfy = (double*)take(sizeof(double) * N);
   t.sfz = (double*)take(sizeof(double) * N);
-  t.epart = (double*)take(sizeof(double) * 2 * MAX_SPLIT * (size_t)std::max(g.nblock, 1));
+  t.erow = (double2*)take(sizeof(double2) * N);
+  t.epart = (double*)take(sizeof(double) * 2 * ((size_t)nblk((int64_t)N, FIN_THREADS * FIN_ITEMS) + 1));
+  t.ticket = (unsigned*)take(sizeof(unsigned) * 4);
+  t.ucol = (int*)take(sizeof(int) * (size_t)c.bond_cap);
+  t.ukey = (int*)take(sizeof(int) * (size_t)c.bond_cap);
+  t.uown = (int*)take(sizeof(int) * (size_t)c.bond_cap);
+  t.uraw = (double4*)take(sizeof(double4) * (size_t)c.bond_cap);
   t.scan_tmp = (long long*)take(sizeof(long long) * nscan);
   t.exp_off = (long long*)take(sizeof(long long) * (N + 1));
+  t.lb_status = (unsigned long long*)take(sizeof(unsigned long long) *
+                                          ((size_t)nblk(std::max<int64_t>((int64_t)N + 1, (int64_t)g.ncell + 1), LB_TILE) + 1));
+  t.lb_ticket = (unsigned*)take(sizeof(unsigned) * 4);
   t.prm = (DevParams*)take(sizeof(DevParams));
   t.st = (Status*)take(sizeof(Status));
   t.h_pos = (double*)take(sizeof(double) * 3 * N);
@@ -365,6 +389,7 @@ struct reax_ctx {
   int launches_step = 0;
   int launches_cur = 0;
   int nsplit = 1;
+  int nsplit_nbr = 1;
 };
 
 namespace {
@@ -388,24 +413,40 @@ struct Timer {
   cudaStream_t s;
   cudaEvent_t a = nullptr;
   int l0;
+  // inside stream capture the events become external event-record nodes, so
+  // a replayed graph still reports per-kernel times (reax_kernel_ms, peek mode)
+  static void record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
+  }
   Timer(reax_ctx* c_, int k_, cudaStream_t s_) : c(c_), k(k_), s(s_) {
     l0 = c->launches_cur;
     if (c->timing) {
       a = take_event(c);
-      cudaEventRecord(a, s);
+      record(a, s);
     }
   }
   ~Timer() {
     c->launches_acc[k] += c->launches_cur - l0;
     if (c->timing) {
       cudaEvent_t b = take_event(c);
-      cudaEventRecord(b, s);
+      record(b, s);
       c->ev_pending[k].push_back({a, b});
     }
   }
 };
 
 #define LAUNCH(ctx) (++(ctx)->launches_cur)
+
+// one-launch scan for the hot path (status cleared by the producing kernel)
+cudaError_t scan1(reax_ctx* c, const int* in, int64_t n, int* out, unsigned long long* status, cudaStream_t s) {
+  if (n <= 0) return cudaMemsetAsync(out, 0, sizeof(int), s);
+  k_scan_lookback<<<nblk(n, LB_TILE), LB_THREADS, 0, s>>>(in, (int)n, out, status, c->w.lb_ticket);
+  LAUNCH(c);
+  return cudaGetLastError();
+}
 
 template <typename TI, typename TO>
 cudaError_t scan(reax_ctx* c, const TI* in, int64_t n, TO* out, cudaStream_t s) {
@@ -488,7 +529,10 @@ reax_status upload_params(reax_ctx* c, const reax_params* p, const reax_cutoffs*
   return REAX_OK;
 }
 
-size_t nbr_smem(int wcap) { return (size_t)wcap * (sizeof(float4) + sizeof(int) + 1) + 64; }
+size_t nbr_smem(int wcap, int row_cap = 0) {
+  (void)row_cap;
+  return (size_t)(wcap + 32) * (sizeof(float4) + sizeof(int) + 1) + 64;
+}
 size_t nb_smem(int wcap, int nt = NT_MAX) { return sizeof(double) * (EXP_TBL + 2 * LOG_TBL) + sizeof(NBPair) * nt * nt + (size_t)wcap * (3 * sizeof(double) + sizeof(int) + 1) + 64; }
 size_t exp_smem(int wcap) { return (size_t)wcap * sizeof(int) + 64; }
 
@@ -522,9 +566,11 @@ reax_status do_build_lists(reax_ctx* c, int64_t n, const double* pos, const int*
   if (N > 0) {
     {
       Timer t(c, 0, s);
-      k_bin<<<nblk(N, TPB), TPB, 0, s>>>(N, pos, type, g, prm->ntypes, w.cell_of, w.cell_cnt, w.st);
+      const int ctiles = nblk(g.ncell, LB_TILE);
+      k_bin<<<nblk(std::max<int64_t>(N, ctiles), TPB), TPB, 0, s>>>(N, pos, type, g, prm->ntypes, w.cell_of, w.cell_cnt,
+                                                                   w.st, w.lb_status, ctiles);
       LAUNCH(c);
-      scan<int, int>(c, w.cell_cnt, g.ncell, w.cell_start, s);
+      scan1(c, w.cell_cnt, g.ncell, w.cell_start, w.lb_status, s);
       k_scatter<<<nblk(N, TPB), TPB, 0, s>>>(N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
       LAUNCH(c);
       k_cell_gather<<<nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s>>>(g.ncell, w.cell_start, w.perm, pos, type, g,
@@ -533,22 +579,25 @@ reax_status do_build_lists(reax_ctx* c, int64_t n, const double* pos, const int*
     }
     {
       Timer t(c, 1, s);
-      k_nbr_build<<<g.nblock * c->nsplit, NBR_THREADS, nbr_smem(c->cap.window_cap), s>>>(
+      k_nbr_build<<<g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s>>>(
           g, w.cell_start, w.sloc, w.spos, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, w.bc, w.bc_len,
-          c->cap.cand_cap, c->cap.window_cap, c->nsplit, w.st);
+          c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st);
       LAUNCH(c);
     }
     {
       Timer t(c, 2, s);
-      k_bond_eval<<<nblk(N, TPB), TPB, 0, s>>>(N, w.spos, w.stype, g, w.prm, w.bc, w.bc_len, w.bc_raw,
-                                              c->cap.cand_cap, w.bdeg);
+      const int btiles = nblk(N, LB_TILE);
+      k_bond_eval<<<nblk(std::max<int64_t>(N, (int64_t)btiles * 32), TPB), TPB, 0, s>>>(
+          N, w.spos, w.stype, g, w.prm, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.bdeg, w.lb_status, btiles);
       LAUNCH(c);
-      scan<int, int>(c, w.bdeg, N, w.brow, s);
+      scan1(c, w.bdeg, N, w.brow, w.lb_status, s);
       k_bond_fill<<<nblk(N, TPB), TPB, 0, s>>>(N, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.brow, w.perm, w.bdeg,
-                                              w.bcol, w.bkey, w.bo, c->cap.bond_cap, w.st);
+                                              w.ucol, w.ukey, w.uown, w.uraw, c->cap.bond_cap, w.st);
       LAUNCH(c);
-      k_bond_sort_delta<<<nblk(N, 128), 128, 0, s>>>(N, w.brow, w.stype, w.prm, w.bcol, w.bkey, w.bown, w.bo, w.delta,
-                                                    c->cap.bond_cap);
+      k_bond_rank<<<148 * 4, TPB, 0, s>>>(w.brow, w.ucol, w.ukey, w.uown, w.uraw, w.bcol, w.bkey, w.bown, w.bo,
+                                         c->cap.bond_cap, w.st);
+      LAUNCH(c);
+      k_bond_delta<<<nblk(N, TPB), TPB, 0, s>>>(N, w.brow, w.stype, w.prm, w.bo, w.delta, c->cap.bond_cap);
       LAUNCH(c);
     }
   }
@@ -607,14 +656,15 @@ reax_status do_nonbonded(reax_ctx* c, int64_t n, const double* pos, const int* t
     Timer t(c, 4, s);
     k_nonbonded<<<g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, prm->ntypes), s>>>(
         g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy,
-        w.sfz, w.epart, c->nsplit, w.st);
+        w.sfz, w.erow, c->nsplit, w.st);
     LAUNCH(c);
   }
   {
     Timer t(c, 5, s);
     k_finalize_forces<<<nblk(N, TPB), TPB, 0, s>>>(N, w.iperm, w.sfx, w.sfy, w.sfz, force, w.st);
     LAUNCH(c);
-    k_finalize_energy<<<1, FIN_THREADS, 0, s>>>(g.nblock * c->nsplit, w.epart, energy, w.st);
+    k_finalize_energy<<<nblk(N, FIN_THREADS * FIN_ITEMS), FIN_THREADS, 0, s>>>(N, w.erow, w.epart, w.ticket, energy,
+                                                                               w.st);
     LAUNCH(c);
   }
   if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
@@ -702,9 +752,9 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  size_t s1 = nbr_smem(c.window_cap) + sizeof(NbrSmem), s2 = nb_smem(c.window_cap) + sizeof(NBSmem);
+  size_t s1 = nbr_smem(c.window_cap, c.row_cap) + sizeof(NbrSmem), s2 = nb_smem(c.window_cap) + sizeof(NBSmem);
   if ((size_t)maxsm < s1 || (size_t)maxsm < s2) return REAX_ERR_CAPACITY;
-  if (cudaFuncSetAttribute(k_nbr_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nbr_smem(c.window_cap)) != cudaSuccess ||
+  if (cudaFuncSetAttribute(k_nbr_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nbr_smem(c.window_cap, c.row_cap)) != cudaSuccess ||
       cudaFuncSetAttribute(k_nonbonded, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nb_smem(c.window_cap)) != cudaSuccess ||
       cudaFuncSetAttribute(k_export_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exp_smem(c.window_cap)) != cudaSuccess)
     return REAX_ERR_CUDA;
@@ -715,6 +765,8 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   ctx->n = n;
   ctx->cap = c;
   ctx->nsplit = choose_split(g.nblock);
+  ctx->nsplit_nbr = ctx->nsplit;
+  if (const char* e = getenv("REAX_NBR_SPLIT")) ctx->nsplit_nbr = std::max(1, std::min(MAX_SPLIT, atoi(e)));
   ctx->cut = *cut;
   ctx->prm_valid = false;
   ctx->lists_ok = ctx->bonds_ok = false;
@@ -722,6 +774,8 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   cudaError_t e = cudaMemset(ctx->w.cell_cnt, 0, sizeof(int) * (g.ncell + 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.bdeg, 0, sizeof(int) * (std::max<int64_t>(n, 1) + 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.st, 0, sizeof(Status));
+  if (e == cudaSuccess) e = cudaMemset(ctx->w.ticket, 0, sizeof(unsigned) * 4);
+  if (e == cudaSuccess) e = cudaMemset(ctx->w.lb_ticket, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return REAX_ERR_CUDA;
   ctx->bound = true;
@@ -811,6 +865,20 @@ reax_status reax_set_timing(reax_ctx* ctx, int enable) {
 
 reax_status reax_kernel_ms(reax_ctx* ctx, double ms[REAX_NKERNELS], int64_t launches[REAX_NKERNELS], int reset) {
   if (!ctx) return REAX_ERR_ARG;
+  if (reset == 2) {  // peek: elapsed time of the recorded events, left in place (graph replays)
+    for (int k = 0; k < REAX_NKERNELS; ++k) {
+      double t = 0.0;
+      for (auto& p : ctx->ev_pending[k]) {
+        if (cudaEventSynchronize(p.second) != cudaSuccess) return REAX_ERR_CUDA;
+        float f = 0.f;
+        if (cudaEventElapsedTime(&f, p.first, p.second) != cudaSuccess) return REAX_ERR_CUDA;
+        t += f;
+      }
+      if (ms) ms[k] = t;
+      if (launches) launches[k] = ctx->launches_acc[k];
+    }
+    return REAX_OK;
+  }
   for (int k = 0; k < REAX_NKERNELS; ++k) {
     for (auto& p : ctx->ev_pending[k]) {
       if (cudaEventSynchronize(p.second) != cudaSuccess) return REAX_ERR_CUDA;
