@@ -445,10 +445,16 @@ __global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int*
     }
     return;
   }
-  // staging, flattened over slots so that all global loads are in flight at once
+  // slot -> window cell map (thread per cell), then staging flattened over
+  // slots so that all global loads are in flight at once
+  for (int k = threadIdx.x; k < nwu; k += blockDim.x) {
+    const int b0 = S.W.slot[k], c = S.W.cnt[k];
+    for (int a = 0; a < c; ++a) cand_k[b0 + a] = (unsigned char)k;
+  }
+  __syncthreads();
 #pragma unroll 4
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
-    const int k = cell_of_slot(S.W, nwu, t);
+    const int k = cand_k[t];
     const int j = S.W.start[k] + (t - S.W.slot[k]);
     const int wb = c_win.wu[k];
     // cell origin relative to the block origin: (w - SR) h per axis
@@ -458,7 +464,6 @@ __global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int*
     const float4 l = sloc[j];
     cand[t] = make_float4(l.x + ox, l.y + oy, l.z + oz, l.w);
     cand_j[t] = j;
-    cand_k[t] = (unsigned char)k;
   }
   if (threadIdx.x < 32) cand[W + threadIdx.x] = make_float4(1e30f, 1e30f, 1e30f, 0.f);  // sentinel
   __syncthreads();
@@ -799,21 +804,34 @@ struct NBConst {
 // ---- branch-free fp64 math for the nonbonded pair (inputs in known, finite,
 // normal ranges; ~1-2 ulp).  Tables live in shared memory.
 constexpr int EXP_TBL = 64;    // 2^(j/64)
+// polynomial / reduction constants as constant-bank operands (ptxas otherwise
+// re-materialises 64-bit literals with register moves inside the pair loop)
+__constant__ double c_nb[24] = {
+    0x1.71547652b82fep+6,      // 0  64 / ln 2
+    6755399441055744.0,        // 1  1.5 * 2^52
+    0x1.62e42fee00000p-7,      // 2  ln2_hi / 64
+    0x1.a39ef35793c76p-39,     // 3  ln2_lo / 64
+    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5,   // 4-7  exp polynomial
+    -1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5,   // 8-12 log1p polynomial
+    0x1.62e42fee00000p-1,      // 13 ln2_hi
+    0x1.a39ef35793c76p-33,     // 14 ln2_lo
+    0.375, 2.0 / 9.0, 1.0 / 3.0,   // 15-17 Halley rsqrt / rcbrt
+    20.0, -70.0, 84.0, -35.0, -140.0,   // 18-22 taper
+    1.0};                      // 23
+
 constexpr int LOG_TBL = 128;   // {1/c_j, -log(1/c_j)}, c_j = 1 + (j + 1/2)/128
 
 // e^x for |x| < 700: x = k ln2/64 + r, |r| <= ln2/128; e^r - 1 by a degree-5
 // polynomial (error r^6/720 < 4e-17); 2^(k/64) = 2^(k>>6) * T[k & 63].
 __device__ __forceinline__ double fexp(double x, const double* __restrict__ T) {
-  const double L2E64 = 0x1.71547652b82fep+6;          // 64 / ln 2
-  const double SHIFT = 6755399441055744.0;             // 1.5 * 2^52
-  const double LN2_64_HI = 0x1.62e42fee00000p-7; // ln2_hi / 64 (fdlibm split)
-  const double LN2_64_LO = 0x1.a39ef35793c76p-39; // ln2_lo / 64
-  double t = fma(x, L2E64, SHIFT);
-  double kd = t - SHIFT;
+  double t = fma(x, c_nb[0], c_nb[1]);
+  double kd = t - c_nb[1];
   int k = __double2loint(t);
-  double r = fma(kd, -LN2_64_HI, x);
-  r = fma(kd, -LN2_64_LO, r);
-  double q = fma(fma(fma(r, 1.0 / 120.0, 1.0 / 24.0), r, 1.0 / 6.0), r, 0.5);
+  double r = fma(kd, -c_nb[2], x);
+  r = fma(kd, -c_nb[3], r);
+  double q = fma(r, c_nb[4], c_nb[5]);
+  q = fma(q, r, c_nb[6]);
+  q = fma(q, r, c_nb[7]);
   double p = fma(q, r * r, r);
   double tj = T[k & (EXP_TBL - 1)];
   double y = fma(tj, p, tj);
@@ -823,18 +841,36 @@ __device__ __forceinline__ double fexp(double x, const double* __restrict__ T) {
 // ln x for finite normal x > 0: x = 2^e m, m in [1,2); m/c_j = 1 + r with
 // |r| < 2^-8; log1p(r) by a degree-6 polynomial (error < 3e-18).
 __device__ __forceinline__ double flog(double x, const double2* __restrict__ LT) {
-  const double LN2_HI = 0x1.62e42fee00000p-1;
-  const double LN2_LO = 0x1.a39ef35793c76p-33;
   int hi = __double2hiint(x);
   int e = (hi >> 20) - 1023;
   int j = (hi >> 13) & (LOG_TBL - 1);
   double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(x));
   double2 t = LT[j];
-  double r = fma(m, t.x, -1.0);
-  double q = fma(fma(fma(fma(r, -1.0 / 6.0, 1.0 / 5.0), r, -0.25), r, 1.0 / 3.0), r, -0.5);
+  double r = fma(m, t.x, -c_nb[23]);
+  double q = fma(r, c_nb[8], c_nb[9]);
+  q = fma(q, r, c_nb[10]);
+  q = fma(q, r, c_nb[11]);
+  q = fma(q, r, c_nb[12]);
   double p = fma(q, r * r, r);
-  double ed = (double)e;
-  return fma(ed, LN2_HI, t.y) + fma(ed, LN2_LO, p);
+  // (double)e without I2F.F64 (an XU op): 2^52 + 2^31 + e, minus 2^52 + 2^31
+  double ed = __hiloint2double(0x43300000, e ^ 0x80000000) - 4503601774854144.0;
+  return fma(ed, c_nb[13], t.y) + fma(ed, c_nb[14], p);
+}
+
+// ---- XU-free seeds.  The XU (MUFU + int/fp64 conversions) is the scarce unit
+// of this kernel (ncu: xu pipe 82% with MUFU seeds and F2F/I2F conversions), so
+// float <-> double conversions are done with integer bit operations (inputs are
+// positive normal numbers in a modest range) and seeds come from bit hacks plus
+// FMA-pipe Newton steps.
+__device__ __forceinline__ float d2f_pos(double x) {       // truncating, positive normal x
+  const int hi = __double2hiint(x), lo = __double2loint(x);
+  const int e = ((hi >> 20) & 0x7ff) - 1023 + 127;
+  return __int_as_float((e << 23) | ((hi & 0xfffff) << 3) | ((unsigned)lo >> 29));
+}
+__device__ __forceinline__ double f2d_pos(float f) {        // exact, positive normal f
+  const int b = __float_as_int(f);
+  const int e = ((b >> 23) & 0xff) - 127 + 1023;
+  return __hiloint2double((e << 20) | ((b & 0x7fffff) >> 3), b << 29);
 }
 
 // approximate seeds from the MUFU unit, then one Halley-type correction:
@@ -843,23 +879,34 @@ __device__ __forceinline__ double flog(double x, const double2* __restrict__ LT)
 __device__ __forceinline__ double frsqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x * y, y, 1.0);
-  return fma(y * e, fma(e, 0.375, 0.5), y);
+  double e = fma(-x * y, y, c_nb[23]);
+  return fma(y * e, fma(e, c_nb[15], c_nb[7]), y);
 }
 __device__ __forceinline__ double frcp(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  return fma(y * e, 1.0 + e, y);
+  // float seed: magic constant (rel. err < 6%), two Newton steps in fp32
+  const float xf = d2f_pos(x);
+  float yf = __int_as_float(0x7ef311c3 - __float_as_int(xf));
+  yf = yf * fmaf(-xf, yf, 2.0f);
+  yf = yf * fmaf(-xf, yf, 2.0f);
+  yf = yf * fmaf(-xf, yf, 2.0f);   // ~1e-7 (fp32 rounding)
+  double y = f2d_pos(yf);
+  double e = fma(-x, y, c_nb[23]);
+  return fma(y * e, c_nb[23] + e, y);   // 1/(1-e) = 1 + e + e^2: ~1e-21
 }
 __device__ __forceinline__ double frcbrt(double x) {
-  float xf = (float)x, yf;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(xf));
-  yf *= -1.0f / 3.0f;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(yf));
-  double y = (double)yf;
-  double e = fma(-x * y, y * y, 1.0);
-  return fma(y * e, fma(e, 2.0 / 9.0, 1.0 / 3.0), y);
+  // float seed for x^(-1/3): magic constant (rel. err ~ 4%), Newton steps in fp32
+  const float xf = d2f_pos(x);
+  const int ix = __float_as_int(xf);
+  float yf = __int_as_float(0x54a2fa8c - (int)(__umulhi((unsigned)ix, 0xAAAAAAABu) >> 1));   // ix / 3 without an XU divide
+  const float t3 = xf * (1.0f / 3.0f);
+#pragma unroll
+  for (int it = 0; it < 3; ++it) {   // y <- y (4/3 - x y^3 / 3)
+    const float y3 = yf * yf * yf;
+    yf = yf * fmaf(-t3, y3, 4.0f / 3.0f);
+  }
+  double y = f2d_pos(yf);          // ~1e-7
+  double e = fma(-x * y, y * y, c_nb[23]);
+  return fma(y * e, fma(e, c_nb[16], c_nb[17]), y);   // Halley: ~1e-21
 }
 
 // device self-test of the nonbonded math (tests/test_math_gpu.py)
@@ -890,9 +937,12 @@ __device__ __forceinline__ void nb_pair(double r2, double qiqj, const NBPair& c,
   // N1 taper: 1 + x^4 (-35 + x (84 + x (-70 + 20 x))), dTap/dr = -140 x^3 (1-x)^3 / R
   double x = r * k.invR;
   double x2 = x * x, x3 = x2 * x;
-  double tap = fma(x2 * x2, fma(x, fma(x, fma(x, 20.0, -70.0), 84.0), -35.0), 1.0);
-  double omx = 1.0 - x;
-  double dtap = (-140.0 * k.invR) * x3 * (omx * omx * omx);
+  double tp = fma(x, c_nb[18], c_nb[19]);
+  tp = fma(x, tp, c_nb[20]);
+  tp = fma(x, tp, c_nb[21]);
+  double tap = fma(x2 * x2, tp, c_nb[23]);
+  double omx = c_nb[23] - x;
+  double dtap = (c_nb[22] * k.invR) * x3 * (omx * omx * omx);
   // N2-N4 shielded vdW: r^p = exp(p ln r), f13 = (r^p + gw^-p)^(1/p)
   double lr = 0.5 * flog(r2, LT);
   double rp = fexp(k.p * lr, ET);
@@ -971,10 +1021,14 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     return;
   }
   const int nwu = c_win.nwu;
+  for (int k = threadIdx.x; k < nwu; k += blockDim.x) {   // thread per window cell (~15 atoms)
+    const int s0 = S.W.start[k], b0 = S.W.slot[k], c = S.W.cnt[k];
+    for (int a = 0; a < c; ++a) {
+      slot_j[b0 + a] = s0 + a;
+      slot_k[b0 + a] = (unsigned char)k;
+    }
+  }
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
-    const int k = cell_of_slot(S.W, nwu, t);
-    slot_j[t] = S.W.start[k] + (t - S.W.slot[k]);
-    slot_k[t] = (unsigned char)k;
     fx[t] = 0.0; fy[t] = 0.0; fz[t] = 0.0;
   }
   // this CTA's rows: split, split + nsplit, ... of the block (home sub-cell
@@ -1035,65 +1089,48 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     const int len = nbr_len[s];
     const uint16_t* row = nbr + (int64_t)s * row_cap;
     double fix = 0.0, fiy = 0.0, fiz = 0.0;
-    // software pipeline: the next chunk's neighbour data is loaded while the
-    // current chunk is evaluated; NB_ILP independent pairs per lane per chunk
-    int slot_n[NB_ILP], k_n[NB_ILP], tj_n[NB_ILP];
-    double4 xj_n[NB_ILP];
-#pragma unroll
-    for (int u = 0; u < NB_ILP; ++u) {
-      const int e = u * 32 + lane;
-      slot_n[u] = 0; k_n[u] = 0; tj_n[u] = 0; xj_n[u] = make_double4(0, 0, 0, 0);
+    // software pipeline, two buffers: chunk c+1's neighbour data (window slot,
+    // position/charge, type) is loaded while chunk c is evaluated
+    struct Nb { int slot, k, tj; double4 xj; };
+    auto load = [&](int e, Nb& b) {
       if (e < len) {
-        slot_n[u] = row[e];
-        const int j = slot_j[slot_n[u]];
-        k_n[u] = slot_k[slot_n[u]];
-        xj_n[u] = spos[j];
-        tj_n[u] = stype[j];
+        b.slot = row[e];
+        const int j = slot_j[b.slot];
+        b.k = slot_k[b.slot];
+        b.xj = spos[j];
+        b.tj = stype[j];
       }
-    }
-    for (int b0 = 0; b0 < len; b0 += 32 * NB_ILP) {
-      int slot[NB_ILP], kk[NB_ILP], tj[NB_ILP];
-      double4 xj[NB_ILP];
-#pragma unroll
-      for (int u = 0; u < NB_ILP; ++u) {
-        slot[u] = slot_n[u]; kk[u] = k_n[u]; tj[u] = tj_n[u]; xj[u] = xj_n[u];
-        const int en = b0 + 32 * NB_ILP + u * 32 + lane;
-        if (en < len) {
-          slot_n[u] = row[en];
-          const int j = slot_j[slot_n[u]];
-          k_n[u] = slot_k[slot_n[u]];
-          xj_n[u] = spos[j];
-          tj_n[u] = stype[j];
-        }
-      }
-      double ev[NB_ILP], ec[NB_ILP], gg[NB_ILP], dx[NB_ILP], dy[NB_ILP], dz[NB_ILP];
-#pragma unroll
-      for (int u = 0; u < NB_ILP; ++u) {
-        const bool act = b0 + u * 32 + lane < len;
-        dx[u] = xj[u].x - xi.x;
-        dy[u] = xj[u].y - xi.y;
-        dz[u] = xj[u].z - xi.z;
+    };
+    auto eval = [&](int e, const Nb& b) {
+      if (e < len) {
+        double dx = b.xj.x - xi.x, dy = b.xj.y - xi.y, dz = b.xj.z - xi.z;
         if (has_shift) {   // block-uniform
-          dx[u] += S.W.shift[kk[u]][0];
-          dy[u] += S.W.shift[kk[u]][1];
-          dz[u] += S.W.shift[kk[u]][2];
+          dx += S.W.shift[b.k][0];
+          dy += S.W.shift[b.k][1];
+          dz += S.W.shift[b.k][2];
         }
-        double r2 = act ? fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u])) : 1.0;
-        nb_pair(r2, cqi * xj[u].w, pc[ti * nt + tj[u]], kc, ET, LT, ev[u], ec[u], gg[u]);
-        if (!act) { ev[u] = 0.0; ec[u] = 0.0; gg[u] = 0.0; }
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double ev, ec, gg;
+        nb_pair(r2, cqi * b.xj.w, pc[ti * nt + b.tj], kc, ET, LT, ev, ec, gg);
+        ev_acc += ev;
+        ec_acc += ec;
+        const double gx = gg * dx, gy = gg * dy, gz = gg * dz;
+        fix += gx; fiy += gy; fiz += gz;
+        atomicAdd(&fx[b.slot], -gx);
+        atomicAdd(&fy[b.slot], -gy);
+        atomicAdd(&fz[b.slot], -gz);
       }
-#pragma unroll
-      for (int u = 0; u < NB_ILP; ++u) {
-        if (b0 + u * 32 + lane < len) {
-          ev_acc += ev[u];
-          ec_acc += ec[u];
-          double gx = gg[u] * dx[u], gy = gg[u] * dy[u], gz = gg[u] * dz[u];
-          fix += gx; fiy += gy; fiz += gz;
-          atomicAdd(&fx[slot[u]], -gx);
-          atomicAdd(&fy[slot[u]], -gy);
-          atomicAdd(&fz[slot[u]], -gz);
-        }
-      }
+    };
+    Nb A, B;
+    A.slot = B.slot = 0; A.k = B.k = 0; A.tj = B.tj = 0;
+    A.xj = B.xj = make_double4(0, 0, 0, 0);
+    load(lane, A);
+    for (int b0 = 0; b0 < len; b0 += 64) {
+      load(b0 + 32 + lane, B);
+      eval(b0 + lane, A);
+      if (b0 + 32 >= len) break;
+      load(b0 + 64 + lane, A);
+      eval(b0 + 32 + lane, B);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

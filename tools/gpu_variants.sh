@@ -1,5 +1,4 @@
 set -x
 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
 python bench.py --steps 50 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
-python bench.py --steps 50 --warmup 3 --no-cpu-baseline --no-e2e --no-graph > gpurun_out/bench_nograph.json 2>&1
-python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b3.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_nbr_build|k_nonbonded" -s 2 -c 2 -o gpurun_out/prof_r01g python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu2.log 2>&1; tail -1 gpurun_out/ncu2.log
+python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b3.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_nbr_build|k_nonbonded" -s 2 -c 2 -o gpurun_out/prof_r01i python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu2.log 2>&1; tail -1 gpurun_out/ncu2.log
