@@ -19,7 +19,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("REAX_LIBRARY", os.path.join(_HERE, "libreax.so"))
 
-OK, ERR_ARG, ERR_BOX, ERR_CUTOFF, ERR_PARAM, ERR_CAPACITY, ERR_NONFINITE, ERR_CUDA, ERR_STATE = range(9)
+OK, ERR_ARG, ERR_BOX, ERR_CUTOFF, ERR_PARAM, ERR_CAPACITY, ERR_NONFINITE, ERR_CUDA, ERR_STATE, ERR_RANGE = range(10)
 KERNEL_GROUPS = ("bin", "nbr", "bonds", "bond_orders", "nonbonded", "other")
 EXPORTED = ("reax_status_str", "reax_create", "reax_destroy", "reax_workspace_bytes", "reax_bind_workspace",
             "reax_required", "reax_build_lists", "reax_bond_orders", "reax_nonbonded", "reax_step",

@@ -88,6 +88,7 @@ enum : int {
   ST_BOND_OVF = 16,
   ST_WIN_OVF = 32,
   ST_NONFINITE_OUT = 64,
+  ST_RANGE = 128,           // a force contribution outside the fixed-point range
 };
 
 struct Status {
@@ -123,9 +124,9 @@ struct WS {
   int* bmir;         // bond_cap
   double* bo;        // bond_cap * 8
   double2* delta;    // n
-  double* sfx;       // n
-  double* sfy;       // n
-  double* sfz;       // n
+  unsigned long long* sfx;   // n  sorted-order forces, int64 fixed point (2^-35 kcal/mol/A)
+  unsigned long long* sfy;   // n
+  unsigned long long* sfz;   // n
   double2* erow;     // n   per-row (E_vdW, E_Coul)
   double* epart;     // energy reduction partials
   unsigned* ticket;  // last-block counter of the energy reduction

@@ -786,19 +786,20 @@ __global__ void k_bond_correct(const int* __restrict__ brow, const int* __restri
 
 // ====================================================== a7-a8 nonbonded
 __global__ void k_nb_prep(int n, const double* __restrict__ q, const int* __restrict__ perm, double4* __restrict__ spos,
-                          double* __restrict__ sfx, double* __restrict__ sfy, double* __restrict__ sfz, Status* st) {
+                          unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy,
+                          unsigned long long* __restrict__ sfz, Status* st) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   double qs = q[perm[s]];
   if (!isfinite(qs)) set_flag(st, ST_NONFINITE_IN);
   spos[s].w = qs;
-  sfx[s] = 0.0;
-  sfy[s] = 0.0;
-  sfz[s] = 0.0;
+  sfx[s] = 0ull;
+  sfy[s] = 0ull;
+  sfz[s] = 0ull;
 }
 
 struct NBConst {
-  double invR, p, inv_p, C;
+  double invR, phalf, inv_p, m140invR;
 };
 
 // ---- branch-free fp64 math for the nonbonded pair (inputs in known, finite,
@@ -806,7 +807,7 @@ struct NBConst {
 constexpr int EXP_TBL = 64;    // 2^(j/64)
 // polynomial / reduction constants as constant-bank operands (ptxas otherwise
 // re-materialises 64-bit literals with register moves inside the pair loop)
-__constant__ double c_nb[24] = {
+__constant__ double c_nb[28] = {
     0x1.71547652b82fep+6,      // 0  64 / ln 2
     6755399441055744.0,        // 1  1.5 * 2^52
     0x1.62e42fee00000p-7,      // 2  ln2_hi / 64
@@ -817,7 +818,11 @@ __constant__ double c_nb[24] = {
     0x1.a39ef35793c76p-33,     // 14 ln2_lo
     0.375, 2.0 / 9.0, 1.0 / 3.0,   // 15-17 Halley rsqrt / rcbrt
     20.0, -70.0, 84.0, -35.0, -140.0,   // 18-22 taper
-    1.0};                      // 23
+    1.0,                       // 23
+    14.0 / 81.0,               // 24 rcbrt quartic term
+    0x1.0p35,                  // 25 fixed-point force scale 2^FIX_BITS
+    6755399441055744.0,        // 26 1.5 * 2^52 (round-to-integer magic)
+    65536.0};                  // 27 fixed-point range limit per contribution
 
 constexpr int LOG_TBL = 128;   // {1/c_j, -log(1/c_j)}, c_j = 1 + (j + 1/2)/128
 
@@ -857,22 +862,6 @@ __device__ __forceinline__ double flog(double x, const double2* __restrict__ LT)
   return fma(ed, c_nb[13], t.y) + fma(ed, c_nb[14], p);
 }
 
-// ---- XU-free seeds.  The XU (MUFU + int/fp64 conversions) is the scarce unit
-// of this kernel (ncu: xu pipe 82% with MUFU seeds and F2F/I2F conversions), so
-// float <-> double conversions are done with integer bit operations (inputs are
-// positive normal numbers in a modest range) and seeds come from bit hacks plus
-// FMA-pipe Newton steps.
-__device__ __forceinline__ float d2f_pos(double x) {       // truncating, positive normal x
-  const int hi = __double2hiint(x), lo = __double2loint(x);
-  const int e = ((hi >> 20) & 0x7ff) - 1023 + 127;
-  return __int_as_float((e << 23) | ((hi & 0xfffff) << 3) | ((unsigned)lo >> 29));
-}
-__device__ __forceinline__ double f2d_pos(float f) {        // exact, positive normal f
-  const int b = __float_as_int(f);
-  const int e = ((b >> 23) & 0xff) - 127 + 1023;
-  return __hiloint2double((e << 20) | ((b & 0x7fffff) >> 3), b << 29);
-}
-
 // approximate seeds from the MUFU unit, then one Halley-type correction:
 // (1-e)^(-1/2) = 1 + e/2 + 3e^2/8 + ..., (1-e)^(-1/3) = 1 + e/3 + 2e^2/9 + ...,
 // 1/(1-e) = 1 + e + e^2: relative error ~ (2^-22)^3
@@ -883,30 +872,25 @@ __device__ __forceinline__ double frsqrt(double x) {
   return fma(y * e, fma(e, c_nb[15], c_nb[7]), y);
 }
 __device__ __forceinline__ double frcp(double x) {
-  // float seed: magic constant (rel. err < 6%), two Newton steps in fp32
-  const float xf = d2f_pos(x);
-  float yf = __int_as_float(0x7ef311c3 - __float_as_int(xf));
-  yf = yf * fmaf(-xf, yf, 2.0f);
-  yf = yf * fmaf(-xf, yf, 2.0f);
-  yf = yf * fmaf(-xf, yf, 2.0f);   // ~1e-7 (fp32 rounding)
-  double y = f2d_pos(yf);
+  // MUFU.RCP64H seed (~2^-22), then 1/(1-e) = 1 + e + e^2: ~1e-20
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   double e = fma(-x, y, c_nb[23]);
-  return fma(y * e, c_nb[23] + e, y);   // 1/(1-e) = 1 + e + e^2: ~1e-21
+  return fma(y * e, c_nb[23] + e, y);
 }
 __device__ __forceinline__ double frcbrt(double x) {
-  // float seed for x^(-1/3): magic constant (rel. err ~ 4%), Newton steps in fp32
-  const float xf = d2f_pos(x);
-  const int ix = __float_as_int(xf);
-  float yf = __int_as_float(0x54a2fa8c - (int)(__umulhi((unsigned)ix, 0xAAAAAAABu) >> 1));   // ix / 3 without an XU divide
-  const float t3 = xf * (1.0f / 3.0f);
-#pragma unroll
-  for (int it = 0; it < 3; ++it) {   // y <- y (4/3 - x y^3 / 3)
-    const float y3 = yf * yf * yf;
-    yf = yf * fmaf(-t3, y3, 4.0f / 3.0f);
-  }
-  double y = f2d_pos(yf);          // ~1e-7
+  // fp32 seed x^(-1/3) = 2^(-log2(x)/3) from MUFU.LG2/EX2 (~1e-6), then one
+  // quartic correction (1-e)^(-1/3) = 1 + e/3 + 2e^2/9 + 14e^3/81: ~1e-23
+  const float xf = __double2float_rn(x);
+  float lf, yf;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lf) : "f"(xf));
+  lf *= -0.333333343f;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(lf));
+  double y = (double)yf;
   double e = fma(-x * y, y * y, c_nb[23]);
-  return fma(y * e, fma(e, c_nb[16], c_nb[17]), y);   // Halley: ~1e-21
+  double q = fma(e, c_nb[24], c_nb[16]);
+  q = fma(e, q, c_nb[17]);
+  return fma(y * e, q, y);
 }
 
 // device self-test of the nonbonded math (tests/test_math_gpu.py)
@@ -928,10 +912,10 @@ __global__ void k_selftest_math(int n, const double* __restrict__ x, double* __r
 }
 
 // One Alg. 2 pair (N1-N5): tapered shielded vdW + Coulomb; returns energies
-// and g = (dE/dr)/r so that F_i += g d, F_j -= g d.
+// and g = (dE/dr)/r so that F_i += g d, F_j -= g d.  dE = dE/dr (range check).
 __device__ __forceinline__ void nb_pair(double r2, double qiqj, const NBPair& c, const NBConst& k,
                                         const double* __restrict__ ET, const double2* __restrict__ LT,
-                                        double& ev, double& ec, double& g) {
+                                        double& ev, double& ec, double& g, double& dE) {
   double rinv = frsqrt(r2);
   double r = r2 * rinv;
   // N1 taper: 1 + x^4 (-35 + x (84 + x (-70 + 20 x))), dTap/dr = -140 x^3 (1-x)^3 / R
@@ -942,13 +926,12 @@ __device__ __forceinline__ void nb_pair(double r2, double qiqj, const NBPair& c,
   tp = fma(x, tp, c_nb[21]);
   double tap = fma(x2 * x2, tp, c_nb[23]);
   double omx = c_nb[23] - x;
-  double dtap = (c_nb[22] * k.invR) * x3 * (omx * omx * omx);
-  // N2-N4 shielded vdW: r^p = exp(p ln r), f13 = (r^p + gw^-p)^(1/p)
-  double lr = 0.5 * flog(r2, LT);
-  double rp = fexp(k.p * lr, ET);
+  double dtap = k.m140invR * x3 * (omx * omx * omx);
+  // N2-N4 shielded vdW: r^p = exp((p/2) ln r^2), f13 = (r^p + gw^-p)^(1/p)
+  double rp = fexp(k.phalf * flog(r2, LT), ET);
   double sv = rp + c.gwmp;
   double f13 = fexp(flog(sv, LT) * k.inv_p, ET);
-  double u = fma(-f13, c.inv_rvdw, 1.0);
+  double u = fma(-f13, c.inv_rvdw, c_nb[23]);
   double e2 = fexp(c.ahalf * u, ET);      // e^{alpha u / 2}
   double e1 = e2 * e2;                    // e^{alpha u}
   double evu = c.D * fma(-2.0, e2, e1);
@@ -963,37 +946,54 @@ __device__ __forceinline__ void nb_pair(double r2, double qiqj, const NBPair& c,
   double decu = -qiqj * r2 * (cb2 * cb2);
   ev = tap * evu;
   ec = tap * ecu;
-  double dE = fma(dtap, evu + ecu, tap * (devu + decu));
+  dE = fma(dtap, evu + ecu, tap * (devu + decu));
   g = dE * rinv;
 }
 
+// ---- fixed-point force accumulation (deterministic: integer sums are exact
+// and order-free).  A contribution c (kcal/mol/A) becomes v = round(c 2^35)
+// via t = c 2^35 + 1.5 2^52 (bits(t) = bits(1.5 2^52) + v for |v| < 2^51), and
+// is added to a slot as two int32 words: A = v mod 2^20 (unsigned, < 2^20, so
+// up to 4096 adds cannot overflow 32 bits) and B = floor(v / 2^20) (mod 2^32).
+// The slot value is B 2^20 + A.  Error per contribution <= 2^-36 (1.5e-11);
+// |c| must stay below 2^16 (flagged otherwise, REAX_ERR_RANGE).
+constexpr int FIX_BITS = 35;
+constexpr unsigned FIX_BKEY = (unsigned)(0x4338000000000000ull >> 20);   // low word of bits(1.5 2^52) >> 20
+
+__device__ __forceinline__ void fix_add(unsigned* A, int* B, double t) {
+  const unsigned lo = (unsigned)__double2loint(t), hi = (unsigned)__double2hiint(t);
+  const unsigned b = __funnelshift_r(lo, hi, 20) - FIX_BKEY;
+  atomicAdd(A, lo & 0xFFFFFu);
+  atomicAdd(B, (int)b);
+}
+
 constexpr int NB_THREADS = 256;
-#ifndef NB_ILP
-#define NB_ILP 1
-#endif
 #ifndef NB_MINB
 #define NB_MINB 3
 #endif
 
-constexpr int NB_MAX_ROWS = 256;   // rows of one (block, split) work unit
+constexpr int NB_MAX_ROWS = 256;   // rows of one (block, split) work unit that are ranked
 struct NBSmem {
   WinSmem W;
+  double4 shift4[NWU_MAX];      // periodic image shift of each window cell (x, y, z, 0)
   int next_row;
+  int bad;
   int order[NB_MAX_ROWS];        // row window slots, longest row first
   int rlen[NB_MAX_ROWS];
 };
 
-// One CTA per home block (Alg. 2, re-designed): a warp per
-// row i streams its half-list entries (lanes over j); F_i stays in registers
-// and is warp-reduced once per row; F_j is accumulated in a shared-memory
-// window (the block's private force array, the GPU form of the paper's
-// thread-private tprivForce) and flushed to the global sorted force array
-// once per block.  Energies: per-block partials reduced later in fixed order.
+// One CTA per (home block, split) (Alg. 2, re-designed): a
+// warp per row i streams its half-list entries (lanes over j); F_i stays in
+// registers and is warp-reduced once per row; F_j is accumulated in a
+// shared-memory fixed-point window (the block's private force array, the GPU
+// form of the paper's thread-private tprivForce) and flushed to the global
+// int64 sorted force array once per CTA.  Energies: per-row partials reduced
+// later in fixed order.  Forces and energies are bitwise reproducible.
 __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const int* __restrict__ cell_start,
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
-    double* __restrict__ sfx, double* __restrict__ sfy, double* __restrict__ sfz, double2* __restrict__ erow,
-    int nsplit, Status* st) {
+    unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
+    double2* __restrict__ erow, int nsplit, Status* st) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
   const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
@@ -1001,18 +1001,17 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   double* ET = reinterpret_cast<double*>(dyn);                  // exp table
   double2* LT = reinterpret_cast<double2*>(ET + EXP_TBL);       // log table
   NBPair* pc = reinterpret_cast<NBPair*>(LT + LOG_TBL);         // nt*nt pair constants
-  double* fx = reinterpret_cast<double*>(pc + nt * nt);        // F window (block-private force array)
-  double* fy = fx + window_cap;
-  double* fz = fy + window_cap;
-  int* slot_j = reinterpret_cast<int*>(fz + window_cap);       // slot -> sorted atom
-  unsigned char* slot_k = reinterpret_cast<unsigned char*>(slot_j + window_cap);  // slot -> window cell
+  int2* sinfo = reinterpret_cast<int2*>(pc + nt * nt);          // slot -> {sorted atom, window cell | type << 8}
+  unsigned* fa = reinterpret_cast<unsigned*>(sinfo + window_cap);   // F window, low words [3][window_cap]
+  int* fb = reinterpret_cast<int*>(fa + 3 * window_cap);            // F window, high words [3][window_cap]
   for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) pc[t] = prm->nb[t];
   for (int t = threadIdx.x; t < EXP_TBL; t += blockDim.x) ET[t] = prm->exp_tbl[t];
   for (int t = threadIdx.x; t < LOG_TBL; t += blockDim.x) LT[t] = make_double2(prm->log_tbl[2 * t], prm->log_tbl[2 * t + 1]);
   NBConst kc;
-  kc.invR = prm->invR; kc.p = prm->p_vdw; kc.inv_p = prm->inv_p; kc.C = prm->C;
+  kc.invR = prm->invR; kc.phalf = 0.5 * prm->p_vdw; kc.inv_p = prm->inv_p; kc.m140invR = -140.0 * prm->invR;
+  const double C = prm->C;
   int W = build_window(S.W, blk, g, cell_start);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
   if (W > window_cap) {
     if (threadIdx.x == 0) {
       set_flag(st, ST_WIN_OVF);
@@ -1023,13 +1022,12 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   const int nwu = c_win.nwu;
   for (int k = threadIdx.x; k < nwu; k += blockDim.x) {   // thread per window cell (~15 atoms)
     const int s0 = S.W.start[k], b0 = S.W.slot[k], c = S.W.cnt[k];
-    for (int a = 0; a < c; ++a) {
-      slot_j[b0 + a] = s0 + a;
-      slot_k[b0 + a] = (unsigned char)k;
-    }
+    S.shift4[k] = make_double4(S.W.shift[k][0], S.W.shift[k][1], S.W.shift[k][2], 0.0);
+    for (int a = 0; a < c; ++a) sinfo[b0 + a] = make_int2(s0 + a, k | (stype[s0 + a] << 8));
   }
-  for (int t = threadIdx.x; t < W; t += blockDim.x) {
-    fx[t] = 0.0; fy[t] = 0.0; fz[t] = 0.0;
+  for (int t = threadIdx.x; t < 3 * W; t += blockDim.x) {
+    fa[(t / W) * window_cap + t % W] = 0u;
+    fb[(t / W) * window_cap + t % W] = 0;
   }
   // this CTA's rows: split, split + nsplit, ... of the block (home sub-cell
   // order), ranked longest first (rows are 90-370 pairs): longest-processing-
@@ -1039,37 +1037,34 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     if (S.W.home_ok[h]) nrows_blk += S.W.cnt[c_win.home_k[h]];
   const int nrows = nrows_blk > split ? (nrows_blk - split + nsplit - 1) / nsplit : 0;
   const int nsorted = nrows < NB_MAX_ROWS ? nrows : NB_MAX_ROWS;
-  if (threadIdx.x == 0) S.next_row = 0;
-  constexpr int RPT = NB_MAX_ROWS / NB_THREADS;   // rows per thread in the ranking
-  int my_row[RPT], my_len[RPT];
-#pragma unroll
-  for (int u = 0; u < RPT; ++u) {
-    const int t = threadIdx.x + u * NB_THREADS;
-    my_row[u] = 0; my_len[u] = 0;
-    if (t < nsorted) {
-      int h, si;
-      row_of(S.W, split + t * nsplit, h, si);
-      my_row[u] = si;
-      my_len[u] = nbr_len[slot_j[si]];
-      S.rlen[t] = my_len[u];
-    }
+  if (threadIdx.x == 0) { S.next_row = 0; S.bad = 0; }
+  __syncthreads();   // sinfo complete
+  for (int t = threadIdx.x; t < nsorted; t += blockDim.x) {
+    int h, si;
+    row_of(S.W, split + t * nsplit, h, si);
+    S.order[t] = si;
+    S.rlen[t] = nbr_len[sinfo[si].x];
   }
   __syncthreads();
-#pragma unroll
-  for (int u = 0; u < RPT; ++u) {
-    const int me = threadIdx.x + u * NB_THREADS;
-    if (me < nsorted) {
-      int rank = 0;
+  static_assert(NB_MAX_ROWS <= NB_THREADS, "one ranked row per thread");
+  {
+    const bool have = (int)threadIdx.x < nsorted;
+    int rank = 0, mrow = 0;
+    if (have) {
+      const int ml = S.rlen[threadIdx.x];
+      mrow = S.order[threadIdx.x];
       for (int t = 0; t < nsorted; ++t) {
         const int lt = S.rlen[t];
-        rank += (lt > my_len[u]) || (lt == my_len[u] && t < me);
+        rank += (lt > ml) || (lt == ml && t < (int)threadIdx.x);
       }
-      S.order[rank] = my_row[u];
     }
+    __syncthreads();
+    if (have) S.order[rank] = mrow;
   }
   __syncthreads();
   const bool has_shift = S.W.has_shift != 0;
-  double ev_acc = 0.0, ec_acc = 0.0;
+  const double FIXS = c_nb[25], MAGIC = c_nb[26], FLIM = c_nb[27];
+  bool bad = false;
   for (;;) {
     int m = 0;
     if (lane == 0) m = atomicAdd(&S.next_row, 1);
@@ -1082,105 +1077,103 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
       int h;
       row_of(S.W, split + m * nsplit, h, si);
     }
-    const int s = slot_j[si];
+    const int2 ii = sinfo[si];
+    const int s = ii.x;
     const double4 xi = spos[s];
-    const int ti = stype[s];
-    const double cqi = kc.C * xi.w;
+    const NBPair* pci = pc + (ii.y >> 8) * nt;
+    const double cqi = C * xi.w;
     const int len = nbr_len[s];
     const uint16_t* row = nbr + (int64_t)s * row_cap;
-    double fix = 0.0, fiy = 0.0, fiz = 0.0;
-    // software pipeline, two buffers: chunk c+1's neighbour data (window slot,
-    // position/charge, type) is loaded while chunk c is evaluated
-    struct Nb { int slot, k, tj; double4 xj; };
-    auto load = [&](int e, Nb& b) {
-      if (e < len) {
-        b.slot = row[e];
-        const int j = slot_j[b.slot];
-        b.k = slot_k[b.slot];
-        b.xj = spos[j];
-        b.tj = stype[j];
+    double fix = 0.0, fiy = 0.0, fiz = 0.0, ev_acc = 0.0, ec_acc = 0.0;
+    // software pipeline: the next chunk's slot info and position are loaded
+    // while the current chunk is evaluated
+    int e = lane;
+    int slot = 0;
+    int2 inf = make_int2(0, 0);
+    double4 xj = make_double4(0, 0, 0, 0);
+    if (e < len) {
+      slot = row[e];
+      inf = sinfo[slot];
+      xj = spos[inf.x];
+    }
+    for (; e - lane < len; e += 32) {
+      const int cslot = slot;
+      const int2 cinf = inf;
+      const double4 cxj = xj;
+      const bool act = e < len;
+      const int en = e + 32;
+      if (en < len) {
+        slot = row[en];
+        inf = sinfo[slot];
+        xj = spos[inf.x];
       }
-    };
-    auto eval = [&](int e, const Nb& b) {
-      if (e < len) {
-        double dx = b.xj.x - xi.x, dy = b.xj.y - xi.y, dz = b.xj.z - xi.z;
+      if (act) {
+        double dx = cxj.x - xi.x, dy = cxj.y - xi.y, dz = cxj.z - xi.z;
         if (has_shift) {   // block-uniform
-          dx += S.W.shift[b.k][0];
-          dy += S.W.shift[b.k][1];
-          dz += S.W.shift[b.k][2];
+          const double4 sh = S.shift4[cinf.y & 255];
+          dx += sh.x;
+          dy += sh.y;
+          dz += sh.z;
         }
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        double ev, ec, gg;
-        nb_pair(r2, cqi * b.xj.w, pc[ti * nt + b.tj], kc, ET, LT, ev, ec, gg);
+        double ev, ec, gg, dE;
+        nb_pair(r2, cqi * cxj.w, pci[cinf.y >> 8], kc, ET, LT, ev, ec, gg, dE);
         ev_acc += ev;
         ec_acc += ec;
-        const double gx = gg * dx, gy = gg * dy, gz = gg * dz;
-        fix += gx; fiy += gy; fiz += gz;
-        atomicAdd(&fx[b.slot], -gx);
-        atomicAdd(&fy[b.slot], -gy);
-        atomicAdd(&fz[b.slot], -gz);
+        fix = fma(gg, dx, fix);
+        fiy = fma(gg, dy, fiy);
+        fiz = fma(gg, dz, fiz);
+        bad |= !(fabs(dE) < FLIM);
+        const double gs = -gg * FIXS;
+        fix_add(fa + cslot, fb + cslot, fma(gs, dx, MAGIC));
+        fix_add(fa + window_cap + cslot, fb + window_cap + cslot, fma(gs, dy, MAGIC));
+        fix_add(fa + 2 * window_cap + cslot, fb + 2 * window_cap + cslot, fma(gs, dz, MAGIC));
       }
-    };
-    Nb A, B;
-    A.slot = B.slot = 0; A.k = B.k = 0; A.tj = B.tj = 0;
-    A.xj = B.xj = make_double4(0, 0, 0, 0);
-    load(lane, A);
-    for (int b0 = 0; b0 < len; b0 += 64) {
-      load(b0 + 32 + lane, B);
-      eval(b0 + lane, A);
-      if (b0 + 32 >= len) break;
-      load(b0 + 64 + lane, A);
-      eval(b0 + 32 + lane, B);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       fix += __shfl_xor_sync(0xffffffffu, fix, o);
       fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
       fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
       ev_acc += __shfl_xor_sync(0xffffffffu, ev_acc, o);
       ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
     }
     if (lane == 0) {
-      atomicAdd(&fx[si], fix);
-      atomicAdd(&fy[si], fiy);
-      atomicAdd(&fz[si], fiz);
+      bad |= !(fabs(fix) < FLIM && fabs(fiy) < FLIM && fabs(fiz) < FLIM);
+      fix_add(fa + si, fb + si, fma(fix, FIXS, MAGIC));
+      fix_add(fa + window_cap + si, fb + window_cap + si, fma(fiy, FIXS, MAGIC));
+      fix_add(fa + 2 * window_cap + si, fb + 2 * window_cap + si, fma(fiz, FIXS, MAGIC));
       erow[s] = make_double2(ev_acc, ec_acc);   // per-row energy: reduced later in row order
     }
-    ev_acc = 0.0;
-    ec_acc = 0.0;
   }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) S.bad = 1;
   __syncthreads();
+  if (threadIdx.x == 0 && S.bad) set_flag(st, ST_RANGE);
+  unsigned long long* gf[3] = {sfx, sfy, sfz};
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
-    double a = fx[t], b = fy[t], c = fz[t];
-    if (a != 0.0 || b != 0.0 || c != 0.0) {
-      int j = slot_j[t];
-      atomicAdd(&sfx[j], a);
-      atomicAdd(&sfy[j], b);
-      atomicAdd(&sfz[j], c);
+    const int j = sinfo[t].x;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long v = ((long long)fb[c * window_cap + t] << 20) + (long long)fa[c * window_cap + t];
+      if (v != 0) atomicAdd(&gf[c][j], (unsigned long long)v);
     }
   }
 }
 
-// un-permute: force[i] = F_sorted[iperm[i]]
-__global__ void k_finalize_forces(int n, const int* __restrict__ iperm, const double* __restrict__ sfx,
-                                  const double* __restrict__ sfy, const double* __restrict__ sfz,
+// un-permute: force[i] = F_sorted[iperm[i]] (int64 fixed point -> fp64)
+__global__ void k_finalize_forces(int n, const int* __restrict__ iperm, const long long* __restrict__ sfx,
+                                  const long long* __restrict__ sfy, const long long* __restrict__ sfz,
                                   double* __restrict__ force, Status* st) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int s = iperm[i];
-  double a = sfx[s], b = sfy[s], c = sfz[s];
-  if (!(isfinite(a) && isfinite(b) && isfinite(c))) set_flag(st, ST_NONFINITE_OUT);
-  force[3 * (int64_t)i] = a;
-  force[3 * (int64_t)i + 1] = b;
-  force[3 * (int64_t)i + 2] = c;
+  const double sc = 0x1.0p-35;
+  static_assert(FIX_BITS == 35, "scale");
+  force[3 * (int64_t)i] = (double)sfx[s] * sc;
+  force[3 * (int64_t)i + 1] = (double)sfy[s] * sc;
+  force[3 * (int64_t)i + 2] = (double)sfz[s] * sc;
 }
 
-// fixed-order energy reduction over the per-row energies: each CTA sums a
-// fixed contiguous range, the last CTA to finish sums the CTA partials in
-// index order (bitwise reproducible)
 constexpr int FIN_THREADS = 512;
 constexpr int FIN_ITEMS = 16;
 __global__ void __launch_bounds__(FIN_THREADS) k_finalize_energy(int n, const double2* __restrict__ erow,

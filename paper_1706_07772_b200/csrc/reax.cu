@@ -329,9 +329,9 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
   t.bmir = (int*)take(sizeof(int) * (size_t)c.bond_cap);
   t.bo = (double*)take(sizeof(double) * 8 * (size_t)c.bond_cap);
   t.delta = (double2*)take(sizeof(double2) * N);
-  t.sfx = (double*)take(sizeof(double) * N);
-  t.sfy = (double*)take(sizeof(double) * N);
-  t.sfz = (double*)take(sizeof(double) * N);
+  t.sfx = (unsigned long long*)take(sizeof(long long) * N);
+  t.sfy = (unsigned long long*)take(sizeof(long long) * N);
+  t.sfz = (unsigned long long*)take(sizeof(long long) * N);
   t.erow = (double2*)take(sizeof(double2) * N);
   t.epart = (double*)take(sizeof(double) * 2 * ((size_t)nblk((int64_t)N, FIN_THREADS * FIN_ITEMS) + 1));
   t.ticket = (unsigned*)take(sizeof(unsigned) * 4);
@@ -390,6 +390,9 @@ struct reax_ctx {
   int launches_cur = 0;
   int nsplit = 1;
   int nsplit_nbr = 1;
+  // fork/join of reax_step (bond chain beside the nonbonded kernel)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -481,7 +484,8 @@ reax_status read_status(reax_ctx* c, cudaStream_t s, bool sync) {
   }
   cudaMemsetAsync(c->w.st, 0, sizeof(Status), s);
   if (f & ST_TYPE) { c->lists_ok = c->bonds_ok = false; return REAX_ERR_ARG; }
-  return REAX_ERR_NONFINITE;
+  if (f & (ST_NONFINITE_IN | ST_NONFINITE_OUT)) return REAX_ERR_NONFINITE;
+  return REAX_ERR_RANGE;
 }
 
 // raw parameter values (and cutoffs) as a flat key: rebuilding the tables
@@ -533,7 +537,9 @@ size_t nbr_smem(int wcap, int row_cap = 0) {
   (void)row_cap;
   return (size_t)(wcap + 32) * (sizeof(float4) + sizeof(int) + 1) + 64;
 }
-size_t nb_smem(int wcap, int nt = NT_MAX) { return sizeof(double) * (EXP_TBL + 2 * LOG_TBL) + sizeof(NBPair) * nt * nt + (size_t)wcap * (3 * sizeof(double) + sizeof(int) + 1) + 64; }
+size_t nb_smem(int wcap, int nt = NT_MAX) {
+  return sizeof(double) * (EXP_TBL + 2 * LOG_TBL) + sizeof(NBPair) * nt * nt + (size_t)wcap * (sizeof(int2) + 6 * sizeof(int)) + 64;
+}
 size_t exp_smem(int wcap) { return (size_t)wcap * sizeof(int) + 64; }
 
 reax_status check_common(reax_ctx* c, int64_t n, const double box[3], const reax_cutoffs* cut) {
@@ -551,8 +557,62 @@ reax_status check_common(reax_ctx* c, int64_t n, const double box[3], const reax
   return REAX_OK;
 }
 
-reax_status do_build_lists(reax_ctx* c, int64_t n, const double* pos, const int* type, const double box[3],
-                           const reax_params* prm, const reax_cutoffs* cut, cudaStream_t s) {
+// a1-a3: binning and the half list (+ bond candidates)
+void launch_lists(reax_ctx* c, int N, const double* pos, const int* type, int nt, cudaStream_t s) {
+  const Grid& g = c->g;
+  WS& w = c->w;
+  {
+    Timer t(c, 0, s);
+    const int ctiles = nblk(g.ncell, LB_TILE);
+    k_bin<<<nblk(std::max<int64_t>(N, ctiles), TPB), TPB, 0, s>>>(N, pos, type, g, nt, w.cell_of, w.cell_cnt,
+                                                                 w.st, w.lb_status, ctiles);
+    LAUNCH(c);
+    scan1(c, w.cell_cnt, g.ncell, w.cell_start, w.lb_status, s);
+    k_scatter<<<nblk(N, TPB), TPB, 0, s>>>(N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
+    LAUNCH(c);
+    k_cell_gather<<<nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s>>>(g.ncell, w.cell_start, w.perm, pos, type, g, nt,
+                                                               w.iperm, w.spos, w.sloc, w.stype);
+    LAUNCH(c);
+  }
+  {
+    Timer t(c, 1, s);
+    k_nbr_build<<<g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s>>>(
+        g, w.cell_start, w.sloc, w.spos, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, w.bc, w.bc_len,
+        c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st);
+    LAUNCH(c);
+  }
+}
+
+// a4-a5: full bond list with BO' and Delta' (reads spos x/y/z, stype, bond candidates)
+void launch_bonds(reax_ctx* c, int N, cudaStream_t s) {
+  const Grid& g = c->g;
+  WS& w = c->w;
+  Timer t(c, 2, s);
+  const int btiles = nblk(N, LB_TILE);
+  k_bond_eval<<<nblk(std::max<int64_t>(N, (int64_t)btiles * 32), TPB), TPB, 0, s>>>(
+      N, w.spos, w.stype, g, w.prm, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.bdeg, w.lb_status, btiles);
+  LAUNCH(c);
+  scan1(c, w.bdeg, N, w.brow, w.lb_status, s);
+  k_bond_fill<<<nblk(N, TPB), TPB, 0, s>>>(N, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.brow, w.perm, w.bdeg,
+                                          w.ucol, w.ukey, w.uown, w.uraw, c->cap.bond_cap, w.st);
+  LAUNCH(c);
+  k_bond_rank<<<148 * 4, TPB, 0, s>>>(w.brow, w.ucol, w.ukey, w.uown, w.uraw, w.bcol, w.bkey, w.bown, w.bo,
+                                     c->cap.bond_cap, w.st);
+  LAUNCH(c);
+  k_bond_delta<<<nblk(N, TPB), TPB, 0, s>>>(N, w.brow, w.stype, w.prm, w.bo, w.delta, c->cap.bond_cap);
+  LAUNCH(c);
+}
+
+// a6: corrected bond orders
+void launch_bond_correct(reax_ctx* c, cudaStream_t s) {
+  Timer t(c, 3, s);
+  k_bond_correct<<<148 * 8, TPB, 0, s>>>(c->w.brow, c->w.perm, c->w.stype, c->w.prm, c->w.bcol, c->w.bkey,
+                                         c->w.bown, c->w.bmir, c->w.bo, c->w.delta, c->cap.bond_cap, c->w.st);
+  LAUNCH(c);
+}
+
+reax_status prep_build(reax_ctx* c, int64_t n, const double* pos, const int* type, const double box[3],
+                       const reax_params* prm, const reax_cutoffs* cut, cudaStream_t s) {
   reax_status r = check_common(c, n, box, cut);
   if (r != REAX_OK) return r;
   if (n > 0 && (!pos || !type)) return REAX_ERR_ARG;
@@ -560,52 +620,26 @@ reax_status do_build_lists(reax_ctx* c, int64_t n, const double* pos, const int*
   if (r != REAX_OK) return r;
   c->cut = *cut;
   c->lists_ok = c->bonds_ok = false;
-  const Grid& g = c->g;
-  WS& w = c->w;
-  int N = (int)n;
-  if (N > 0) {
-    {
-      Timer t(c, 0, s);
-      const int ctiles = nblk(g.ncell, LB_TILE);
-      k_bin<<<nblk(std::max<int64_t>(N, ctiles), TPB), TPB, 0, s>>>(N, pos, type, g, prm->ntypes, w.cell_of, w.cell_cnt,
-                                                                   w.st, w.lb_status, ctiles);
-      LAUNCH(c);
-      scan1(c, w.cell_cnt, g.ncell, w.cell_start, w.lb_status, s);
-      k_scatter<<<nblk(N, TPB), TPB, 0, s>>>(N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
-      LAUNCH(c);
-      k_cell_gather<<<nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s>>>(g.ncell, w.cell_start, w.perm, pos, type, g,
-                                                                 prm->ntypes, w.iperm, w.spos, w.sloc, w.stype);
-      LAUNCH(c);
-    }
-    {
-      Timer t(c, 1, s);
-      k_nbr_build<<<g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s>>>(
-          g, w.cell_start, w.sloc, w.spos, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, w.bc, w.bc_len,
-          c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st);
-      LAUNCH(c);
-    }
-    {
-      Timer t(c, 2, s);
-      const int btiles = nblk(N, LB_TILE);
-      k_bond_eval<<<nblk(std::max<int64_t>(N, (int64_t)btiles * 32), TPB), TPB, 0, s>>>(
-          N, w.spos, w.stype, g, w.prm, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.bdeg, w.lb_status, btiles);
-      LAUNCH(c);
-      scan1(c, w.bdeg, N, w.brow, w.lb_status, s);
-      k_bond_fill<<<nblk(N, TPB), TPB, 0, s>>>(N, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.brow, w.perm, w.bdeg,
-                                              w.ucol, w.ukey, w.uown, w.uraw, c->cap.bond_cap, w.st);
-      LAUNCH(c);
-      k_bond_rank<<<148 * 4, TPB, 0, s>>>(w.brow, w.ucol, w.ukey, w.uown, w.uraw, w.bcol, w.bkey, w.bown, w.bo,
-                                         c->cap.bond_cap, w.st);
-      LAUNCH(c);
-      k_bond_delta<<<nblk(N, TPB), TPB, 0, s>>>(N, w.brow, w.stype, w.prm, w.bo, w.delta, c->cap.bond_cap);
-      LAUNCH(c);
-    }
-  }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  return REAX_OK;
+}
+
+void note_build(reax_ctx* c, const double* pos, const int* type, const double box[3]) {
   c->last_pos = pos;
   c->last_type = type;
   memcpy(c->last_box, box, sizeof(c->last_box));
+}
+
+reax_status do_build_lists(reax_ctx* c, int64_t n, const double* pos, const int* type, const double box[3],
+                           const reax_params* prm, const reax_cutoffs* cut, cudaStream_t s) {
+  reax_status r = prep_build(c, n, pos, type, box, prm, cut, s);
+  if (r != REAX_OK) return r;
+  int N = (int)n;
+  if (N > 0) {
+    launch_lists(c, N, pos, type, prm->ntypes, s);
+    launch_bonds(c, N, s);
+  }
+  if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
+  note_build(c, pos, type, box);
   r = read_status(c, s, !c->async);
   if (r != REAX_OK) return r;
   c->lists_ok = true;
@@ -617,36 +651,16 @@ reax_status do_bond_orders(reax_ctx* c, const reax_params* prm, const reax_cutof
   if (!c->bound || !c->lists_ok) return REAX_ERR_STATE;
   reax_status r = upload_params(c, prm, cut, s);
   if (r != REAX_OK) return r;
-  int N = (int)c->n;
-  if (N > 0) {
-    Timer t(c, 3, s);
-    k_bond_correct<<<148 * 8, TPB, 0, s>>>(c->w.brow, c->w.perm, c->w.stype, c->w.prm, c->w.bcol, c->w.bkey,
-                                           c->w.bown, c->w.bmir, c->w.bo, c->w.delta, c->cap.bond_cap, c->w.st);
-    LAUNCH(c);
-  }
+  if (c->n > 0) launch_bond_correct(c, s);
   if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
   c->bonds_ok = true;
   return REAX_OK;
 }
 
-reax_status do_nonbonded(reax_ctx* c, int64_t n, const double* pos, const int* type, const double* q,
-                         const double box[3], const reax_params* prm, const reax_cutoffs* cut, double* force,
-                         double* energy, cudaStream_t s) {
-  reax_status r = check_common(c, n, box, cut);
-  if (r != REAX_OK) return r;
-  if (!c->lists_ok) return REAX_ERR_STATE;
-  if (pos != c->last_pos || type != c->last_type || memcmp(box, c->last_box, sizeof(c->last_box)) != 0)
-    return REAX_ERR_STATE;
-  if (!energy || (n > 0 && (!q || !force))) return REAX_ERR_ARG;
-  r = upload_params(c, prm, cut, s);
-  if (r != REAX_OK) return r;
+// a7-a8: nonbonded energies and forces (reads the half list, spos, stype, perm/iperm)
+void launch_nonbonded(reax_ctx* c, int N, const double* q, double* force, double* energy, int nt, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
-  int N = (int)n;
-  if (N == 0) {
-    if (cudaMemsetAsync(energy, 0, 2 * sizeof(double), s) != cudaSuccess) return REAX_ERR_CUDA;
-    return REAX_OK;
-  }
   {
     Timer t(c, 5, s);
     k_nb_prep<<<nblk(N, TPB), TPB, 0, s>>>(N, q, w.perm, w.spos, w.sfx, w.sfy, w.sfz, w.st);
@@ -654,21 +668,80 @@ reax_status do_nonbonded(reax_ctx* c, int64_t n, const double* pos, const int* t
   }
   {
     Timer t(c, 4, s);
-    k_nonbonded<<<g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, prm->ntypes), s>>>(
+    k_nonbonded<<<g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, nt), s>>>(
         g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy,
         w.sfz, w.erow, c->nsplit, w.st);
     LAUNCH(c);
   }
   {
     Timer t(c, 5, s);
-    k_finalize_forces<<<nblk(N, TPB), TPB, 0, s>>>(N, w.iperm, w.sfx, w.sfy, w.sfz, force, w.st);
+    k_finalize_forces<<<nblk(N, TPB), TPB, 0, s>>>(N, w.iperm, (const long long*)w.sfx, (const long long*)w.sfy,
+                                                  (const long long*)w.sfz, force, w.st);
     LAUNCH(c);
     k_finalize_energy<<<nblk(N, FIN_THREADS * FIN_ITEMS), FIN_THREADS, 0, s>>>(N, w.erow, w.epart, w.ticket, energy,
                                                                                w.st);
     LAUNCH(c);
   }
+}
+
+reax_status check_nonbonded(reax_ctx* c, int64_t n, const double* pos, const int* type, const double* q,
+                            const double box[3], const reax_cutoffs* cut, double* force, double* energy) {
+  reax_status r = check_common(c, n, box, cut);
+  if (r != REAX_OK) return r;
+  if (!c->lists_ok) return REAX_ERR_STATE;
+  if (pos != c->last_pos || type != c->last_type || memcmp(box, c->last_box, sizeof(c->last_box)) != 0)
+    return REAX_ERR_STATE;
+  if (!energy || (n > 0 && (!q || !force))) return REAX_ERR_ARG;
+  return REAX_OK;
+}
+
+reax_status do_nonbonded(reax_ctx* c, int64_t n, const double* pos, const int* type, const double* q,
+                         const double box[3], const reax_params* prm, const reax_cutoffs* cut, double* force,
+                         double* energy, cudaStream_t s) {
+  reax_status r = check_nonbonded(c, n, pos, type, q, box, cut, force, energy);
+  if (r != REAX_OK) return r;
+  r = upload_params(c, prm, cut, s);
+  if (r != REAX_OK) return r;
+  if (n == 0) {
+    if (cudaMemsetAsync(energy, 0, 2 * sizeof(double), s) != cudaSuccess) return REAX_ERR_CUDA;
+    return REAX_OK;
+  }
+  launch_nonbonded(c, (int)n, q, force, energy, prm->ntypes, s);
   if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
   return read_status(c, s, !c->async);
+}
+
+// reax_step: lists on `s`, then a fork: the bond chain (a4-a6, small
+// latency-bound kernels) runs on the context's side stream while the
+// nonbonded kernel (a7-a8) runs on `s`; both only read the lists and the
+// sorted atoms.  The join makes `s` wait for the side stream, so the call is
+// stream-ordered on `s` as a whole (and capturable into one CUDA graph).
+reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, const double* q, const double box[3],
+                    const reax_params* prm, const reax_cutoffs* cut, double* force, double* energy, cudaStream_t s) {
+  reax_status r = prep_build(c, n, pos, type, box, prm, cut, s);
+  if (r != REAX_OK) return r;
+  if (!energy || (n > 0 && (!q || !force))) return REAX_ERR_ARG;
+  const int N = (int)n;
+  if (N == 0) {
+    note_build(c, pos, type, box);
+    c->lists_ok = c->bonds_ok = true;
+    if (cudaMemsetAsync(energy, 0, 2 * sizeof(double), s) != cudaSuccess) return REAX_ERR_CUDA;
+    return REAX_OK;
+  }
+  launch_lists(c, N, pos, type, prm->ntypes, s);
+  if (cudaEventRecord(c->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(c->side, c->ev_fork, 0) != cudaSuccess)
+    return REAX_ERR_CUDA;
+  launch_bonds(c, N, c->side);
+  launch_bond_correct(c, c->side);
+  launch_nonbonded(c, N, q, force, energy, prm->ntypes, s);
+  if (cudaEventRecord(c->ev_join, c->side) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join, 0) != cudaSuccess)
+    return REAX_ERR_CUDA;
+  if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
+  note_build(c, pos, type, box);
+  c->lists_ok = c->bonds_ok = true;
+  r = read_status(c, s, !c->async);
+  if (r != REAX_OK) c->lists_ok = c->bonds_ok = false;
+  return r;
 }
 
 }  // namespace
@@ -687,6 +760,7 @@ const char* reax_status_str(reax_status s) {
     case REAX_ERR_NONFINITE: return "non-finite input or output";
     case REAX_ERR_CUDA: return "CUDA error";
     case REAX_ERR_STATE: return "invalid call sequence or binding";
+    case REAX_ERR_RANGE: return "force contribution outside the fixed-point accumulator range (>= 65536 kcal/mol/A)";
   }
   return "unknown";
 }
@@ -703,6 +777,12 @@ reax_status reax_create(reax_ctx** out) {
     return REAX_ERR_CUDA;
   }
   memset(c->h_st, 0, sizeof(Status));
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    reax_destroy(c);
+    return REAX_ERR_CUDA;
+  }
   *out = c;
   return REAX_OK;
 }
@@ -717,6 +797,9 @@ reax_status reax_destroy(reax_ctx* c) {
     }
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_prm) cudaFreeHost(c->h_prm);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
   return REAX_OK;
 }
@@ -810,12 +893,7 @@ reax_status reax_step(reax_ctx* ctx, int64_t n, const double* pos, const int32_t
                       double* energy, void* stream) {
   if (!ctx) return REAX_ERR_ARG;
   ctx->launches_cur = 0;
-  cudaStream_t s = (cudaStream_t)stream;
-  reax_status r = do_build_lists(ctx, n, pos, type, box, params, cut, s);
-  if (r != REAX_OK) return r;
-  r = do_bond_orders(ctx, params, cut, s);
-  if (r != REAX_OK) return r;
-  r = do_nonbonded(ctx, n, pos, type, q, box, params, cut, force, energy, s);
+  reax_status r = do_step(ctx, n, pos, type, q, box, params, cut, force, energy, (cudaStream_t)stream);
   ctx->launches_step = ctx->launches_cur;
   return r;
 }
