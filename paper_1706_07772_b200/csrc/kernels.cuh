@@ -968,32 +968,74 @@ __device__ __forceinline__ void fix_add(unsigned* A, int* B, double t) {
 }
 
 constexpr int NB_THREADS = 256;
+constexpr int NB_WARPS = NB_THREADS / 32;
 #ifndef NB_MINB
-#define NB_MINB 3
+#define NB_MINB 2   // 2 CTAs x 8 warps at <= 128 registers (3 CTAs at 80 registers spills; measured slower)
 #endif
 
 constexpr int NB_MAX_ROWS = 256;   // rows of one (block, split) work unit that are ranked
 struct NBSmem {
   WinSmem W;
   double4 shift4[NWU_MAX];      // periodic image shift of each window cell (x, y, z, 0)
-  int next_row;
   int bad;
   int order[NB_MAX_ROWS];        // row window slots, longest row first
-  int rlen[NB_MAX_ROWS];
+  int rlen[NB_MAX_ROWS];         // their lengths
 };
 
+// Row r (rank order) of this CTA -> window slot and length.
+__device__ __forceinline__ void nb_row(const NBSmem& S, int r, int nsorted, int split, int nsplit,
+                                       const int* __restrict__ nbr_len, int& si, int& len) {
+  if (r < nsorted) {
+    si = S.order[r];
+    len = S.rlen[r];
+  } else {   // beyond the ranked rows (dense blocks): original order
+    int h;
+    row_of(S.W, split + r * nsplit, h, si);
+    const int k = c_win.home_k[h];
+    len = nbr_len[S.W.start[k] + (si - S.W.slot[k])];
+  }
+}
+
+// Warp stream position: the warp's k-th row (snake order over the ranked
+// rows: warp w takes ranks w, 2W-1-w, 2W+w, ... so every warp gets a similar
+// share of long and short rows) and its chunk c of 32 entries.
+struct NbPos {
+  int k, c, si, len;   // len < 0: end of stream
+};
+__device__ __forceinline__ void nb_pos_row(NbPos& p, const NBSmem& S, int nrows, int nsorted, int split, int nsplit,
+                                           const int* __restrict__ nbr_len, int warp) {
+  for (;;) {
+    const int r = p.k * NB_WARPS + ((p.k & 1) ? NB_WARPS - 1 - warp : warp);
+    if (r >= nrows) { p.len = -1; return; }
+    nb_row(S, r, nsorted, split, nsplit, nbr_len, p.si, p.len);
+    if (p.len > 0) return;
+    ++p.k;   // empty row
+  }
+}
+__device__ __forceinline__ void nb_pos_next(NbPos& p, const NBSmem& S, int nrows, int nsorted, int split, int nsplit,
+                                            const int* __restrict__ nbr_len, int warp) {
+  if (p.len < 0) return;
+  if ((p.c + 1) * 32 < p.len) { ++p.c; return; }
+  ++p.k;
+  p.c = 0;
+  nb_pos_row(p, S, nrows, nsorted, split, nsplit, nbr_len, warp);
+}
+
 // One CTA per (home block, split) (Alg. 2, re-designed): a
-// warp per row i streams its half-list entries (lanes over j); F_i stays in
-// registers and is warp-reduced once per row; F_j is accumulated in a
-// shared-memory fixed-point window (the block's private force array, the GPU
-// form of the paper's thread-private tprivForce) and flushed to the global
-// int64 sorted force array once per CTA.  Energies: per-row partials reduced
-// later in fixed order.  Forces and energies are bitwise reproducible.
+// warp streams the half-list entries of its rows 32 at a time (lanes over
+// j), with the next chunk's slot info and positions and the chunk after's
+// row entries in flight while the current chunk is evaluated (across row
+// boundaries).  F_i stays in registers and is warp-reduced once per row;
+// F_j is accumulated in a shared-memory fixed-point window (the block's
+// private force array, the GPU form of the paper's thread-private
+// tprivForce) and flushed to the global int64 sorted force array once per
+// CTA.  Energies: per-lane sums in a fixed pair order, one partial per warp,
+// reduced later in fixed order.  Forces and energies are bitwise reproducible.
 __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const int* __restrict__ cell_start,
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
     unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
-    double2* __restrict__ erow, int nsplit, Status* st) {
+    double2* __restrict__ epart, int nsplit, Status* st) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
   const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
@@ -1010,146 +1052,173 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   NBConst kc;
   kc.invR = prm->invR; kc.phalf = 0.5 * prm->p_vdw; kc.inv_p = prm->inv_p; kc.m140invR = -140.0 * prm->invR;
   const double C = prm->C;
-  int W = build_window(S.W, blk, g, cell_start);
-  const int lane = threadIdx.x & 31;
+  const int W = build_window(S.W, blk, g, cell_start);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (W > window_cap) {
     if (threadIdx.x == 0) {
       set_flag(st, ST_WIN_OVF);
       atomicMax(&st->max_window, W);
     }
+    if (lane == 0) epart[blockIdx.x * NB_WARPS + warp] = make_double2(0.0, 0.0);
     return;
   }
   const int nwu = c_win.nwu;
-  for (int k = threadIdx.x; k < nwu; k += blockDim.x) {   // thread per window cell (~15 atoms)
-    const int s0 = S.W.start[k], b0 = S.W.slot[k], c = S.W.cnt[k];
+  for (int k = threadIdx.x; k < nwu; k += blockDim.x)
     S.shift4[k] = make_double4(S.W.shift[k][0], S.W.shift[k][1], S.W.shift[k][2], 0.0);
-    for (int a = 0; a < c; ++a) sinfo[b0 + a] = make_int2(s0 + a, k | (stype[s0 + a] << 8));
+  // slot info, flattened over slots so that the type loads are all in flight
+  for (int t = threadIdx.x; t < W; t += blockDim.x) {
+    const int k = cell_of_slot(S.W, nwu, t);
+    const int j = S.W.start[k] + (t - S.W.slot[k]);
+    sinfo[t] = make_int2(j, k | (stype[j] << 8));
   }
-  for (int t = threadIdx.x; t < 3 * W; t += blockDim.x) {
-    fa[(t / W) * window_cap + t % W] = 0u;
-    fb[(t / W) * window_cap + t % W] = 0;
+#ifndef NB_EXP_NOZERO
+  for (int t = threadIdx.x; t < 3 * window_cap; t += blockDim.x) {
+    fa[t] = 0u;
+    fb[t] = 0;
   }
+#endif
   // this CTA's rows: split, split + nsplit, ... of the block (home sub-cell
-  // order), ranked longest first (rows are 90-370 pairs): longest-processing-
-  // time-first keeps the warps busy until the flush barrier
+  // order), ranked longest first (rows are 90-370 pairs)
   int nrows_blk = 0;
   for (int h = 0; h < NHOME; ++h)
     if (S.W.home_ok[h]) nrows_blk += S.W.cnt[c_win.home_k[h]];
   const int nrows = nrows_blk > split ? (nrows_blk - split + nsplit - 1) / nsplit : 0;
   const int nsorted = nrows < NB_MAX_ROWS ? nrows : NB_MAX_ROWS;
-  if (threadIdx.x == 0) { S.next_row = 0; S.bad = 0; }
-  __syncthreads();   // sinfo complete
-  for (int t = threadIdx.x; t < nsorted; t += blockDim.x) {
-    int h, si;
-    row_of(S.W, split + t * nsplit, h, si);
-    S.order[t] = si;
-    S.rlen[t] = nbr_len[sinfo[si].x];
+  if (threadIdx.x == 0) S.bad = 0;
+  static_assert(NB_MAX_ROWS <= NB_THREADS, "one ranked row per thread");
+  int my_si = 0, my_len = 0;
+  if ((int)threadIdx.x < nsorted) {
+    int h;
+    row_of(S.W, split + threadIdx.x * nsplit, h, my_si);
+    const int k = c_win.home_k[h];
+    my_len = nbr_len[S.W.start[k] + (my_si - S.W.slot[k])];
+    S.rlen[threadIdx.x] = my_len;
   }
   __syncthreads();
-  static_assert(NB_MAX_ROWS <= NB_THREADS, "one ranked row per thread");
-  {
-    const bool have = (int)threadIdx.x < nsorted;
-    int rank = 0, mrow = 0;
-    if (have) {
-      const int ml = S.rlen[threadIdx.x];
-      mrow = S.order[threadIdx.x];
-      for (int t = 0; t < nsorted; ++t) {
-        const int lt = S.rlen[t];
-        rank += (lt > ml) || (lt == ml && t < (int)threadIdx.x);
-      }
+  if ((int)threadIdx.x < nsorted) {
+    int rank = 0;
+    for (int t = 0; t < nsorted; ++t) {
+      const int lt = S.rlen[t];
+      rank += (lt > my_len) || (lt == my_len && t < (int)threadIdx.x);
     }
-    __syncthreads();
-    if (have) S.order[rank] = mrow;
+    S.order[rank] = my_si;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < nsorted) S.rlen[threadIdx.x] = 0;
+  __syncthreads();
+  if ((int)threadIdx.x < nsorted) {
+    // lengths in rank order (order[] is final now)
+    const int si = S.order[threadIdx.x];
+    S.rlen[threadIdx.x] = nbr_len[sinfo[si].x];
   }
   __syncthreads();
   const bool has_shift = S.W.has_shift != 0;
   const double FIXS = c_nb[25], MAGIC = c_nb[26], FLIM = c_nb[27];
   bool bad = false;
-  for (;;) {
-    int m = 0;
-    if (lane == 0) m = atomicAdd(&S.next_row, 1);
-    m = __shfl_sync(0xffffffffu, m, 0);
-    if (m >= nrows) break;
-    int si;
-    if (m < nsorted) {
-      si = S.order[m];
-    } else {
-      int h;
-      row_of(S.W, split + m * nsplit, h, si);
-    }
-    const int2 ii = sinfo[si];
-    const int s = ii.x;
-    const double4 xi = spos[s];
-    const NBPair* pci = pc + (ii.y >> 8) * nt;
-    const double cqi = C * xi.w;
-    const int len = nbr_len[s];
-    const uint16_t* row = nbr + (int64_t)s * row_cap;
-    double fix = 0.0, fiy = 0.0, fiz = 0.0, ev_acc = 0.0, ec_acc = 0.0;
-    // software pipeline: the next chunk's slot info and position are loaded
-    // while the current chunk is evaluated
-    int e = lane;
-    int slot = 0;
-    int2 inf = make_int2(0, 0);
-    double4 xj = make_double4(0, 0, 0, 0);
-    if (e < len) {
-      slot = row[e];
-      inf = sinfo[slot];
-      xj = spos[inf.x];
-    }
-    for (; e - lane < len; e += 32) {
-      const int cslot = slot;
-      const int2 cinf = inf;
-      const double4 cxj = xj;
-      const bool act = e < len;
-      const int en = e + 32;
-      if (en < len) {
-        slot = row[en];
-        inf = sinfo[slot];
-        xj = spos[inf.x];
-      }
-      if (act) {
-        double dx = cxj.x - xi.x, dy = cxj.y - xi.y, dz = cxj.z - xi.z;
-        if (has_shift) {   // block-uniform
-          const double4 sh = S.shift4[cinf.y & 255];
-          dx += sh.x;
-          dy += sh.y;
-          dz += sh.z;
-        }
-        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        double ev, ec, gg, dE;
-        nb_pair(r2, cqi * cxj.w, pci[cinf.y >> 8], kc, ET, LT, ev, ec, gg, dE);
-        ev_acc += ev;
-        ec_acc += ec;
-        fix = fma(gg, dx, fix);
-        fiy = fma(gg, dy, fiy);
-        fiz = fma(gg, dz, fiz);
-        bad |= !(fabs(dE) < FLIM);
-        const double gs = -gg * FIXS;
-        fix_add(fa + cslot, fb + cslot, fma(gs, dx, MAGIC));
-        fix_add(fa + window_cap + cslot, fb + window_cap + cslot, fma(gs, dy, MAGIC));
-        fix_add(fa + 2 * window_cap + cslot, fb + 2 * window_cap + cslot, fma(gs, dz, MAGIC));
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      fix += __shfl_xor_sync(0xffffffffu, fix, o);
-      fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
-      fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
-      ev_acc += __shfl_xor_sync(0xffffffffu, ev_acc, o);
-      ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
-    }
-    if (lane == 0) {
-      bad |= !(fabs(fix) < FLIM && fabs(fiy) < FLIM && fabs(fiz) < FLIM);
-      fix_add(fa + si, fb + si, fma(fix, FIXS, MAGIC));
-      fix_add(fa + window_cap + si, fb + window_cap + si, fma(fiy, FIXS, MAGIC));
-      fix_add(fa + 2 * window_cap + si, fb + 2 * window_cap + si, fma(fiz, FIXS, MAGIC));
-      erow[s] = make_double2(ev_acc, ec_acc);   // per-row energy: reduced later in row order
-    }
+  double ev_acc = 0.0, ec_acc = 0.0;
+  // ---- warp stream with a 2-deep software pipeline
+  NbPos pA, pB, pC;
+  pA.k = 0; pA.c = 0;
+  nb_pos_row(pA, S, nrows, nsorted, split, nsplit, nbr_len, warp);
+  pB = pA; nb_pos_next(pB, S, nrows, nsorted, split, nsplit, nbr_len, warp);
+  pC = pB; nb_pos_next(pC, S, nrows, nsorted, split, nsplit, nbr_len, warp);
+  auto row_entry = [&](const NbPos& p) -> int {
+    const int e = p.c * 32 + lane;
+    return (p.len > 0 && e < p.len) ? (int)nbr[(int64_t)sinfo[p.si].x * row_cap + e] : 0;
+  };
+  int slotA = row_entry(pA);
+  int2 infA = sinfo[slotA];
+  double4 xjA = spos[infA.x];
+  int slotB = row_entry(pB);
+  int slotC = row_entry(pC);
+  double4 xi = make_double4(0, 0, 0, 0);
+  const NBPair* pci = pc;
+  double cqi = 0.0;
+  if (pA.len > 0) {
+    const int2 ii = sinfo[pA.si];
+    xi = spos[ii.x];
+    pci = pc + (ii.y >> 8) * nt;
+    cqi = C * xi.w;
   }
+  double fix = 0.0, fiy = 0.0, fiz = 0.0;
+  while (pA.len > 0) {
+    // issue: B's slot info + positions, D's row entries, B's row atom
+    NbPos pD = pC;
+    nb_pos_next(pD, S, nrows, nsorted, split, nsplit, nbr_len, warp);
+    const int2 infB = sinfo[slotB];
+    const double4 xjB = spos[infB.x];
+#ifndef NB_NO_PREFETCH
+    if (pC.len > 0 && pC.c * 32 + lane < pC.len)   // chunk after next: its positions into L1
+      asm volatile("prefetch.global.L1 [%0];" :: "l"(spos + sinfo[slotC].x));
+#endif
+    const int slotD = row_entry(pD);
+    const bool newrow = pB.len < 0 || pB.k != pA.k;
+    int2 iiB = make_int2(0, 0);
+    double4 xiB = xi;
+    if (newrow && pB.len > 0) {
+      iiB = sinfo[pB.si];
+      xiB = spos[iiB.x];
+    }
+    // evaluate A
+    if (pA.c * 32 + lane < pA.len) {
+      double dx = xjA.x - xi.x, dy = xjA.y - xi.y, dz = xjA.z - xi.z;
+      if (has_shift) {   // block-uniform
+        const double4 sh = S.shift4[infA.y & 255];
+        dx += sh.x;
+        dy += sh.y;
+        dz += sh.z;
+      }
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      double ev, ec, gg, dE;
+      nb_pair(r2, cqi * xjA.w, pci[infA.y >> 8], kc, ET, LT, ev, ec, gg, dE);
+      ev_acc += ev;
+      ec_acc += ec;
+      fix = fma(gg, dx, fix);
+      fiy = fma(gg, dy, fiy);
+      fiz = fma(gg, dz, fiz);
+      bad |= !(fabs(dE) < FLIM);
+      const double gs = -gg * FIXS;
+      fix_add(fa + slotA, fb + slotA, fma(gs, dx, MAGIC));
+      fix_add(fa + window_cap + slotA, fb + window_cap + slotA, fma(gs, dy, MAGIC));
+      fix_add(fa + 2 * window_cap + slotA, fb + 2 * window_cap + slotA, fma(gs, dz, MAGIC));
+    }
+    if (newrow) {   // A was the last chunk of its row: F_i
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        fix += __shfl_xor_sync(0xffffffffu, fix, o);
+        fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
+        fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
+      }
+      if (lane == 0) {
+        const int si = pA.si;
+        bad |= !(fabs(fix) < FLIM && fabs(fiy) < FLIM && fabs(fiz) < FLIM);
+        fix_add(fa + si, fb + si, fma(fix, FIXS, MAGIC));
+        fix_add(fa + window_cap + si, fb + window_cap + si, fma(fiy, FIXS, MAGIC));
+        fix_add(fa + 2 * window_cap + si, fb + 2 * window_cap + si, fma(fiz, FIXS, MAGIC));
+      }
+      fix = 0.0; fiy = 0.0; fiz = 0.0;
+      xi = xiB;
+      pci = pc + (iiB.y >> 8) * nt;
+      cqi = C * xi.w;
+    }
+    // rotate
+    pA = pB; pB = pC; pC = pD;
+    slotA = slotB; infA = infB; xjA = xjB;
+    slotB = slotC; slotC = slotD;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ev_acc += __shfl_xor_sync(0xffffffffu, ev_acc, o);
+    ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
+  }
+  if (lane == 0) epart[blockIdx.x * NB_WARPS + warp] = make_double2(ev_acc, ec_acc);
   if (__any_sync(0xffffffffu, bad) && lane == 0) S.bad = 1;
   __syncthreads();
   if (threadIdx.x == 0 && S.bad) set_flag(st, ST_RANGE);
   unsigned long long* gf[3] = {sfx, sfy, sfz};
+#ifdef NB_EXP_NOFLUSH
+  if (W > 0) return;
+#endif
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
     const int j = sinfo[t].x;
 #pragma unroll

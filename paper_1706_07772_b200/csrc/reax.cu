@@ -23,9 +23,9 @@ constexpr int MAX_SPLIT = 8;
 // CTAs per home block for the window kernels: small systems (c0/c1) have too
 // few home blocks to fill 148 SMs, so each block's rows are split over
 // several CTAs (each builds the same window)
-int choose_split(int nblock) {
-  int per_sm = 8;
-  if (const char* e = getenv("REAX_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));   // tuning experiments
+// (measured on c1: nonbonded best at 4 CTA-units per SM, list build at 6)
+int choose_split(int nblock, int per_sm, const char* env) {
+  if (const char* e = getenv(env)) per_sm = std::max(1, atoi(e));   // tuning experiments
   int target = 148 * per_sm;
   int s = (target + nblock - 1) / std::max(nblock, 1);
   return std::max(1, std::min(MAX_SPLIT, s));
@@ -332,8 +332,8 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
   t.sfx = (unsigned long long*)take(sizeof(long long) * N);
   t.sfy = (unsigned long long*)take(sizeof(long long) * N);
   t.sfz = (unsigned long long*)take(sizeof(long long) * N);
-  t.erow = (double2*)take(sizeof(double2) * N);
-  t.epart = (double*)take(sizeof(double) * 2 * ((size_t)nblk((int64_t)N, FIN_THREADS * FIN_ITEMS) + 1));
+  t.erow = (double2*)take(sizeof(double2) * std::max<size_t>(N, (size_t)g.nblock * MAX_SPLIT * NB_WARPS));
+  t.epart = (double*)take(sizeof(double) * 2 * ((size_t)nblk((int64_t)std::max<size_t>(N, (size_t)g.nblock * MAX_SPLIT * NB_WARPS), FIN_THREADS * FIN_ITEMS) + 1));
   t.ticket = (unsigned*)take(sizeof(unsigned) * 4);
   t.ucol = (int*)take(sizeof(int) * (size_t)c.bond_cap);
   t.ukey = (int*)take(sizeof(int) * (size_t)c.bond_cap);
@@ -393,6 +393,7 @@ struct reax_ctx {
   // fork/join of reax_step (bond chain beside the nonbonded kernel)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool serial = getenv("REAX_SERIAL") != nullptr;
 };
 
 namespace {
@@ -678,8 +679,9 @@ void launch_nonbonded(reax_ctx* c, int N, const double* q, double* force, double
     k_finalize_forces<<<nblk(N, TPB), TPB, 0, s>>>(N, w.iperm, (const long long*)w.sfx, (const long long*)w.sfy,
                                                   (const long long*)w.sfz, force, w.st);
     LAUNCH(c);
-    k_finalize_energy<<<nblk(N, FIN_THREADS * FIN_ITEMS), FIN_THREADS, 0, s>>>(N, w.erow, w.epart, w.ticket, energy,
-                                                                               w.st);
+    const int nparts = g.nblock * c->nsplit * NB_WARPS;   // one energy partial per nonbonded warp
+    k_finalize_energy<<<nblk(nparts, FIN_THREADS * FIN_ITEMS), FIN_THREADS, 0, s>>>(nparts, w.erow, w.epart, w.ticket,
+                                                                                   energy, w.st);
     LAUNCH(c);
   }
 }
@@ -729,12 +731,16 @@ reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, 
     return REAX_OK;
   }
   launch_lists(c, N, pos, type, prm->ntypes, s);
-  if (cudaEventRecord(c->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(c->side, c->ev_fork, 0) != cudaSuccess)
+  // REAX_SERIAL=1 (measurement only): everything on `s`, so per-kernel event
+  // times are not shared between concurrent kernels
+  const bool fork = !c->serial;
+  cudaStream_t sb = fork ? c->side : s;
+  if (fork && (cudaEventRecord(c->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(sb, c->ev_fork, 0) != cudaSuccess))
     return REAX_ERR_CUDA;
-  launch_bonds(c, N, c->side);
-  launch_bond_correct(c, c->side);
+  launch_bonds(c, N, sb);
+  launch_bond_correct(c, sb);
   launch_nonbonded(c, N, q, force, energy, prm->ntypes, s);
-  if (cudaEventRecord(c->ev_join, c->side) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join, 0) != cudaSuccess)
+  if (fork && (cudaEventRecord(c->ev_join, sb) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join, 0) != cudaSuccess))
     return REAX_ERR_CUDA;
   if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
   note_build(c, pos, type, box);
@@ -847,8 +853,8 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   ctx->g = g;
   ctx->n = n;
   ctx->cap = c;
-  ctx->nsplit = choose_split(g.nblock);
-  ctx->nsplit_nbr = ctx->nsplit;
+  ctx->nsplit = choose_split(g.nblock, 4, "REAX_CTAS_PER_SM");
+  ctx->nsplit_nbr = choose_split(g.nblock, 6, "REAX_NBR_CTAS_PER_SM");
   if (const char* e = getenv("REAX_NBR_SPLIT")) ctx->nsplit_nbr = std::max(1, std::min(MAX_SPLIT, atoi(e)));
   ctx->cut = *cut;
   ctx->prm_valid = false;

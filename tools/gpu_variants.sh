@@ -1,4 +1,16 @@
+# usage: bash tools/gpu_variants.sh lib1.so lib2.so ...  -- quick parity (c0/c1) + serial and forked bench per library
 set -x
-python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
-python bench.py --steps 50 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
-python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b3.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_nbr_build|k_nonbonded" -s 2 -c 2 -o gpurun_out/prof_r01i python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu2.log 2>&1; tail -1 gpurun_out/ncu2.log
+mkdir -p gpurun_out
+for L in "$@"; do
+  T=$(basename $L .so)
+  REAX_LIBRARY=$PWD/$L timeout 600 python -m pytest tests/test_parity_gpu.py -m gpu -q -x -p no:cacheprovider -k "c0_full or c1_full or deterministic or graph" > gpurun_out/var_$T.test 2>&1; tail -1 gpurun_out/var_$T.test
+  REAX_LIBRARY=$PWD/$L REAX_SERIAL=1 timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/var_${T}_serial.json 2>/dev/null
+  REAX_LIBRARY=$PWD/$L timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/var_${T}.json 2>/dev/null
+  python - "$T" <<'PY'
+import json, sys
+t = sys.argv[1]
+for suf in ("_serial", ""):
+    d = json.load(open(f"gpurun_out/var_{t}{suf}.json"))
+    print(t + suf, "ms/step %.4f" % d["ms_per_step"], {k: round(v * 1000, 1) for k, v in d["kernel_ms_per_step"].items()})
+PY
+done

@@ -62,6 +62,28 @@ __global__ void smk(double* out, int iters) {
   if (acc == 12345.678 || s[threadIdx.x] == 1e300) out[blockIdx.x] = acc;
 }
 
+// dependent-chain latency: one warp per SM, one chain
+template <int OP>
+__global__ void latk(double* out, int iters, double a) {
+  double x = 1.0 + threadIdx.x * 1e-9;
+  int ix = threadIdx.x;
+  __shared__ double tbl[64];
+  if (threadIdx.x < 64) tbl[threadIdx.x] = 1.0 + threadIdx.x * 1e-9;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    if (OP == 0) x = fma(x, a, 1e-9);
+    if (OP == 1) x = x * a;
+    if (OP == 2) x = x + a;
+    if (OP == 3) { asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(x) : "d"(x)); }
+    if (OP == 4) { x = tbl[(__double2loint(x) + it) & 63]; }              // LDS + int op
+    if (OP == 5) { ix = ix * 3 + 1; ix ^= ix >> 3; }                       // 2 int ops
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = (double)(t1 - t0) / iters;
+  if (x == 12345.678 || ix == 7) out[1000 + blockIdx.x] = x + ix;
+}
+
 int main() {
   cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0));
   int sms = p.multiProcessorCount;
@@ -95,6 +117,20 @@ int main() {
     double n = (double)blocks * thr * iters;
     printf("%-34s %.3f ms  %.2f lane-ops/SM-cycle\n", name, ms, n / (ms * 1e-3) / sms / clk);
   };
+  auto lat = [&](const char* name, void (*k)(double*, int, double)) {
+    double* o; CK(cudaMalloc(&o, 4096 * 8));
+    k<<<sms, 32>>>(o, 10000, 0.9999999);
+    CK(cudaDeviceSynchronize());
+    double h; CK(cudaMemcpy(&h, o, 8, cudaMemcpyDeviceToHost));
+    printf("latency %-24s %.1f cycles/op\n", name, h);
+    cudaFree(o);
+  };
+  lat("DFMA", latk<0>);
+  lat("DMUL", latk<1>);
+  lat("DADD", latk<2>);
+  lat("MUFU.RSQ64H", latk<3>);
+  lat("LDS.64 (+int)", latk<4>);
+  lat("2 int ops", latk<5>);
   runs("smem LDS.64 random", smk<0>);
   runs("smem ATOMS.ADD int32 random", smk<1>);
   runs("smem atomicAdd f64 (CAS) random", smk<2>);

@@ -3,7 +3,9 @@ backward-branch region holding >= 30 DFMA): python tools/sass_loop.py k_nonbonde
 import re, subprocess, sys
 from collections import Counter
 kern = sys.argv[1]
-lib = sys.argv[2] if len(sys.argv) > 2 else "paper_1706_07772_b200/libreax.so"
+lib = sys.argv[2] if len(sys.argv) > 2 and sys.argv[2] != "-" else "paper_1706_07772_b200/libreax.so"
+OPC = sys.argv[3] if len(sys.argv) > 3 else "DFMA"
+MINC = int(sys.argv[4]) if len(sys.argv) > 4 else 30
 out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s+Function : ", out)
 f = [x for x in funcs if x.split("\n")[0].find(kern) >= 0][0]
@@ -20,8 +22,8 @@ for i, (a, t) in enumerate(ins):
         tgt = int(m.group(1), 16)
         if tgt < a and tgt in addr:
             n = i - addr[tgt]
-            ndfma = sum(1 for _, u in ins[addr[tgt]:i + 1] if "DFMA" in u)
-            if ndfma >= 30 and (best is None or n < best[0]):
+            ndfma = sum(1 for _, u in ins[addr[tgt]:i + 1] if OPC in u)
+            if ndfma >= MINC and (best is None or n < best[0]):
                 best = (n, addr[tgt], i)
 n, lo, hi = best
 c = Counter()
