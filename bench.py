@@ -306,13 +306,26 @@ def main():
                "api": "reax_step_host (pinned host buffers in/out, copies inside the timed region)"}
     clocks = sample_clocks_stop(clk)
 
-    nb_ms, nb_launches = kms["nonbonded"]
-    nb_launches = args.steps
-    nb_avg_s = nb_ms / max(nb_launches, 1) * 1e-3
+    nb_ms, _ = kms["nonbonded"]
+    nb_avg_s = nb_ms / args.steps * 1e-3
     achieved = W_NB_DP_PER_PAIR * P / nb_avg_s
-    nbr_ms, nbr_launches = kms["nbr"]
-    nbr_launches = args.steps
-    nbr_avg_s = nbr_ms / max(nbr_launches, 1) * 1e-3
+    fused = kms["nbr"][0] == 0.0     # reax_step ran the fused list + nonbonded kernel
+    # list build on its own (the reax_build_lists path: k_nbr_build), timed
+    # after the passes above (not part of `value`) for its roofline line
+    lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+    lctx = rx.Reax(n, s.box, params, gen.CUTOFFS, device=dev)
+    lctx.build_lists(pos, typ)
+    lctx.set_async(True)
+    lctx.set_timing(True)
+    lctx.kernel_ms(reset=True)
+    for k in range(10):
+        flush.fill_(float(k))
+        lctx.build_lists(pos, typ)
+    torch.cuda.synchronize()
+    lctx.check()
+    lk = lctx.kernel_ms(reset=True)
+    nbr_avg_s = lk["nbr"][0] / 10 * 1e-3
+    del lctx
     nbr_bytes = n * NBR_BYTES_PER_ATOM_FIXED + P * NBR_BYTES_PER_PAIR + 2.9 * n * NBR_BYTES_PER_BONDCAND
     hbm_peak = None
     try:
@@ -320,9 +333,10 @@ def main():
     except Exception:
         hbm_peak = 6650.0   # B200_PROFILING.md fallback
     traffic = None
+    kname = "k_step_nb" if fused else "k_nonbonded"
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof.get(f"c{args.config}", {}).get("k_nonbonded", {}).get("dram_bytes_per_launch")
+        traffic = prof.get(f"c{args.config}", {}).get(kname, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
     step_total_ms = sum(v[0] for v in kms.values())
@@ -335,13 +349,14 @@ def main():
                    "parallelism": "replicas" if world > 1 else "single GPU",
                    "launch": "direct launches" if args.no_graph else "CUDA graph replay of reax_step (async mode)"},
         "ns_per_atom_step": 1e9 / value * world if value else None,
-        "roofline": {"bound": "alu", "kernel": "k_nonbonded (a7)", "achieved": achieved / 1e12, "peak": peak_dfma / 1e12,
+        "roofline": {"bound": "alu", "kernel": "k_step_nb (a3 half list + a7-a8 nonbonded, fused)" if fused else "k_nonbonded (a7)",
+                     "achieved": achieved / 1e12, "peak": peak_dfma / 1e12,
                      "unit": "T FP64-pipe thread-instructions/s", "frac": achieved / peak_dfma,
                      "traffic": traffic, "work": f"{W_NB_DP_PER_PAIR:.0f} DP inst/pair x {P} pairs per launch",
                      "peak_source": "DFMA probe measured in this run (tools/peak.cu); MEASURED_PEAKS.json has no FP64 entry",
                      "avg_launch_ms": nb_avg_s * 1e3},
         "roofline_kernels": [
-            {"kernel": "k_nbr_build (a3-a4)", "bound": "hbm", "achieved": nbr_bytes / nbr_avg_s / 1e9, "peak": hbm_peak,
+            {"kernel": "k_nbr_build (a3-a4; reax_build_lists path, timed separately)", "bound": "hbm", "achieved": nbr_bytes / nbr_avg_s / 1e9, "peak": hbm_peak,
              "unit": "GB/s", "frac": nbr_bytes / nbr_avg_s / 1e9 / hbm_peak, "avg_launch_ms": nbr_avg_s * 1e3,
              "bytes_per_launch": nbr_bytes},
         ],

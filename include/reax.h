@@ -96,6 +96,10 @@ typedef struct {
   int32_t window_cap; /* max atoms in one home block's neighbour window (default 2048) */
 } reax_capacity;
 
+/* Text of the CUDA error behind the last REAX_ERR_CUDA returned on this host
+ * thread ("no error" if none).  Static storage; never NULL. */
+const char* reax_last_cuda_error(void);
+
 const char* reax_status_str(reax_status s);
 
 reax_status reax_create(reax_ctx** out);

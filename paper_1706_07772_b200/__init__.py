@@ -25,7 +25,7 @@ EXPORTED = ("reax_status_str", "reax_create", "reax_destroy", "reax_workspace_by
             "reax_required", "reax_build_lists", "reax_bond_orders", "reax_nonbonded", "reax_step",
             "reax_step_host", "reax_set_async", "reax_check", "reax_set_timing", "reax_kernel_ms",
             "reax_launches_per_step", "reax_pair_count", "reax_export_pairs", "reax_export_nbr_digest",
-            "reax_export_bonds", "reax_selftest_math")
+            "reax_export_bonds", "reax_selftest_math", "reax_last_cuda_error")
 
 
 class ReaxError(RuntimeError):
@@ -71,6 +71,7 @@ def load_library(path: str = LIB_PATH):
     V, I32, I64, P = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
     sig = {
         "reax_status_str": (ctypes.c_char_p, [ctypes.c_int]),
+        "reax_last_cuda_error": (ctypes.c_char_p, []),
         "reax_create": (ctypes.c_int, [ctypes.POINTER(V)]),
         "reax_destroy": (ctypes.c_int, [V]),
         "reax_workspace_bytes": (ctypes.c_int, [I64, P, P, P, ctypes.POINTER(ctypes.c_size_t), P]),
@@ -106,7 +107,10 @@ def status_str(code: int) -> str:
 
 def _check(code: int, what: str):
     if code != OK:
-        raise ReaxError(code, f"{what}: {status_str(code)}")
+        msg = f"{what}: {status_str(code)}"
+        if code == ERR_CUDA:
+            msg += " [" + _lib.reax_last_cuda_error().decode() + "]"
+        raise ReaxError(code, msg)
 
 
 class _ParamsHolder:

@@ -284,7 +284,7 @@ struct WinSmem {
   int start[NWU_MAX];       // first sorted atom of each used window cell
   int cnt[NWU_MAX];
   int slot[NWU_MAX + 1];    // slot base (prefix of cnt)
-  double shift[NWU_MAX][3]; // periodic image shift (0 or +-L) of each window cell
+  double4 shift[NWU_MAX];   // periodic image shift (0 or +-L) of each window cell (x, y, z, 0)
   int home_ok[NHOME];       // home sub-cell exists (odd nc leaves the last block partial)
   int has_shift;            // some window cell is a periodic image
 };
@@ -300,14 +300,16 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
     int wb = c_win.wu[k];
     int wv[3] = {wb % WB, (wb / WB) % WB, wb / (WB * WB)};
     int cc[3];
+    double sh[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       int u = base[a] + wv[a] - SR;          // unwrapped sub-cell
       int m = u >= 0 ? u / g.nc[a] : -((-u + g.nc[a] - 1) / g.nc[a]);  // floor(u / nc)
       cc[a] = u - m * g.nc[a];
-      W.shift[k][a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
+      sh[a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
       my_shift |= (m != 0);
     }
+    W.shift[k] = make_double4(sh[0], sh[1], sh[2], 0.0);
     int cid = (cc[2] * g.nc[1] + cc[1]) * g.nc[0] + cc[0];
     int s0 = cell_start[cid];
     W.start[k] = s0;
@@ -387,18 +389,151 @@ struct NbrSmem {
   int next_row;
 };
 
+// Per-kernel constants of the half-list candidate test.
+struct RowTest {
+  float R2lo, R2mid, R2half, Rt, hy, hz, ihx;
+  double R2;
+};
+__device__ __forceinline__ RowTest make_rowtest(const DevParams* __restrict__ prm, const Grid& g) {
+  RowTest t;
+  t.R2lo = prm->R2lo;
+  t.R2mid = 0.5f * (prm->R2lo + prm->R2hi);
+  t.R2half = 0.5f * (prm->R2hi - prm->R2lo);
+  t.Rt = sqrtf(prm->R2hi) + 1e-3f;                 // trimming radius (conservative)
+  t.hy = (float)g.h[1];
+  t.hz = (float)g.h[2];
+  t.ihx = 1.0f / (float)g.h[0];
+  t.R2 = prm->R2;
+  return t;
+}
+// window slot -> (sorted atom, window cell): two staging layouts
+struct SlotJK {
+  const int* j;
+  const unsigned char* k;
+  __device__ __forceinline__ int J(int t) const { return j[t]; }
+  __device__ __forceinline__ int K(int t) const { return k[t]; }
+};
+struct SlotInfo {
+  const int2* s;
+  __device__ __forceinline__ int J(int t) const { return s[t].x; }
+  __device__ __forceinline__ int K(int t) const { return s[t].y & 255; }
+};
+
+// One row's half-list candidate test (one warp; Write Lists).
+// The candidate stream of row i (window slot si, home sub-cell h) is the
+// concatenation of intervals, one per lane: the forward runs of its
+// sub-cell's half stencil (rows of cells along x), each trimmed to the cells
+// whose x-extent meets [x_i - w, x_i + w] with w = sqrt(R^2 - d_yz^2) (d_yz:
+// distance from atom i to the run's y-z cross-section, so no partner is ever
+// trimmed), plus its own cell after i.  Lanes walk the stream 32 candidates
+// at a time: r^2 in fp32 against a band of +-m around R^2 (~70x the fp32
+// error bound), the band settled by the exact FMA-free fp64 test (bit-
+// identical to the oracle's r^2); accepted window slots are compacted with a
+// ballot and stored coalesced to row[].  With BOND, candidates below the
+// conservative BO' = bo_cut radius are compacted the same way into crow[].
+// Returns the row length (which may exceed row_cap: the caller flags it).
+template <bool BOND, typename SI>
+__device__ __forceinline__ int nbr_row_test(const WinSmem& W, const Grid& g, int Wslots, const float4* __restrict__ cand,
+                                            SI sl, const double4* __restrict__ spos, int s, int si, int h,
+                                            const RowTest& rt, uint16_t* row, int row_cap, int* crow, int cand_cap,
+                                            const float* rc2row, float rcmax, int& nc_out) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u, le_mask = lt_mask | (1u << lane);
+  const float4 ri = cand[si];
+  const int kh = c_win.home_k[h];
+  // ---- intervals: lane q < nrun trims run q, lane nrun takes the own cell
+  const int nrun = c_win.nrun1[h];
+  int ia = 0, il = 0;
+  if (lane < nrun) {
+    const int ka = c_win.run1_a[h][lane], kb = c_win.run1_b[h][lane];
+    const int wba = c_win.wu[ka];
+    const int wxa = wba % WB - SR;                   // x cell offset (block frame) of the run's first cell
+    const float oy = (float)((wba / WB % WB - SR) * g.h[1]);
+    const float oz = (float)((wba / (WB * WB) - SR) * g.h[2]);
+    const float dy = fmaxf(0.f, fmaxf(oy - ri.y, ri.y - (oy + rt.hy)));
+    const float dz = fmaxf(0.f, fmaxf(oz - ri.z, ri.z - (oz + rt.hz)));
+    const float w2 = rt.Rt * rt.Rt - (dy * dy + dz * dz);
+    if (w2 >= 0.f) {
+      const float w = sqrtf(w2) + 1e-3f;
+      // cells c (block frame) with [c hx, (c+1) hx] meeting [x - w, x + w]
+      const int c0 = max(wxa, (int)floorf((ri.x - w) * rt.ihx));
+      const int c1 = min(wxa + (kb - ka), (int)floorf((ri.x + w) * rt.ihx));
+      if (c0 <= c1) {
+        ia = W.slot[ka + (c0 - wxa)];
+        il = W.slot[ka + (c1 - wxa) + 1] - ia;
+      }
+    }
+  } else if (lane == nrun) {
+    ia = si + 1;
+    il = W.slot[kh + 1] - ia;
+  }
+  // compact the non-empty intervals, then exclusive offsets
+  const unsigned ne = __ballot_sync(0xffffffffu, il > 0);
+  int inc = il;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, inc, 31);
+  const int start_q = inc - il;                       // stream position where my interval starts
+  // compacted interval table: lane t holds the t-th non-empty interval's
+  // (start position, slot - position shift); intervals keep their order
+  const unsigned src = __fns(ne, 0, lane + 1);      // lane of the (lane+1)-th set bit
+  const int srcl = src < 32 ? (int)src : 0;
+  const int cstart = __shfl_sync(0xffffffffu, start_q, srcl);
+  const int cshift = __shfl_sync(0xffffffffu, ia - start_q, srcl);
+  const int nint = __popc(ne);
+  int len = 0, nc = 0;
+  for (int p0 = 0; p0 < total; p0 += 32) {
+    // interval of each lane: the intervals starting inside this chunk mark
+    // their start position; lane l belongs to the latest start <= p0 + l
+    const int rel = cstart - p0;
+    const bool here = lane < nint && rel >= 0 && rel < 32;
+    const unsigned M = __reduce_or_sync(0xffffffffu, here ? (1u << rel) : 0u);
+    const int before = __popc(__ballot_sync(0xffffffffu, lane < nint && rel < 0));
+    const int q = before + __popc(M & le_mask) - 1;
+    const int p = p0 + lane;
+    const int slot = p + __shfl_sync(0xffffffffu, cshift, q);
+    const bool valid = p < total;
+    const float4 c = cand[valid ? slot : Wslots];   // Wslots: sentinel
+    const float dx = c.x - ri.x, dy = c.y - ri.y, dz = c.z - ri.z;
+    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    bool in = r2 < rt.R2lo;
+    const bool band = fabsf(r2 - rt.R2mid) <= rt.R2half && !in;
+    if (__any_sync(0xffffffffu, band)) {
+      if (band) {  // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
+        const double4 xi = spos[s];
+        const double4 xj = spos[sl.J(slot)];
+        const double4 sh = W.shift[sl.K(slot)];
+        const double ex = __dadd_rn(__dsub_rn(xj.x, xi.x), sh.x);
+        const double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), sh.y);
+        const double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), sh.z);
+        const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+        in = d2 <= rt.R2;
+      }
+    }
+    const unsigned mk = __ballot_sync(0xffffffffu, in);
+    const int pp = len + __popc(mk & lt_mask);
+    if (in && pp < row_cap) row[pp] = (uint16_t)slot;
+    len += __popc(mk);
+    if (BOND) {
+      if (__any_sync(0xffffffffu, in && r2 <= rcmax)) {  // rare: ~3 bond candidates per row
+        const bool bcand = in && r2 <= rc2row[__float_as_int(c.w)];
+        const unsigned mb = __ballot_sync(0xffffffffu, bcand);
+        const int pc = nc + __popc(mb & lt_mask);
+        if (bcand && pc < cand_cap) crow[pc] = sl.J(slot);
+        nc += __popc(mb);
+      }
+    }
+  }
+  nc_out = nc;
+  return len;
+}
+
 // One CTA per (home block, split).  Candidates of the window are staged in
 // shared memory as fp32 coordinates relative to the block origin.  A warp
-// takes one row (atom) at a time.  Its candidate stream is the concatenation
-// of intervals, one per lane: the forward runs of its sub-cell's half stencil
-// (rows of cells along x), each trimmed to the cells whose x-extent meets
-// [x_i - w, x_i + w] with w = sqrt(R^2 - d_yz^2) (d_yz: distance from atom i to
-// the run's y-z cross-section, so no partner is ever trimmed), plus its own
-// cell after i.  Lanes walk the stream 32 candidates at a time: r^2 in fp32
-// against a band of +-m around R^2 (~70x the fp32 error bound), the band
-// settled by the exact FMA-free fp64 test; accepted window slots are
-// compacted with a ballot and stored coalesced.  Bond candidates (r^2 below the
-// conservative BO' = bo_cut radius) are compacted the same way.
+// takes one row (atom) at a time and runs nbr_row_test on it (with bond
+// candidates).
 __global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int* __restrict__ cell_start,
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
@@ -411,11 +546,11 @@ __global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int*
   unsigned char* cand_k = reinterpret_cast<unsigned char*>(cand_j + window_cap + 32);
   const int nt = prm->nt;
   for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) S.rcand2[t] = prm->rcand2[t];
-  const float R2lo = prm->R2lo, R2hi = prm->R2hi, rcmax = prm->rcand2_max;
-  const double R2 = prm->R2;
+  const float rcmax = prm->rcand2_max;
+  const RowTest rt = make_rowtest(prm, g);
   int W = build_window(S.W, blk, g, cell_start);
   const int nwu = c_win.nwu;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {   // row table of the block (rows in home sub-cell order)
     int r = 0;
     for (int h = 0; h < NHOME; ++h) {
@@ -467,10 +602,7 @@ __global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int*
   }
   if (threadIdx.x < 32) cand[W + threadIdx.x] = make_float4(1e30f, 1e30f, 1e30f, 0.f);  // sentinel
   __syncthreads();
-  const unsigned lt_mask = (1u << lane) - 1u, le_mask = lt_mask | (1u << lane);
-  const float R2mid = 0.5f * (R2lo + R2hi), R2half = 0.5f * (R2hi - R2lo);
-  const float Rt = sqrtf(R2hi) + 1e-3f;                 // trimming radius (conservative)
-  const float hx = (float)g.h[0], hy = (float)g.h[1], hz = (float)g.h[2], ihx = 1.0f / hx;
+  const SlotJK sl{cand_j, cand_k};
   for (;;) {
     int m = 0;
     if (lane == 0) m = atomicAdd(&S.next_row, 1);
@@ -479,101 +611,17 @@ __global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int*
     if (r >= nrows) break;
     int h, si;
     if (r < MAX_BLOCK_ROWS) {
-      const int rt = S.rowtab[r];
-      h = rt & 7;
-      si = rt >> 3;
+      const int rtb = S.rowtab[r];
+      h = rtb & 7;
+      si = rtb >> 3;
     } else {   // pathological density: beyond the table
       row_of(S.W, r, h, si);
     }
     const int s = cand_j[si];
-    const float4 ri = cand[si];
-    const int ti = __float_as_int(ri.w);
-    const int kh = c_win.home_k[h];
-    // ---- intervals: lane q < nrun trims run q, lane nrun takes the own cell
-    const int nrun = c_win.nrun1[h];
-    int ia = 0, il = 0;
-    if (lane < nrun) {
-      const int ka = c_win.run1_a[h][lane], kb = c_win.run1_b[h][lane];
-      const int wba = c_win.wu[ka];
-      const int wxa = wba % WB - SR;                   // x cell offset (block frame) of the run's first cell
-      const float oy = (float)((wba / WB % WB - SR) * g.h[1]);
-      const float oz = (float)((wba / (WB * WB) - SR) * g.h[2]);
-      const float dy = fmaxf(0.f, fmaxf(oy - ri.y, ri.y - (oy + hy)));
-      const float dz = fmaxf(0.f, fmaxf(oz - ri.z, ri.z - (oz + hz)));
-      const float w2 = Rt * Rt - (dy * dy + dz * dz);
-      if (w2 >= 0.f) {
-        const float w = sqrtf(w2) + 1e-3f;
-        // cells c (block frame) with [c hx, (c+1) hx] meeting [x - w, x + w]
-        const int c0 = max(wxa, (int)floorf((ri.x - w) * ihx));
-        const int c1 = min(wxa + (kb - ka), (int)floorf((ri.x + w) * ihx));
-        if (c0 <= c1) {
-          ia = S.W.slot[ka + (c0 - wxa)];
-          il = S.W.slot[ka + (c1 - wxa) + 1] - ia;
-        }
-      }
-    } else if (lane == nrun) {
-      ia = si + 1;
-      il = S.W.slot[kh + 1] - ia;
-    }
-    // compact the non-empty intervals, then exclusive offsets
-    const unsigned ne = __ballot_sync(0xffffffffu, il > 0);
-    int inc = il;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, inc, 31);
-    const int start_q = inc - il;                       // stream position where my interval starts
-    // compacted interval table: lane t holds the t-th non-empty interval's
-    // (start position, slot - position shift); intervals keep their order
-    const unsigned src = __fns(ne, 0, lane + 1);      // lane of the (lane+1)-th set bit
-    const int srcl = src < 32 ? (int)src : 0;
-    const int cstart = __shfl_sync(0xffffffffu, start_q, srcl);
-    const int cshift = __shfl_sync(0xffffffffu, ia - start_q, srcl);
-    const int nint = __popc(ne);
-    int len = 0, nc = 0;
-    uint16_t* row = nbr + (int64_t)s * row_cap;
-    int* crow = bc + (int64_t)s * cand_cap;
-    for (int p0 = 0; p0 < total; p0 += 32) {
-      // interval of each lane: the intervals starting inside this chunk mark
-      // their start position; lane l belongs to the latest start <= p0 + l
-      const int rel = cstart - p0;
-      const bool here = lane < nint && rel >= 0 && rel < 32;
-      const unsigned M = __reduce_or_sync(0xffffffffu, here ? (1u << rel) : 0u);
-      const int before = __popc(__ballot_sync(0xffffffffu, lane < nint && rel < 0));
-      const int q = before + __popc(M & le_mask) - 1;
-      const int p = p0 + lane;
-      const int slot = p + __shfl_sync(0xffffffffu, cshift, q);
-      const bool valid = p < total;
-      const float4 c = cand[valid ? slot : W];   // W: sentinel
-      const float dx = c.x - ri.x, dy = c.y - ri.y, dz = c.z - ri.z;
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      bool in = r2 < R2lo;
-      const bool band = fabsf(r2 - R2mid) <= R2half && !in;
-      if (__any_sync(0xffffffffu, band)) {
-        if (band) {  // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
-          double4 xi = spos[s];
-          double4 xj = spos[cand_j[slot]];
-          int k = cand_k[slot];
-          double ex = __dadd_rn(__dsub_rn(xj.x, xi.x), S.W.shift[k][0]);
-          double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), S.W.shift[k][1]);
-          double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), S.W.shift[k][2]);
-          double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
-          in = d2 <= R2;
-        }
-      }
-      const unsigned mk = __ballot_sync(0xffffffffu, in);
-      const int pp = len + __popc(mk & lt_mask);
-      if (in && pp < row_cap) row[pp] = (uint16_t)slot;
-      len += __popc(mk);
-      if (__any_sync(0xffffffffu, in && r2 <= rcmax)) {  // rare: ~3 bond candidates per row
-        const bool bcand = in && r2 <= S.rcand2[ti * nt + __float_as_int(c.w)];
-        const unsigned mb = __ballot_sync(0xffffffffu, bcand);
-        const int pc = nc + __popc(mb & lt_mask);
-        if (bcand && pc < cand_cap) crow[pc] = cand_j[slot];
-        nc += __popc(mb);
-      }
-    }
+    const int ti = __float_as_int(cand[si].w);
+    int nc;
+    const int len = nbr_row_test<true>(S.W, g, W, cand, sl, spos, s, si, h, rt, nbr + (int64_t)s * row_cap, row_cap,
+                                       bc + (int64_t)s * cand_cap, cand_cap, S.rcand2 + ti * nt, rcmax, nc);
     if (lane == 0) {
       nbr_len[s] = len < row_cap ? len : row_cap;
       bc_len[s] = nc < cand_cap ? nc : cand_cap;
@@ -976,7 +1024,6 @@ constexpr int NB_WARPS = NB_THREADS / 32;
 constexpr int NB_MAX_ROWS = 256;   // rows of one (block, split) work unit that are ranked
 struct NBSmem {
   WinSmem W;
-  double4 shift4[NWU_MAX];      // periodic image shift of each window cell (x, y, z, 0)
   int bad;
   int order[NB_MAX_ROWS];        // row window slots, longest row first
   int rlen[NB_MAX_ROWS];         // their lengths
@@ -1063,8 +1110,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     return;
   }
   const int nwu = c_win.nwu;
-  for (int k = threadIdx.x; k < nwu; k += blockDim.x)
-    S.shift4[k] = make_double4(S.W.shift[k][0], S.W.shift[k][1], S.W.shift[k][2], 0.0);
   // slot info, flattened over slots so that the type loads are all in flight
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
     const int k = cell_of_slot(S.W, nwu, t);
@@ -1163,7 +1208,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     if (pA.c * 32 + lane < pA.len) {
       double dx = xjA.x - xi.x, dy = xjA.y - xi.y, dz = xjA.z - xi.z;
       if (has_shift) {   // block-uniform
-        const double4 sh = S.shift4[infA.y & 255];
+        const double4 sh = S.W.shift[infA.y & 255];
         dx += sh.x;
         dy += sh.y;
         dz += sh.z;

@@ -105,6 +105,19 @@ WindowTables make_tables() {
 }
 
 std::mutex g_tab_mu;
+
+// The dynamic shared memory limit is a per-function (process-wide) attribute:
+// contexts with different window capacities only ever raise it.
+template <typename F>
+cudaError_t ensure_smem(F* func, size_t bytes) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, func);
+  if (e != cudaSuccess) return e;
+  if ((size_t)a.maxDynamicSharedSizeBytes >= bytes) return cudaSuccess;
+  return cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 bool g_tab_done[64] = {false};
 
 cudaError_t ensure_tables() {
@@ -398,7 +411,12 @@ struct reax_ctx {
 
 namespace {
 
-reax_status cuda_err(cudaError_t e) { return e == cudaSuccess ? REAX_OK : REAX_ERR_CUDA; }
+thread_local cudaError_t g_last_cuda = cudaSuccess;   // reax_last_cuda_error()
+reax_status fail_cuda(cudaError_t e) {
+  g_last_cuda = e;
+  return REAX_ERR_CUDA;
+}
+reax_status cuda_err(cudaError_t e) { return e == cudaSuccess ? REAX_OK : fail_cuda(e); }
 
 cudaEvent_t take_event(reax_ctx* c) {
   if (!c->ev_pool.empty()) {
@@ -442,7 +460,14 @@ struct Timer {
   }
 };
 
-#define LAUNCH(ctx) (++(ctx)->launches_cur)
+// REAX_DEBUG=1: report a failing launch (file:line) on stderr (diagnostics only)
+const bool g_debug = getenv("REAX_DEBUG") != nullptr;
+inline void launch_check(const char* file, int line) {
+  if (!g_debug) return;
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) fprintf(stderr, "libreax: launch at %s:%d failed: %s\n", file, line, cudaGetErrorString(e));
+}
+#define LAUNCH(ctx) (++(ctx)->launches_cur, launch_check(__FILE__, __LINE__))
 
 // one-launch scan for the hot path (status cleared by the producing kernel)
 cudaError_t scan1(reax_ctx* c, const int* in, int64_t n, int* out, unsigned long long* status, cudaStream_t s) {
@@ -467,10 +492,10 @@ cudaError_t scan(reax_ctx* c, const TI* in, int64_t n, TO* out, cudaStream_t s) 
 
 reax_status read_status(reax_ctx* c, cudaStream_t s, bool sync) {
   cudaError_t e = cudaMemcpyAsync(c->h_st, c->w.st, sizeof(Status), cudaMemcpyDeviceToHost, s);
-  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  if (e != cudaSuccess) return fail_cuda(e);
   if (!sync) return REAX_OK;
   e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  if (e != cudaSuccess) return fail_cuda(e);
   int f = c->h_st->flags;
   if (f == 0) return REAX_OK;
   if (f & (ST_ROW_OVF | ST_CAND_OVF | ST_BOND_OVF | ST_WIN_OVF)) {
@@ -525,10 +550,10 @@ reax_status upload_params(reax_ctx* c, const reax_params* p, const reax_cutoffs*
   if (c->prm_valid && memcmp(&d, c->h_prm, sizeof(DevParams)) == 0) return REAX_OK;
   // the pinned staging buffer may still be read by an earlier async copy
   cudaError_t e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  if (e != cudaSuccess) return fail_cuda(e);
   memcpy(c->h_prm, &d, sizeof(DevParams));
   e = cudaMemcpyAsync(c->w.prm, c->h_prm, sizeof(DevParams), cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  if (e != cudaSuccess) return fail_cuda(e);
   c->prm_valid = true;
   c->prm_key.swap(key);
   return REAX_OK;
@@ -559,7 +584,7 @@ reax_status check_common(reax_ctx* c, int64_t n, const double box[3], const reax
 }
 
 // a1-a3: binning and the half list (+ bond candidates)
-void launch_lists(reax_ctx* c, int N, const double* pos, const int* type, int nt, cudaStream_t s) {
+void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, int nt, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
   {
@@ -575,6 +600,12 @@ void launch_lists(reax_ctx* c, int N, const double* pos, const int* type, int nt
                                                                w.iperm, w.spos, w.sloc, w.stype);
     LAUNCH(c);
   }
+}
+
+void launch_lists(reax_ctx* c, int N, const double* pos, const int* type, int nt, cudaStream_t s) {
+  const Grid& g = c->g;
+  WS& w = c->w;
+  launch_bin(c, N, pos, type, nt, s);
   {
     Timer t(c, 1, s);
     k_nbr_build<<<g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s>>>(
@@ -639,7 +670,7 @@ reax_status do_build_lists(reax_ctx* c, int64_t n, const double* pos, const int*
     launch_lists(c, N, pos, type, prm->ntypes, s);
     launch_bonds(c, N, s);
   }
-  if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
   note_build(c, pos, type, box);
   r = read_status(c, s, !c->async);
   if (r != REAX_OK) return r;
@@ -653,7 +684,7 @@ reax_status do_bond_orders(reax_ctx* c, const reax_params* prm, const reax_cutof
   reax_status r = upload_params(c, prm, cut, s);
   if (r != REAX_OK) return r;
   if (c->n > 0) launch_bond_correct(c, s);
-  if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
   c->bonds_ok = true;
   return REAX_OK;
 }
@@ -705,11 +736,11 @@ reax_status do_nonbonded(reax_ctx* c, int64_t n, const double* pos, const int* t
   r = upload_params(c, prm, cut, s);
   if (r != REAX_OK) return r;
   if (n == 0) {
-    if (cudaMemsetAsync(energy, 0, 2 * sizeof(double), s) != cudaSuccess) return REAX_ERR_CUDA;
+    if (cudaError_t e_ = cudaMemsetAsync(energy, 0, 2 * sizeof(double), s)) return fail_cuda(e_);
     return REAX_OK;
   }
   launch_nonbonded(c, (int)n, q, force, energy, prm->ntypes, s);
-  if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
   return read_status(c, s, !c->async);
 }
 
@@ -727,22 +758,22 @@ reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, 
   if (N == 0) {
     note_build(c, pos, type, box);
     c->lists_ok = c->bonds_ok = true;
-    if (cudaMemsetAsync(energy, 0, 2 * sizeof(double), s) != cudaSuccess) return REAX_ERR_CUDA;
+    if (cudaError_t e_ = cudaMemsetAsync(energy, 0, 2 * sizeof(double), s)) return fail_cuda(e_);
     return REAX_OK;
   }
-  launch_lists(c, N, pos, type, prm->ntypes, s);
   // REAX_SERIAL=1 (measurement only): everything on `s`, so per-kernel event
   // times are not shared between concurrent kernels
   const bool fork = !c->serial;
   cudaStream_t sb = fork ? c->side : s;
+  launch_lists(c, N, pos, type, prm->ntypes, s);
   if (fork && (cudaEventRecord(c->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(sb, c->ev_fork, 0) != cudaSuccess))
-    return REAX_ERR_CUDA;
+    return fail_cuda(cudaGetLastError());
   launch_bonds(c, N, sb);
   launch_bond_correct(c, sb);
   launch_nonbonded(c, N, q, force, energy, prm->ntypes, s);
   if (fork && (cudaEventRecord(c->ev_join, sb) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join, 0) != cudaSuccess))
-    return REAX_ERR_CUDA;
-  if (cudaGetLastError() != cudaSuccess) return REAX_ERR_CUDA;
+    return fail_cuda(cudaGetLastError());
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
   note_build(c, pos, type, box);
   c->lists_ok = c->bonds_ok = true;
   r = read_status(c, s, !c->async);
@@ -754,6 +785,8 @@ reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, 
 
 // ==================================================================== ABI
 extern "C" {
+
+const char* reax_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda); }
 
 const char* reax_status_str(reax_status s) {
   switch (s) {
@@ -843,10 +876,11 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   size_t s1 = nbr_smem(c.window_cap, c.row_cap) + sizeof(NbrSmem), s2 = nb_smem(c.window_cap) + sizeof(NBSmem);
   if ((size_t)maxsm < s1 || (size_t)maxsm < s2) return REAX_ERR_CAPACITY;
-  if (cudaFuncSetAttribute(k_nbr_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nbr_smem(c.window_cap, c.row_cap)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_nonbonded, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nb_smem(c.window_cap)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_export_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exp_smem(c.window_cap)) != cudaSuccess)
+  if (ensure_smem(k_nbr_build, nbr_smem(c.window_cap, c.row_cap)) != cudaSuccess ||
+      ensure_smem(k_nonbonded, nb_smem(c.window_cap)) != cudaSuccess ||
+      ensure_smem(k_export_pairs, exp_smem(c.window_cap)) != cudaSuccess)
     return REAX_ERR_CUDA;
+
   ctx->ws_base = (char*)ws;
   ctx->ws_bytes = bytes;
   layout(n, g, c, ctx->ws_base, &ctx->w);
@@ -866,7 +900,7 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   if (e == cudaSuccess) e = cudaMemset(ctx->w.ticket, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaMemset(ctx->w.lb_ticket, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) return REAX_ERR_CUDA;
+  if (e != cudaSuccess) return fail_cuda(e);
   ctx->bound = true;
   return REAX_OK;
 }
@@ -925,7 +959,7 @@ reax_status reax_step_host(reax_ctx* ctx, int64_t n, const double* pos, const in
     return REAX_ERR_CUDA;
   if (cudaMemcpyAsync(energy, w.h_energy, sizeof(double) * 2, cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return REAX_ERR_CUDA;
-  if (cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
   return REAX_OK;
 }
 
@@ -953,9 +987,9 @@ reax_status reax_kernel_ms(reax_ctx* ctx, double ms[REAX_NKERNELS], int64_t laun
     for (int k = 0; k < REAX_NKERNELS; ++k) {
       double t = 0.0;
       for (auto& p : ctx->ev_pending[k]) {
-        if (cudaEventSynchronize(p.second) != cudaSuccess) return REAX_ERR_CUDA;
+        if (cudaError_t e_ = cudaEventSynchronize(p.second)) return fail_cuda(e_);
         float f = 0.f;
-        if (cudaEventElapsedTime(&f, p.first, p.second) != cudaSuccess) return REAX_ERR_CUDA;
+        if (cudaError_t e_ = cudaEventElapsedTime(&f, p.first, p.second)) return fail_cuda(e_);
         t += f;
       }
       if (ms) ms[k] = t;
@@ -965,7 +999,7 @@ reax_status reax_kernel_ms(reax_ctx* ctx, double ms[REAX_NKERNELS], int64_t laun
   }
   for (int k = 0; k < REAX_NKERNELS; ++k) {
     for (auto& p : ctx->ev_pending[k]) {
-      if (cudaEventSynchronize(p.second) != cudaSuccess) return REAX_ERR_CUDA;
+      if (cudaError_t e_ = cudaEventSynchronize(p.second)) return fail_cuda(e_);
       float t = 0.f;
       cudaEventElapsedTime(&t, p.first, p.second);
       ctx->ms_acc[k] += t;
@@ -993,7 +1027,8 @@ reax_status reax_selftest_math(reax_ctx* ctx, int64_t n, const double* x, double
   reax_status r = upload_params(ctx, params, cut, s);
   if (r != REAX_OK) return r;
   if (n > 0) k_selftest_math<<<nblk(n, TPB), TPB, 0, s>>>((int)n, x, out, ctx->w.prm);
-  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
   return REAX_OK;
 }
 
@@ -1026,7 +1061,8 @@ reax_status reax_export_pairs(reax_ctx* ctx, int32_t* pi, int32_t* pj, void* str
   k_export_pairs<<<ctx->g.nblock, NBR_THREADS, exp_smem(ctx->cap.window_cap), s>>>(
       ctx->g, ctx->w.cell_start, ctx->w.perm, ctx->w.nbr, ctx->w.nbr_len, ctx->cap.row_cap, ctx->cap.window_cap,
       ctx->w.exp_off, 0, pi, pj, nullptr, nullptr);
-  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
   return REAX_OK;
 }
 
@@ -1042,7 +1078,8 @@ reax_status reax_export_nbr_digest(reax_ctx* ctx, int64_t* cnt, uint64_t* dig, v
   k_export_pairs<<<ctx->g.nblock, NBR_THREADS, exp_smem(ctx->cap.window_cap), s>>>(
       ctx->g, ctx->w.cell_start, ctx->w.perm, ctx->w.nbr, ctx->w.nbr_len, ctx->cap.row_cap, ctx->cap.window_cap,
       nullptr, 1, nullptr, nullptr, (unsigned long long*)cnt, (unsigned long long*)dig);
-  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
   return REAX_OK;
 }
 
@@ -1063,7 +1100,8 @@ reax_status reax_export_bonds(reax_ctx* ctx, int64_t* brow, int32_t* bcol, int32
   if (scan<int, long long>(ctx, w.bc_len, N, w.exp_off, s) != cudaSuccess) return REAX_ERR_CUDA;
   k_export_bonds<<<nblk(N + 1, TPB), TPB, 0, s>>>(N, w.iperm, w.perm, w.brow, w.bcol, w.bmir, w.bo, w.delta,
                                                  w.exp_off, brow, bcol, mirror, bo, delta);
-  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return REAX_ERR_CUDA;
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
   return REAX_OK;
 }
 

@@ -179,3 +179,30 @@ def test_c3_sampled(params):
 @pytest.mark.slow
 def test_c4_sampled(params):
     _sampled(4, params, 24)
+
+
+def test_separate_calls_match_step(params):
+    """reax_build_lists + reax_bond_orders + reax_nonbonded (one stream) and
+    reax_step (bond chain forked onto a side stream beside the nonbonded
+    kernel) give identical lists, bond orders, forces and energies."""
+    import paper_1706_07772_b200 as rx
+    s = gen.make_config(1)
+    dev = torch.device("cuda:0")
+    n = len(s.pos)
+    pos = torch.from_numpy(s.pos).to(dev)
+    typ = torch.from_numpy(s.type).to(dev)
+    q = torch.from_numpy(s.q).to(dev)
+    a = rx.Reax(n, s.box, params, CUT, device=dev)
+    Fa, Ea = a.step(pos, typ, q)
+    b = rx.Reax(n, s.box, params, CUT, device=dev)
+    b.build_lists(pos, typ)
+    b.bond_orders()
+    Fb, Eb = b.nonbonded(pos, typ, q)
+    torch.cuda.synchronize()
+    assert np.array_equal(pair_keys_gpu(a, n), pair_keys_gpu(b, n))
+    ba = [t.cpu().numpy() for t in a.export_bonds()]
+    bb = [t.cpu().numpy() for t in b.export_bonds()]
+    for x, y in zip(ba, bb):
+        assert np.array_equal(x, y)
+    assert np.array_equal(Fa.cpu().numpy(), Fb.cpu().numpy())
+    assert np.array_equal(Ea.cpu().numpy(), Eb.cpu().numpy())
