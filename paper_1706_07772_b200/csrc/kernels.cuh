@@ -6,6 +6,9 @@
 namespace rx {
 
 __constant__ WindowTables c_win;
+#ifdef NB_EXP_PROF
+__device__ unsigned long long g_nbprof[16 * 8192];   // experiments: per-CTA phase timestamps
+#endif
 
 __device__ __forceinline__ void set_flag(Status* st, int f) { atomicOr(&st->flags, f); }
 
@@ -233,8 +236,11 @@ __global__ void k_scatter(int n, const int* __restrict__ cell_of, const int* __r
   perm[cell_start[c] + r] = i;
 }
 
-// Per cell (one warp): order the cell's atoms by original index (rank
-// sort in registers; deterministic), then gather the sorted arrays.
+// sort key of a coordinate: the wrapped value (non-finite -> 0, flagged by k_bin)
+__device__ __forceinline__ double wrap_key(double x, double L) { return isfinite(x) ? wrap_coord(x, L) : 0.0; }
+
+// Per cell (one warp): order the cell's atoms by x (rank sort in registers;
+// deterministic), then gather the sorted arrays.
 __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int* __restrict__ perm,
                               const double* __restrict__ pos, const int* __restrict__ type, Grid g, int nt,
                               int* __restrict__ iperm, double4* __restrict__ spos, float4* __restrict__ sloc,
@@ -243,16 +249,32 @@ __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int
   int lane = threadIdx.x & 31;
   if (c >= ncell) return;
   int a = cell_start[c], b = cell_start[c + 1], m = b - a;
+  // order the cell's atoms by (wrapped x, original index): deterministic, and
+  // every run of cells along x is then x-sorted, which lets the list build
+  // cut each run to the x-window of a row by binary search
   if (m <= 32) {
-    int v = lane < m ? perm[a + lane] : 0x7fffffff;
+    const int v = lane < m ? perm[a + lane] : 0x7fffffff;
+    const double xv = lane < m ? wrap_key(pos[3 * (int64_t)v], g.L[0]) : 0.0;
     int rank = 0;
-    for (int q = 0; q < m; ++q) rank += (__shfl_sync(0xffffffffu, v, q) < v);
+    for (int q = 0; q < m; ++q) {
+      const int vq = __shfl_sync(0xffffffffu, v, q);
+      const double xq = __shfl_sync(0xffffffffu, xv, q);
+      rank += (xq < xv) || (xq == xv && vq < v);
+    }
     __syncwarp();
     if (lane < m) perm[a + rank] = v;
   } else if (lane == 0) {  // rare (Poisson tail): serial insertion sort
     for (int i = a + 1; i < b; ++i) {
-      int v = perm[i], j = i - 1;
-      while (j >= a && perm[j] > v) { perm[j + 1] = perm[j]; --j; }
+      const int v = perm[i];
+      const double xv = wrap_key(pos[3 * (int64_t)v], g.L[0]);
+      int j = i - 1;
+      while (j >= a) {
+        const int u = perm[j];
+        const double xu = wrap_key(pos[3 * (int64_t)u], g.L[0]);
+        if (!(xu > xv || (xu == xv && u > v))) break;
+        perm[j + 1] = u;
+        --j;
+      }
       perm[j + 1] = v;
     }
   }
@@ -459,8 +481,22 @@ __device__ __forceinline__ int nbr_row_test(const WinSmem& W, const Grid& g, int
       const int c0 = max(wxa, (int)floorf((ri.x - w) * rt.ihx));
       const int c1 = min(wxa + (kb - ka), (int)floorf((ri.x + w) * rt.ihx));
       if (c0 <= c1) {
-        ia = W.slot[ka + (c0 - wxa)];
-        il = W.slot[ka + (c1 - wxa) + 1] - ia;
+        // the run's atoms are x-sorted (cells along x, atoms by x within a
+        // cell): cut [ta, tb) to x in [x_i - w, x_i + w] by binary search
+        int lo = W.slot[ka + (c0 - wxa)], hi = W.slot[ka + (c1 - wxa) + 1];
+        const float xlo = ri.x - w, xhi = ri.x + w;
+        int l = lo, u = hi;
+        while (l < u) {
+          const int mid = (l + u) >> 1;
+          if (cand[mid].x < xlo) l = mid + 1; else u = mid;
+        }
+        int l2 = l, u2 = hi;
+        while (l2 < u2) {
+          const int mid = (l2 + u2) >> 1;
+          if (cand[mid].x <= xhi) l2 = mid + 1; else u2 = mid;
+        }
+        ia = l;
+        il = l2 - l;
       }
     }
   } else if (lane == nrun) {
@@ -1025,59 +1061,22 @@ constexpr int NB_MAX_ROWS = 256;   // rows of one (block, split) work unit that 
 struct NBSmem {
   WinSmem W;
   int bad;
+  int rlen0[NB_MAX_ROWS];        // row lengths in home order (ranking input)
   int order[NB_MAX_ROWS];        // row window slots, longest row first
   int rlen[NB_MAX_ROWS];         // their lengths
 };
 
-// Row r (rank order) of this CTA -> window slot and length.
-__device__ __forceinline__ void nb_row(const NBSmem& S, int r, int nsorted, int split, int nsplit,
-                                       const int* __restrict__ nbr_len, int& si, int& len) {
-  if (r < nsorted) {
-    si = S.order[r];
-    len = S.rlen[r];
-  } else {   // beyond the ranked rows (dense blocks): original order
-    int h;
-    row_of(S.W, split + r * nsplit, h, si);
-    const int k = c_win.home_k[h];
-    len = nbr_len[S.W.start[k] + (si - S.W.slot[k])];
-  }
-}
-
-// Warp stream position: the warp's k-th row (snake order over the ranked
-// rows: warp w takes ranks w, 2W-1-w, 2W+w, ... so every warp gets a similar
-// share of long and short rows) and its chunk c of 32 entries.
-struct NbPos {
-  int k, c, si, len;   // len < 0: end of stream
-};
-__device__ __forceinline__ void nb_pos_row(NbPos& p, const NBSmem& S, int nrows, int nsorted, int split, int nsplit,
-                                           const int* __restrict__ nbr_len, int warp) {
-  for (;;) {
-    const int r = p.k * NB_WARPS + ((p.k & 1) ? NB_WARPS - 1 - warp : warp);
-    if (r >= nrows) { p.len = -1; return; }
-    nb_row(S, r, nsorted, split, nsplit, nbr_len, p.si, p.len);
-    if (p.len > 0) return;
-    ++p.k;   // empty row
-  }
-}
-__device__ __forceinline__ void nb_pos_next(NbPos& p, const NBSmem& S, int nrows, int nsorted, int split, int nsplit,
-                                            const int* __restrict__ nbr_len, int warp) {
-  if (p.len < 0) return;
-  if ((p.c + 1) * 32 < p.len) { ++p.c; return; }
-  ++p.k;
-  p.c = 0;
-  nb_pos_row(p, S, nrows, nsorted, split, nsplit, nbr_len, warp);
-}
-
 // One CTA per (home block, split) (Alg. 2, re-designed): a
 // warp streams the half-list entries of its rows 32 at a time (lanes over
-// j), with the next chunk's slot info and positions and the chunk after's
-// row entries in flight while the current chunk is evaluated (across row
-// boundaries).  F_i stays in registers and is warp-reduced once per row;
-// F_j is accumulated in a shared-memory fixed-point window (the block's
-// private force array, the GPU form of the paper's thread-private
-// tprivForce) and flushed to the global int64 sorted force array once per
-// CTA.  Energies: per-lane sums in a fixed pair order, one partial per warp,
-// reduced later in fixed order.  Forces and energies are bitwise reproducible.
+// j), with the next chunk's entries, slot info and positions in flight while
+// the current chunk is evaluated.  Rows are ranked longest first and dealt to
+// the warps in snake order (w, 2W-1-w, 2W+w, ...).  F_i stays in registers
+// and is warp-reduced once per row; F_j is accumulated in a shared-memory
+// fixed-point window (the block's private force array, the GPU form of the
+// paper's thread-private tprivForce) and flushed to the global int64 sorted
+// force array once per CTA.  Energies: per-lane sums in a fixed pair order,
+// one partial per warp, reduced later in fixed order.  Forces and energies
+// are bitwise reproducible.
 __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const int* __restrict__ cell_start,
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
@@ -1085,6 +1084,10 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     double2* __restrict__ epart, int nsplit, Status* st) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
+#ifdef NB_EXP_PROF
+  unsigned long long t_start = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
   const int nt = prm->nt;
   double* ET = reinterpret_cast<double*>(dyn);                  // exp table
@@ -1093,6 +1096,9 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   int2* sinfo = reinterpret_cast<int2*>(pc + nt * nt);          // slot -> {sorted atom, window cell | type << 8}
   unsigned* fa = reinterpret_cast<unsigned*>(sinfo + window_cap);   // F window, low words [3][window_cap]
   int* fb = reinterpret_cast<int*>(fa + 3 * window_cap);            // F window, high words [3][window_cap]
+  unsigned char* kmap = reinterpret_cast<unsigned char*>(fb + 3 * window_cap);   // slot -> window cell
+  const int rb_cap = (row_cap + 7) & ~7;                                          // row buffer entries (16-byte multiple)
+  uint16_t* rbuf = reinterpret_cast<uint16_t*>(((uintptr_t)(kmap + window_cap) + 15) & ~(uintptr_t)15);  // [NB_WARPS][2][rb_cap]
   for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) pc[t] = prm->nb[t];
   for (int t = threadIdx.x; t < EXP_TBL; t += blockDim.x) ET[t] = prm->exp_tbl[t];
   for (int t = threadIdx.x; t < LOG_TBL; t += blockDim.x) LT[t] = make_double2(prm->log_tbl[2 * t], prm->log_tbl[2 * t + 1]);
@@ -1110,160 +1116,167 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     return;
   }
   const int nwu = c_win.nwu;
-  // slot info, flattened over slots so that the type loads are all in flight
-  for (int t = threadIdx.x; t < W; t += blockDim.x) {
-    const int k = cell_of_slot(S.W, nwu, t);
-    const int j = S.W.start[k] + (t - S.W.slot[k]);
-    sinfo[t] = make_int2(j, k | (stype[j] << 8));
-  }
-#ifndef NB_EXP_NOZERO
-  for (int t = threadIdx.x; t < 3 * window_cap; t += blockDim.x) {
-    fa[t] = 0u;
-    fb[t] = 0;
-  }
-#endif
-  // this CTA's rows: split, split + nsplit, ... of the block (home sub-cell
-  // order), ranked longest first (rows are 90-370 pairs)
+  // this CTA's rows: split, split + nsplit, ... of the block (home sub-cell order)
   int nrows_blk = 0;
   for (int h = 0; h < NHOME; ++h)
     if (S.W.home_ok[h]) nrows_blk += S.W.cnt[c_win.home_k[h]];
   const int nrows = nrows_blk > split ? (nrows_blk - split + nsplit - 1) / nsplit : 0;
   const int nsorted = nrows < NB_MAX_ROWS ? nrows : NB_MAX_ROWS;
-  if (threadIdx.x == 0) S.bad = 0;
-  static_assert(NB_MAX_ROWS <= NB_THREADS, "one ranked row per thread");
+  // phase 1 (no global dependence between threads): slot -> cell map, row
+  // lengths, F window zero
+  for (int k = threadIdx.x; k < nwu; k += blockDim.x) {
+    const int b0 = S.W.slot[k], c = S.W.cnt[k];
+    for (int a = 0; a < c; ++a) kmap[b0 + a] = (unsigned char)k;
+  }
   int my_si = 0, my_len = 0;
   if ((int)threadIdx.x < nsorted) {
     int h;
     row_of(S.W, split + threadIdx.x * nsplit, h, my_si);
     const int k = c_win.home_k[h];
     my_len = nbr_len[S.W.start[k] + (my_si - S.W.slot[k])];
-    S.rlen[threadIdx.x] = my_len;
+    S.rlen0[threadIdx.x] = my_len;
   }
+  {
+    uint4* z = reinterpret_cast<uint4*>(fa);          // fa and fb are contiguous: 6 window_cap words
+    for (int t = threadIdx.x; t < (6 * window_cap) / 4; t += blockDim.x) z[t] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (threadIdx.x == 0) S.bad = 0;
   __syncthreads();
+  // phase 2: slot info (flattened over slots: the type loads are independent),
+  // row ranking (longest first; ties by home order)
+#pragma unroll 4
+  for (int t = threadIdx.x; t < W; t += blockDim.x) {
+    const int k = kmap[t];
+    const int j = S.W.start[k] + (t - S.W.slot[k]);
+    sinfo[t] = make_int2(j, k | (stype[j] << 8));
+  }
+  static_assert(NB_MAX_ROWS <= NB_THREADS, "one ranked row per thread");
   if ((int)threadIdx.x < nsorted) {
     int rank = 0;
     for (int t = 0; t < nsorted; ++t) {
-      const int lt = S.rlen[t];
+      const int lt = S.rlen0[t];
       rank += (lt > my_len) || (lt == my_len && t < (int)threadIdx.x);
     }
     S.order[rank] = my_si;
-  }
-  __syncthreads();
-  if ((int)threadIdx.x < nsorted) S.rlen[threadIdx.x] = 0;
-  __syncthreads();
-  if ((int)threadIdx.x < nsorted) {
-    // lengths in rank order (order[] is final now)
-    const int si = S.order[threadIdx.x];
-    S.rlen[threadIdx.x] = nbr_len[sinfo[si].x];
+    S.rlen[rank] = my_len;
   }
   __syncthreads();
   const bool has_shift = S.W.has_shift != 0;
   const double FIXS = c_nb[25], MAGIC = c_nb[26], FLIM = c_nb[27];
   bool bad = false;
   double ev_acc = 0.0, ec_acc = 0.0;
-  // ---- warp stream with a 2-deep software pipeline
-  NbPos pA, pB, pC;
-  pA.k = 0; pA.c = 0;
-  nb_pos_row(pA, S, nrows, nsorted, split, nsplit, nbr_len, warp);
-  pB = pA; nb_pos_next(pB, S, nrows, nsorted, split, nsplit, nbr_len, warp);
-  pC = pB; nb_pos_next(pC, S, nrows, nsorted, split, nsplit, nbr_len, warp);
-  auto row_entry = [&](const NbPos& p) -> int {
-    const int e = p.c * 32 + lane;
-    return (p.len > 0 && e < p.len) ? (int)nbr[(int64_t)sinfo[p.si].x * row_cap + e] : 0;
-  };
-  int slotA = row_entry(pA);
-  int2 infA = sinfo[slotA];
-  double4 xjA = spos[infA.x];
-  int slotB = row_entry(pB);
-  int slotC = row_entry(pC);
-  double4 xi = make_double4(0, 0, 0, 0);
-  const NBPair* pci = pc;
-  double cqi = 0.0;
-  if (pA.len > 0) {
-    const int2 ii = sinfo[pA.si];
-    xi = spos[ii.x];
-    pci = pc + (ii.y >> 8) * nt;
-    cqi = C * xi.w;
-  }
-  double fix = 0.0, fiy = 0.0, fiz = 0.0;
-  while (pA.len > 0) {
-    // issue: B's slot info + positions, D's row entries, B's row atom
-    NbPos pD = pC;
-    nb_pos_next(pD, S, nrows, nsorted, split, nsplit, nbr_len, warp);
-    const int2 infB = sinfo[slotB];
-    const double4 xjB = spos[infB.x];
-#ifndef NB_NO_PREFETCH
-    if (pC.len > 0 && pC.c * 32 + lane < pC.len)   // chunk after next: its positions into L1
-      asm volatile("prefetch.global.L1 [%0];" :: "l"(spos + sinfo[slotC].x));
+#ifdef NB_EXP_PROF
+  unsigned long long t_setup = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_setup));
 #endif
-    const int slotD = row_entry(pD);
-    const bool newrow = pB.len < 0 || pB.k != pA.k;
-    int2 iiB = make_int2(0, 0);
-    double4 xiB = xi;
-    if (newrow && pB.len > 0) {
-      iiB = sinfo[pB.si];
-      xiB = spos[iiB.x];
+  // per-warp double buffer of row entries in shared memory: row k+1 is
+  // copied (cp.async) while row k is evaluated
+  uint16_t* rb = rbuf + warp * 2 * rb_cap;
+  auto row_info = [&](int kr, int& si, int& len) -> bool {
+    const int r = kr * NB_WARPS + ((kr & 1) ? NB_WARPS - 1 - warp : warp);
+    if (r >= nrows) return false;
+    if (r < nsorted) {
+      si = S.order[r];
+      len = S.rlen[r];
+    } else {   // beyond the ranked rows (dense blocks): original order
+      int h;
+      row_of(S.W, split + r * nsplit, h, si);
+      len = nbr_len[sinfo[si].x];
     }
-    // evaluate A
-    if (pA.c * 32 + lane < pA.len) {
-      double dx = xjA.x - xi.x, dy = xjA.y - xi.y, dz = xjA.z - xi.z;
+    return true;
+  };
+  auto row_fetch = [&](int si, int len, uint16_t* dst) {
+    const uint16_t* src = nbr + (int64_t)sinfo[si].x * row_cap;
+    for (int p = lane; p < (len + 7) >> 3; p += 32) {   // 16-byte pieces (rows are 16-byte aligned)
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dst + 8 * p);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + 8 * p));
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  int si_n = 0, len_n = 0;
+  bool have_n = row_info(0, si_n, len_n);
+  if (have_n) row_fetch(si_n, len_n, rb);
+  for (int kr = 0; have_n; ++kr) {
+    const int si = si_n, len = len_n;
+    const uint16_t* row = rb + (kr & 1) * rb_cap;
+    have_n = row_info(kr + 1, si_n, len_n);
+    if (have_n) row_fetch(si_n, len_n, rb + ((kr + 1) & 1) * rb_cap);
+    else asm volatile("cp.async.commit_group;");
+    const int2 ii = sinfo[si];
+    const double4 xi = spos[ii.x];
+    const NBPair* pci = pc + (ii.y >> 8) * nt;
+    const double cqi = C * xi.w;
+    asm volatile("cp.async.wait_group 1;" ::: "memory");   // this row's entries have landed
+    __syncwarp();
+    double fix = 0.0, fiy = 0.0, fiz = 0.0;
+    int slot = lane < len ? (int)row[lane] : si;
+    int2 inf = sinfo[slot];
+    double4 xj = spos[inf.x];
+    for (int e0 = 0; e0 < len; e0 += 32) {
+      const int cslot = slot;
+      const int2 cinf = inf;
+      const double4 cxj = xj;
+      const bool act = e0 + lane < len;
+      if (e0 + 32 < len) {   // next chunk in flight
+        slot = e0 + 32 + lane < len ? (int)row[e0 + 32 + lane] : si;
+        inf = sinfo[slot];
+        xj = spos[inf.x];
+      }
+      double dx = cxj.x - xi.x, dy = cxj.y - xi.y, dz = cxj.z - xi.z;
       if (has_shift) {   // block-uniform
-        const double4 sh = S.W.shift[infA.y & 255];
+        const double4 sh = S.W.shift[cinf.y & 255];
         dx += sh.x;
         dy += sh.y;
         dz += sh.z;
       }
-      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      double ev, ec, gg, dE;
-      nb_pair(r2, cqi * xjA.w, pci[infA.y >> 8], kc, ET, LT, ev, ec, gg, dE);
-      ev_acc += ev;
-      ec_acc += ec;
-      fix = fma(gg, dx, fix);
-      fiy = fma(gg, dy, fiy);
-      fiz = fma(gg, dz, fiz);
-      bad |= !(fabs(dE) < FLIM);
-      const double gs = -gg * FIXS;
-      fix_add(fa + slotA, fb + slotA, fma(gs, dx, MAGIC));
-      fix_add(fa + window_cap + slotA, fb + window_cap + slotA, fma(gs, dy, MAGIC));
-      fix_add(fa + 2 * window_cap + slotA, fb + 2 * window_cap + slotA, fma(gs, dz, MAGIC));
+      if (act) {
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double ev, ec, gg, dE;
+        nb_pair(r2, cqi * cxj.w, pci[cinf.y >> 8], kc, ET, LT, ev, ec, gg, dE);
+        ev_acc += ev;
+        ec_acc += ec;
+        fix = fma(gg, dx, fix);
+        fiy = fma(gg, dy, fiy);
+        fiz = fma(gg, dz, fiz);
+        bad |= !(fabs(dE) < FLIM);
+        const double gs = -gg * FIXS;
+        fix_add(fa + cslot, fb + cslot, fma(gs, dx, MAGIC));
+        fix_add(fa + window_cap + cslot, fb + window_cap + cslot, fma(gs, dy, MAGIC));
+        fix_add(fa + 2 * window_cap + cslot, fb + 2 * window_cap + cslot, fma(gs, dz, MAGIC));
+      }
     }
-    if (newrow) {   // A was the last chunk of its row: F_i
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        fix += __shfl_xor_sync(0xffffffffu, fix, o);
-        fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
-        fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
-      }
-      if (lane == 0) {
-        const int si = pA.si;
-        bad |= !(fabs(fix) < FLIM && fabs(fiy) < FLIM && fabs(fiz) < FLIM);
-        fix_add(fa + si, fb + si, fma(fix, FIXS, MAGIC));
-        fix_add(fa + window_cap + si, fb + window_cap + si, fma(fiy, FIXS, MAGIC));
-        fix_add(fa + 2 * window_cap + si, fb + 2 * window_cap + si, fma(fiz, FIXS, MAGIC));
-      }
-      fix = 0.0; fiy = 0.0; fiz = 0.0;
-      xi = xiB;
-      pci = pc + (iiB.y >> 8) * nt;
-      cqi = C * xi.w;
+    for (int o = 16; o > 0; o >>= 1) {
+      fix += __shfl_xor_sync(0xffffffffu, fix, o);
+      fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
+      fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
     }
-    // rotate
-    pA = pB; pB = pC; pC = pD;
-    slotA = slotB; infA = infB; xjA = xjB;
-    slotB = slotC; slotC = slotD;
+    if (lane == 0) {
+      bad |= !(fabs(fix) < FLIM && fabs(fiy) < FLIM && fabs(fiz) < FLIM);
+      fix_add(fa + si, fb + si, fma(fix, FIXS, MAGIC));
+      fix_add(fa + window_cap + si, fb + window_cap + si, fma(fiy, FIXS, MAGIC));
+      fix_add(fa + 2 * window_cap + si, fb + 2 * window_cap + si, fma(fiz, FIXS, MAGIC));
+    }
+    __syncwarp();   // the buffer of this row is refilled two rows later
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     ev_acc += __shfl_xor_sync(0xffffffffu, ev_acc, o);
     ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
   }
   if (lane == 0) epart[blockIdx.x * NB_WARPS + warp] = make_double2(ev_acc, ec_acc);
+#ifdef NB_EXP_PROF
+  if (lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_nbprof[blockIdx.x * 16 + 4 + warp] = t;
+  }
+#endif
   if (__any_sync(0xffffffffu, bad) && lane == 0) S.bad = 1;
   __syncthreads();
   if (threadIdx.x == 0 && S.bad) set_flag(st, ST_RANGE);
   unsigned long long* gf[3] = {sfx, sfy, sfz};
-#ifdef NB_EXP_NOFLUSH
-  if (W > 0) return;
-#endif
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
     const int j = sinfo[t].x;
 #pragma unroll
@@ -1272,6 +1285,19 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
       if (v != 0) atomicAdd(&gf[c][j], (unsigned long long)v);
     }
   }
+#ifdef NB_EXP_PROF
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_nbprof[blockIdx.x * 16 + 0] = t_start;
+    g_nbprof[blockIdx.x * 16 + 1] = t_setup;
+    g_nbprof[blockIdx.x * 16 + 2] = t;
+    g_nbprof[blockIdx.x * 16 + 3] = sm;
+  }
+#endif
 }
 
 // un-permute: force[i] = F_sorted[iperm[i]] (int64 fixed point -> fp64)

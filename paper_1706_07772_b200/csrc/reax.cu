@@ -300,9 +300,11 @@ void resolve_caps(int64_t n, const double box[3], const reax_cutoffs* cut, const
   int rc = (int)std::ceil(2.0 * mean + 96.0);
   rc = (rc + 31) / 32 * 32;
   c.row_cap = in->row_cap > 0 ? in->row_cap : std::min(rc, 65535);
+  c.row_cap = std::min((c.row_cap + 7) & ~7, 65528);   // 16-byte rows (asynchronous row copies)
   c.cand_cap = in->cand_cap > 0 ? in->cand_cap : 16;
   c.bond_cap = in->bond_cap > 0 ? in->bond_cap : std::max<int64_t>(8 * n, 64);
   c.window_cap = in->window_cap > 0 ? in->window_cap : 2048;
+  c.window_cap = (c.window_cap + 31) & ~31;   // vector zeroing of the shared F window
 }
 
 struct Layout {
@@ -563,8 +565,9 @@ size_t nbr_smem(int wcap, int row_cap = 0) {
   (void)row_cap;
   return (size_t)(wcap + 32) * (sizeof(float4) + sizeof(int) + 1) + 64;
 }
-size_t nb_smem(int wcap, int nt = NT_MAX) {
-  return sizeof(double) * (EXP_TBL + 2 * LOG_TBL) + sizeof(NBPair) * nt * nt + (size_t)wcap * (sizeof(int2) + 6 * sizeof(int)) + 64;
+size_t nb_smem(int wcap, int row_cap, int nt = NT_MAX) {
+  return sizeof(double) * (EXP_TBL + 2 * LOG_TBL) + sizeof(NBPair) * nt * nt + (size_t)wcap * (sizeof(int2) + 6 * sizeof(int) + 1) +
+         16 + (size_t)NB_WARPS * 2 * ((row_cap + 7) & ~7) * sizeof(uint16_t) + 64;
 }
 size_t exp_smem(int wcap) { return (size_t)wcap * sizeof(int) + 64; }
 
@@ -700,7 +703,7 @@ void launch_nonbonded(reax_ctx* c, int N, const double* q, double* force, double
   }
   {
     Timer t(c, 4, s);
-    k_nonbonded<<<g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, nt), s>>>(
+    k_nonbonded<<<g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s>>>(
         g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy,
         w.sfz, w.erow, c->nsplit, w.st);
     LAUNCH(c);
@@ -788,6 +791,12 @@ extern "C" {
 
 const char* reax_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda); }
 
+#ifdef NB_EXP_PROF
+int reax_exp_nbprof(unsigned long long* out, int n) {   // experiments only
+  return cudaMemcpyFromSymbol(out, g_nbprof, sizeof(unsigned long long) * 16 * (size_t)n) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 const char* reax_status_str(reax_status s) {
   switch (s) {
     case REAX_OK: return "ok";
@@ -874,10 +883,10 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  size_t s1 = nbr_smem(c.window_cap, c.row_cap) + sizeof(NbrSmem), s2 = nb_smem(c.window_cap) + sizeof(NBSmem);
+  size_t s1 = nbr_smem(c.window_cap, c.row_cap) + sizeof(NbrSmem), s2 = nb_smem(c.window_cap, c.row_cap) + sizeof(NBSmem);
   if ((size_t)maxsm < s1 || (size_t)maxsm < s2) return REAX_ERR_CAPACITY;
   if (ensure_smem(k_nbr_build, nbr_smem(c.window_cap, c.row_cap)) != cudaSuccess ||
-      ensure_smem(k_nonbonded, nb_smem(c.window_cap)) != cudaSuccess ||
+      ensure_smem(k_nonbonded, nb_smem(c.window_cap, c.row_cap)) != cudaSuccess ||
       ensure_smem(k_export_pairs, exp_smem(c.window_cap)) != cudaSuccess)
     return REAX_ERR_CUDA;
 
