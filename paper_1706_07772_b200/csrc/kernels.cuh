@@ -12,6 +12,13 @@ __device__ unsigned long long g_nbprof[16 * 8192];   // experiments: per-CTA pha
 
 __device__ __forceinline__ void set_flag(Status* st, int f) { atomicOr(&st->flags, f); }
 
+// Programmatic dependent launch (the hot path is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): every such kernel
+// waits for its predecessor's memory before touching global memory; small
+// kernels let their successor launch right away (its blocks then wait here).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // a1: x <- x - L floor(x/L), a result equal to L (or below 0 by rounding) -> 0.
 // Explicitly rounded operations keep it bit-identical to any IEEE scalar code.
 __device__ __forceinline__ double wrap_coord(double x, double L) {
@@ -131,6 +138,8 @@ constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_MASK =
 __global__ void __launch_bounds__(LB_THREADS) k_scan_lookback(const int* __restrict__ in, int n, int* __restrict__ out,
                                                               unsigned long long* __restrict__ status,
                                                               unsigned* __restrict__ ticket) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int tile_id;
   __shared__ long long warp_tot[LB_THREADS / 32];
   __shared__ long long excl_tile;
@@ -205,6 +214,8 @@ __device__ __forceinline__ void clear_status(unsigned long long* status, int nti
 __global__ void k_bin(int n, const double* __restrict__ pos, const int* __restrict__ type, Grid g,
                       int nt, int* __restrict__ cell_of, int* __restrict__ cell_cnt, Status* st,
                       unsigned long long* __restrict__ scan_status, int scan_tiles) {
+  pdl_wait();
+  pdl_trigger();
   clear_status(scan_status, scan_tiles);
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -229,6 +240,8 @@ __global__ void k_bin(int n, const double* __restrict__ pos, const int* __restri
 // counting-sort scatter; cell_cnt returns to zero (ready for the next call)
 __global__ void k_scatter(int n, const int* __restrict__ cell_of, const int* __restrict__ cell_start,
                           int* __restrict__ cell_cnt, int* __restrict__ perm) {
+  pdl_wait();
+  pdl_trigger();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int c = cell_of[i];
@@ -245,6 +258,8 @@ __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int
                               const double* __restrict__ pos, const int* __restrict__ type, Grid g, int nt,
                               int* __restrict__ iperm, double4* __restrict__ spos, float4* __restrict__ sloc,
                               int* __restrict__ stype) {
+  pdl_wait();
+  pdl_trigger();
   int c = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   int lane = threadIdx.x & 31;
   if (c >= ncell) return;
@@ -574,6 +589,7 @@ __global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int*
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
     int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NbrSmem S;
   const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
@@ -694,6 +710,8 @@ __global__ void k_bond_eval(int n, const double4* __restrict__ spos, const int* 
                             const DevParams* __restrict__ prm, int* __restrict__ bc, const int* __restrict__ bc_len,
                             double4* __restrict__ bc_raw, int cand_cap, int* __restrict__ bdeg,
                             unsigned long long* __restrict__ scan_status, int scan_tiles) {
+  pdl_wait();
+  pdl_trigger();
   clear_status(scan_status, scan_tiles);
   __shared__ BOPair sbo[NTP_MAX];
   const int nt = prm->nt;
@@ -749,6 +767,8 @@ __global__ void k_bond_fill(int n, const int* __restrict__ bc, const int* __rest
                             const int* __restrict__ perm, int* __restrict__ bdeg, int* __restrict__ ucol,
                             int* __restrict__ ukey, int* __restrict__ uown, double4* __restrict__ uraw,
                             long long bond_cap, Status* st) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int a0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
   if (blockIdx.x == 0 && threadIdx.x == 0) st->bonds = brow[n];
@@ -788,6 +808,8 @@ __global__ void k_bond_rank(const int* __restrict__ brow, const int* __restrict_
                             const int* __restrict__ uown, const double4* __restrict__ uraw, int* __restrict__ bcol,
                             int* __restrict__ bkey, int* __restrict__ bown, double* __restrict__ bo, long long bond_cap,
                             const Status* __restrict__ st) {
+  pdl_wait();
+  pdl_trigger();
   long long B = st->bonds < bond_cap ? st->bonds : bond_cap;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
     int s = uown[e];
@@ -809,6 +831,8 @@ __global__ void k_bond_rank(const int* __restrict__ brow, const int* __restrict_
 __global__ void k_bond_delta(int n, const int* __restrict__ brow, const int* __restrict__ stype,
                              const DevParams* __restrict__ prm, const double* __restrict__ bo,
                              double2* __restrict__ delta, long long bond_cap) {
+  pdl_wait();
+  pdl_trigger();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   int a = brow[s], b = brow[s + 1];
@@ -827,6 +851,8 @@ __global__ void k_bond_correct(const int* __restrict__ brow, const int* __restri
                                const int* __restrict__ bcol, const int* __restrict__ bkey, const int* __restrict__ bown,
                                int* __restrict__ bmir, double* __restrict__ bo, const double2* __restrict__ delta,
                                long long bond_cap, const Status* __restrict__ st) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ BOPair sbo[NTP_MAX];
   __shared__ double sval[NT_MAX];
   const int nt = prm->nt;
@@ -872,6 +898,8 @@ __global__ void k_bond_correct(const int* __restrict__ brow, const int* __restri
 __global__ void k_nb_prep(int n, const double* __restrict__ q, const int* __restrict__ perm, double4* __restrict__ spos,
                           unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy,
                           unsigned long long* __restrict__ sfz, Status* st) {
+  pdl_wait();
+  pdl_trigger();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   double qs = q[perm[s]];
@@ -1082,6 +1110,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
     unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
     double2* __restrict__ epart, int nsplit, Status* st) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
 #ifdef NB_EXP_PROF
@@ -1304,6 +1333,8 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
 __global__ void k_finalize_forces(int n, const int* __restrict__ iperm, const long long* __restrict__ sfx,
                                   const long long* __restrict__ sfy, const long long* __restrict__ sfz,
                                   double* __restrict__ force, Status* st) {
+  pdl_wait();
+  pdl_trigger();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int s = iperm[i];
@@ -1318,6 +1349,8 @@ constexpr int FIN_THREADS = 512;
 constexpr int FIN_ITEMS = 16;
 __global__ void __launch_bounds__(FIN_THREADS) k_finalize_energy(int n, const double2* __restrict__ erow,
     double* __restrict__ part, unsigned* __restrict__ ticket, double* __restrict__ energy, Status* st) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[2][FIN_THREADS / 32];
   __shared__ bool last;
   double a = 0.0, b = 0.0;

@@ -409,6 +409,7 @@ struct reax_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool serial = getenv("REAX_SERIAL") != nullptr;
+  bool pdl = getenv("REAX_NO_PDL") == nullptr;   // programmatic dependent launch on the hot path
 };
 
 namespace {
@@ -471,10 +472,28 @@ inline void launch_check(const char* file, int line) {
 }
 #define LAUNCH(ctx) (++(ctx)->launches_cur, launch_check(__FILE__, __LINE__))
 
+// Hot-path launches: programmatic dependent launch (each kernel starts with
+// griddepcontrol.wait, so a successor's launch and block scheduling overlap
+// its predecessor's tail; captured as programmatic edges in CUDA graphs)
+template <typename... KArgs, typename... Args>
+void launch_k(reax_ctx* c, void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // one-launch scan for the hot path (status cleared by the producing kernel)
 cudaError_t scan1(reax_ctx* c, const int* in, int64_t n, int* out, unsigned long long* status, cudaStream_t s) {
   if (n <= 0) return cudaMemsetAsync(out, 0, sizeof(int), s);
-  k_scan_lookback<<<nblk(n, LB_TILE), LB_THREADS, 0, s>>>(in, (int)n, out, status, c->w.lb_ticket);
+  launch_k(c, k_scan_lookback, nblk(n, LB_TILE), LB_THREADS, 0, s, in, (int)n, out, status, c->w.lb_ticket);
   LAUNCH(c);
   return cudaGetLastError();
 }
@@ -593,13 +612,13 @@ void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, int nt, 
   {
     Timer t(c, 0, s);
     const int ctiles = nblk(g.ncell, LB_TILE);
-    k_bin<<<nblk(std::max<int64_t>(N, ctiles), TPB), TPB, 0, s>>>(N, pos, type, g, nt, w.cell_of, w.cell_cnt,
+    launch_k(c, k_bin, nblk(std::max<int64_t>(N, ctiles), TPB), TPB, 0, s, N, pos, type, g, nt, w.cell_of, w.cell_cnt,
                                                                  w.st, w.lb_status, ctiles);
     LAUNCH(c);
     scan1(c, w.cell_cnt, g.ncell, w.cell_start, w.lb_status, s);
-    k_scatter<<<nblk(N, TPB), TPB, 0, s>>>(N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
+    launch_k(c, k_scatter, nblk(N, TPB), TPB, 0, s, N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
     LAUNCH(c);
-    k_cell_gather<<<nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s>>>(g.ncell, w.cell_start, w.perm, pos, type, g, nt,
+    launch_k(c, k_cell_gather, nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s, g.ncell, w.cell_start, w.perm, pos, type, g, nt,
                                                                w.iperm, w.spos, w.sloc, w.stype);
     LAUNCH(c);
   }
@@ -611,7 +630,7 @@ void launch_lists(reax_ctx* c, int N, const double* pos, const int* type, int nt
   launch_bin(c, N, pos, type, nt, s);
   {
     Timer t(c, 1, s);
-    k_nbr_build<<<g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s>>>(
+    launch_k(c, k_nbr_build, g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s, 
         g, w.cell_start, w.sloc, w.spos, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, w.bc, w.bc_len,
         c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st);
     LAUNCH(c);
@@ -624,24 +643,24 @@ void launch_bonds(reax_ctx* c, int N, cudaStream_t s) {
   WS& w = c->w;
   Timer t(c, 2, s);
   const int btiles = nblk(N, LB_TILE);
-  k_bond_eval<<<nblk(std::max<int64_t>(N, (int64_t)btiles * 32), TPB), TPB, 0, s>>>(
+  launch_k(c, k_bond_eval, nblk(std::max<int64_t>(N, (int64_t)btiles * 32), TPB), TPB, 0, s, 
       N, w.spos, w.stype, g, w.prm, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.bdeg, w.lb_status, btiles);
   LAUNCH(c);
   scan1(c, w.bdeg, N, w.brow, w.lb_status, s);
-  k_bond_fill<<<nblk(N, TPB), TPB, 0, s>>>(N, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.brow, w.perm, w.bdeg,
+  launch_k(c, k_bond_fill, nblk(N, TPB), TPB, 0, s, N, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.brow, w.perm, w.bdeg,
                                           w.ucol, w.ukey, w.uown, w.uraw, c->cap.bond_cap, w.st);
   LAUNCH(c);
-  k_bond_rank<<<148 * 4, TPB, 0, s>>>(w.brow, w.ucol, w.ukey, w.uown, w.uraw, w.bcol, w.bkey, w.bown, w.bo,
+  launch_k(c, k_bond_rank, 148 * 4, TPB, 0, s, w.brow, w.ucol, w.ukey, w.uown, w.uraw, w.bcol, w.bkey, w.bown, w.bo,
                                      c->cap.bond_cap, w.st);
   LAUNCH(c);
-  k_bond_delta<<<nblk(N, TPB), TPB, 0, s>>>(N, w.brow, w.stype, w.prm, w.bo, w.delta, c->cap.bond_cap);
+  launch_k(c, k_bond_delta, nblk(N, TPB), TPB, 0, s, N, w.brow, w.stype, w.prm, w.bo, w.delta, c->cap.bond_cap);
   LAUNCH(c);
 }
 
 // a6: corrected bond orders
 void launch_bond_correct(reax_ctx* c, cudaStream_t s) {
   Timer t(c, 3, s);
-  k_bond_correct<<<148 * 8, TPB, 0, s>>>(c->w.brow, c->w.perm, c->w.stype, c->w.prm, c->w.bcol, c->w.bkey,
+  launch_k(c, k_bond_correct, 148 * 8, TPB, 0, s, c->w.brow, c->w.perm, c->w.stype, c->w.prm, c->w.bcol, c->w.bkey,
                                          c->w.bown, c->w.bmir, c->w.bo, c->w.delta, c->cap.bond_cap, c->w.st);
   LAUNCH(c);
 }
@@ -698,23 +717,23 @@ void launch_nonbonded(reax_ctx* c, int N, const double* q, double* force, double
   WS& w = c->w;
   {
     Timer t(c, 5, s);
-    k_nb_prep<<<nblk(N, TPB), TPB, 0, s>>>(N, q, w.perm, w.spos, w.sfx, w.sfy, w.sfz, w.st);
+    launch_k(c, k_nb_prep, nblk(N, TPB), TPB, 0, s, N, q, w.perm, w.spos, w.sfx, w.sfy, w.sfz, w.st);
     LAUNCH(c);
   }
   {
     Timer t(c, 4, s);
-    k_nonbonded<<<g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s>>>(
+    launch_k(c, k_nonbonded, g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s, 
         g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy,
         w.sfz, w.erow, c->nsplit, w.st);
     LAUNCH(c);
   }
   {
     Timer t(c, 5, s);
-    k_finalize_forces<<<nblk(N, TPB), TPB, 0, s>>>(N, w.iperm, (const long long*)w.sfx, (const long long*)w.sfy,
+    launch_k(c, k_finalize_forces, nblk(N, TPB), TPB, 0, s, N, w.iperm, (const long long*)w.sfx, (const long long*)w.sfy,
                                                   (const long long*)w.sfz, force, w.st);
     LAUNCH(c);
     const int nparts = g.nblock * c->nsplit * NB_WARPS;   // one energy partial per nonbonded warp
-    k_finalize_energy<<<nblk(nparts, FIN_THREADS * FIN_ITEMS), FIN_THREADS, 0, s>>>(nparts, w.erow, w.epart, w.ticket,
+    launch_k(c, k_finalize_energy, nblk(nparts, FIN_THREADS * FIN_ITEMS), FIN_THREADS, 0, s, nparts, w.erow, w.epart, w.ticket,
                                                                                    energy, w.st);
     LAUNCH(c);
   }
