@@ -309,7 +309,6 @@ def main():
     nb_ms, _ = kms["nonbonded"]
     nb_avg_s = nb_ms / args.steps * 1e-3
     achieved = W_NB_DP_PER_PAIR * P / nb_avg_s
-    fused = kms["nbr"][0] == 0.0     # reax_step ran the fused list + nonbonded kernel
     # list build on its own (the reax_build_lists path: k_nbr_build), timed
     # after the passes above (not part of `value`) for its roofline line
     lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
@@ -332,11 +331,12 @@ def main():
         hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     except Exception:
         hbm_peak = 6650.0   # B200_PROFILING.md fallback
-    traffic = None
-    kname = "k_step_nb" if fused else "k_nonbonded"
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof.get(f"c{args.config}", {}).get(kname, {}).get("dram_bytes_per_launch")
+    traffic = nbr_traffic = dp_exec = None
+    try:   # from the committed ncu capture of this workload (profiles/ncu_summary.json)
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get(f"c{args.config}", {})
+        traffic = prof.get("k_nonbonded", {}).get("dram_bytes_per_launch")
+        nbr_traffic = prof.get("k_nbr_build", {}).get("dram_bytes_per_launch")
+        dp_exec = prof.get("k_nonbonded", {}).get("dp_thread_inst_per_pair")
     except Exception:
         pass
     step_total_ms = sum(v[0] for v in kms.values())
@@ -349,16 +349,21 @@ def main():
                    "parallelism": "replicas" if world > 1 else "single GPU",
                    "launch": "direct launches" if args.no_graph else "CUDA graph replay of reax_step (async mode)"},
         "ns_per_atom_step": 1e9 / value * world if value else None,
-        "roofline": {"bound": "alu", "kernel": "k_step_nb (a3 half list + a7-a8 nonbonded, fused)" if fused else "k_nonbonded (a7)",
+        "roofline": {"bound": "alu", "kernel": "k_nonbonded (a7)",
                      "achieved": achieved / 1e12, "peak": peak_dfma / 1e12,
                      "unit": "T FP64-pipe thread-instructions/s", "frac": achieved / peak_dfma,
                      "traffic": traffic, "work": f"{W_NB_DP_PER_PAIR:.0f} DP inst/pair x {P} pairs per launch",
                      "peak_source": "DFMA probe measured in this run (tools/peak.cu); MEASURED_PEAKS.json has no FP64 entry",
-                     "avg_launch_ms": nb_avg_s * 1e3},
+                     "avg_launch_ms": nb_avg_s * 1e3,
+                     "executed_dp_per_pair": dp_exec,
+                     "fp64_pipe_frac": (dp_exec * P / nb_avg_s / peak_dfma) if dp_exec else None,
+                     "note": "achieved/frac count the formula-minimal work W_nb = 200 FP64 inst/pair (SURVEY.md 8(d)); "
+                             "the kernel executes executed_dp_per_pair (ncu DFMA+DMUL+DADD), fp64_pipe_frac is that rate "
+                             "over the same peak"},
         "roofline_kernels": [
             {"kernel": "k_nbr_build (a3-a4; reax_build_lists path, timed separately)", "bound": "hbm", "achieved": nbr_bytes / nbr_avg_s / 1e9, "peak": hbm_peak,
              "unit": "GB/s", "frac": nbr_bytes / nbr_avg_s / 1e9 / hbm_peak, "avg_launch_ms": nbr_avg_s * 1e3,
-             "bytes_per_launch": nbr_bytes},
+             "bytes_per_launch": nbr_bytes, "traffic": nbr_traffic},
         ],
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kms.items()},
         "timing_pass_ms_per_step": pass2_ms,

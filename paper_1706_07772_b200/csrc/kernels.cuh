@@ -257,7 +257,7 @@ __device__ __forceinline__ double wrap_key(double x, double L) { return isfinite
 __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int* __restrict__ perm,
                               const double* __restrict__ pos, const int* __restrict__ type, Grid g, int nt,
                               int* __restrict__ iperm, double4* __restrict__ spos, float4* __restrict__ sloc,
-                              int* __restrict__ stype) {
+                              int* __restrict__ stype, const double* __restrict__ qin, Status* st) {
   pdl_wait();
   pdl_trigger();
   int c = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -308,7 +308,12 @@ __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int
     }
     int t = type[i];
     t = (t < 0 || t >= nt) ? 0 : t;  // flagged by k_bin; clamp keeps every table index valid
-    spos[s] = make_double4(w[0], w[1], w[2], 0.0);
+    double qs = 0.0;
+    if (qin) {   // reax_step: charges gathered here (reax_nonbonded does it in k_nb_prep)
+      qs = qin[i];
+      if (!isfinite(qs)) set_flag(st, ST_NONFINITE_IN);
+    }
+    spos[s] = make_double4(w[0], w[1], w[2], qs);
     sloc[s] = make_float4(l[0], l[1], l[2], __int_as_float(t));
     stype[s] = t;
     iperm[i] = s;
@@ -416,13 +421,11 @@ __device__ __forceinline__ int warp_find(int incl, int t) {
 
 // ========================================================= a3-a4 list build
 constexpr int NBR_THREADS = 256;
-constexpr int MAX_BLOCK_ROWS = 1024;
 
 struct NbrSmem {
   WinSmem W;
   float rcand2[NTP_MAX];
-  int rowtab[MAX_BLOCK_ROWS];   // row r of the block -> (window slot << 3) | home sub-cell
-  int nrows;
+  int gbase[NHOME + 1];   // first row group of each home sub-cell (groups of NBR_G rows)
   int next_row;
 };
 
@@ -581,11 +584,181 @@ __device__ __forceinline__ int nbr_row_test(const WinSmem& W, const Grid& g, int
   return len;
 }
 
+// A group of up to NBR_G consecutive rows (atoms) of one home sub-cell,
+// tested by one warp (Write Lists).  The atoms of a cell are
+// x-sorted, so the rows of a group are x-neighbours and share one candidate
+// stream: the forward runs of the sub-cell's half stencil, each cut to the
+// cells meeting [x_min - w, x_max + w] and then, the run being x-sorted, to
+// that x-window by binary search (w = sqrt(R^2 - d_yz^2), d_yz the smallest
+// distance of the group's atoms to the run's y-z cross-section, so no partner
+// is ever cut), then the own cell after the group's first row.  Each lane
+// loads one candidate (32 per step) and tests it against every row of the
+// group held in registers: the candidate's load and stream bookkeeping are
+// shared by the rows.  r^2 in fp32 against a band of +-m around R^2 (~70x the
+// fp32 error bound), the band settled by the exact FMA-free fp64 test (bit-
+// identical to the oracle's r^2); accepted window slots of row r are compacted
+// with one ballot per row and stored coalesced; with BOND, candidates below the
+// conservative BO' = bo_cut radius likewise.  len[r] may exceed row_cap (the
+// caller flags it).
+constexpr int NBR_G = 4;
+template <bool BOND, typename SI>
+__device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, const float4* __restrict__ cand, SI sl,
+                                               const double4* __restrict__ spos, int si0, int nrow, int h,
+                                               const Grid& g, const RowTest& rt, uint16_t* __restrict__ nbr,
+                                               int row_cap, int* __restrict__ bc, int cand_cap,
+                                               const float* __restrict__ rc2, int nt, float rcmax,
+                                               int (&len)[NBR_G], int (&nc)[NBR_G]) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u, le_mask = lt_mask | (1u << lane);
+  float4 ri[NBR_G];
+  int sr[NBR_G];
+  uint16_t* rowp[NBR_G];
+  int* crowp[NBR_G];
+#pragma unroll
+  for (int r = 0; r < NBR_G; ++r) {
+    const int q = si0 + (r < nrow ? r : 0);
+    ri[r] = cand[q];
+    sr[r] = sl.J(q);
+    rowp[r] = nbr + (int64_t)sr[r] * row_cap;
+    crowp[r] = BOND ? bc + (int64_t)sr[r] * cand_cap : nullptr;
+    len[r] = 0;
+    nc[r] = 0;
+  }
+  const int kh = c_win.home_k[h];
+  const int ownlo = W.slot[kh];
+  float xmin = ri[0].x, xmax = ri[0].x;
+#pragma unroll
+  for (int r = 1; r < NBR_G; ++r)
+    if (r < nrow) { xmin = fminf(xmin, ri[r].x); xmax = fmaxf(xmax, ri[r].x); }
+  // ---- intervals: lane q < nrun cuts run q, lane nrun takes the own cell
+  const int nrun = c_win.nrun1[h];
+  int ia = 0, il = 0;
+  if (lane < nrun) {
+    const int ka = c_win.run1_a[h][lane], kb = c_win.run1_b[h][lane];
+    const int wba = c_win.wu[ka];
+    const int wxa = wba % WB - SR;                   // x cell offset (block frame) of the run's first cell
+    const float oy = (float)((wba / WB % WB - SR) * g.h[1]);
+    const float oz = (float)((wba / (WB * WB) - SR) * g.h[2]);
+    float d2min = 1e30f;
+#pragma unroll
+    for (int r = 0; r < NBR_G; ++r) {
+      if (r < nrow) {
+        const float dy = fmaxf(0.f, fmaxf(oy - ri[r].y, ri[r].y - (oy + rt.hy)));
+        const float dz = fmaxf(0.f, fmaxf(oz - ri[r].z, ri[r].z - (oz + rt.hz)));
+        d2min = fminf(d2min, dy * dy + dz * dz);
+      }
+    }
+    const float w2 = rt.Rt * rt.Rt - d2min;
+    if (w2 >= 0.f) {
+      const float w = sqrtf(w2) + 1e-3f;
+      const int c0 = max(wxa, (int)floorf((xmin - w) * rt.ihx));
+      const int c1 = min(wxa + (kb - ka), (int)floorf((xmax + w) * rt.ihx));
+      if (c0 <= c1) {
+        int lo = W.slot[ka + (c0 - wxa)], hi = W.slot[ka + (c1 - wxa) + 1];
+        const float xlo = xmin - w, xhi = xmax + w;
+        int l = lo, u = hi;
+        while (l < u) {
+          const int mid = (l + u) >> 1;
+          if (cand[mid].x < xlo) l = mid + 1; else u = mid;
+        }
+        int l2 = l, u2 = hi;
+        while (l2 < u2) {
+          const int mid = (l2 + u2) >> 1;
+          if (cand[mid].x <= xhi) l2 = mid + 1; else u2 = mid;
+        }
+        ia = l;
+        il = l2 - l;
+      }
+    }
+  } else if (lane == nrun) {
+    ia = si0 + 1;
+    il = W.slot[kh + 1] - ia;
+  }
+  // compact the non-empty intervals, then exclusive offsets
+  const unsigned ne = __ballot_sync(0xffffffffu, il > 0);
+  int inc = il;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, inc, 31);
+  const int start_q = inc - il;
+  const unsigned src = __fns(ne, 0, lane + 1);      // lane of the (lane+1)-th set bit
+  const int srcl = src < 32 ? (int)src : 0;
+  const int cstart = __shfl_sync(0xffffffffu, start_q, srcl);
+  const int cshift = __shfl_sync(0xffffffffu, ia - start_q, srcl);
+  const int nint = __popc(ne);
+  for (int p0 = 0; p0 < total; p0 += 32) {
+    const int rel = cstart - p0;
+    const bool here = lane < nint && rel >= 0 && rel < 32;
+    const unsigned M = __reduce_or_sync(0xffffffffu, here ? (1u << rel) : 0u);
+    const int before = __popc(__ballot_sync(0xffffffffu, lane < nint && rel < 0));
+    const int q = before + __popc(M & le_mask) - 1;
+    const int p = p0 + lane;
+    const int slot = p + __shfl_sync(0xffffffffu, cshift, q);
+    const bool valid = p < total;
+    const float4 c = cand[valid ? slot : Wslots];   // Wslots: sentinel
+    const unsigned tself = (unsigned)(slot - ownlo);
+    // all rows first (independent chains), then the rare band / bond paths
+    float r2v[NBR_G];
+    bool in[NBR_G], band[NBR_G];
+    bool anyband = false, anybond = false;
+#pragma unroll
+    for (int r = 0; r < NBR_G; ++r) {
+      const float dx = c.x - ri[r].x, dy = c.y - ri[r].y, dz = c.z - ri[r].z;
+      r2v[r] = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      const bool ok = r < nrow && tself > (unsigned)(si0 + r - ownlo);   // own-cell partners after row r only
+      in[r] = ok && r2v[r] < rt.R2lo;
+      band[r] = ok && !in[r] && fabsf(r2v[r] - rt.R2mid) <= rt.R2half;
+      anyband |= band[r];
+    }
+    if (__any_sync(0xffffffffu, anyband)) {
+#pragma unroll
+      for (int r = 0; r < NBR_G; ++r) {
+        if (band[r]) {  // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
+          const double4 xi = spos[sr[r]];
+          const double4 xj = spos[sl.J(slot)];
+          const double4 sh = W.shift[sl.K(slot)];
+          const double ex = __dadd_rn(__dsub_rn(xj.x, xi.x), sh.x);
+          const double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), sh.y);
+          const double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), sh.z);
+          const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+          in[r] = d2 <= rt.R2;
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NBR_G; ++r) {
+      const unsigned mk = __ballot_sync(0xffffffffu, in[r]);
+      const int pp = len[r] + __popc(mk & lt_mask);
+      if (in[r] && pp < row_cap) rowp[r][pp] = (uint16_t)slot;
+      len[r] += __popc(mk);
+      anybond |= in[r] && r2v[r] <= rcmax;
+    }
+    if (BOND) {
+      if (__any_sync(0xffffffffu, anybond)) {  // ~3 bond candidates per row
+        const int tj = __float_as_int(c.w);
+#pragma unroll
+        for (int r = 0; r < NBR_G; ++r) {
+          const bool bcand = in[r] && r2v[r] <= rc2[__float_as_int(ri[r].w) * nt + tj];
+          const unsigned mb = __ballot_sync(0xffffffffu, bcand);
+          const int pc = nc[r] + __popc(mb & lt_mask);
+          if (bcand && pc < cand_cap) crowp[r][pc] = sl.J(slot);
+          nc[r] += __popc(mb);
+        }
+      }
+    }
+  }
+}
+
 // One CTA per (home block, split).  Candidates of the window are staged in
 // shared memory as fp32 coordinates relative to the block origin.  A warp
 // takes one row (atom) at a time and runs nbr_row_test on it (with bond
 // candidates).
-__global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int* __restrict__ cell_start,
+#ifndef NBR_MINB
+#define NBR_MINB 3
+#endif
+__global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, const int* __restrict__ cell_start,
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
     int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st) {
@@ -603,19 +776,16 @@ __global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int*
   int W = build_window(S.W, blk, g, cell_start);
   const int nwu = c_win.nwu;
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {   // row table of the block (rows in home sub-cell order)
-    int r = 0;
+  if (threadIdx.x == 0) {   // row groups of the block (home sub-cell order)
+    int gb = 0;
     for (int h = 0; h < NHOME; ++h) {
-      if (!S.W.home_ok[h]) continue;
-      const int kk = c_win.home_k[h], a = S.W.slot[kk], c = S.W.cnt[kk];
-      for (int q = 0; q < c; ++q, ++r)
-        if (r < MAX_BLOCK_ROWS) S.rowtab[r] = ((a + q) << 3) | h;
+      S.gbase[h] = gb;
+      if (S.W.home_ok[h]) gb += (S.W.cnt[c_win.home_k[h]] + NBR_G - 1) / NBR_G;
     }
-    S.nrows = r;
+    S.gbase[NHOME] = gb;
     S.next_row = 0;
   }
   __syncthreads();
-  const int nrows = S.nrows;
   if (W > window_cap) {
     if (threadIdx.x == 0) {
       set_flag(st, ST_WIN_OVF);
@@ -655,30 +825,34 @@ __global__ void __launch_bounds__(NBR_THREADS, 3) k_nbr_build(Grid g, const int*
   if (threadIdx.x < 32) cand[W + threadIdx.x] = make_float4(1e30f, 1e30f, 1e30f, 0.f);  // sentinel
   __syncthreads();
   const SlotJK sl{cand_j, cand_k};
+  // groups of NBR_G consecutive rows of one home sub-cell; this CTA takes
+  // groups split, split + nsplit, ...
+  const int ngroups = S.gbase[NHOME];
   for (;;) {
     int m = 0;
     if (lane == 0) m = atomicAdd(&S.next_row, 1);
     m = __shfl_sync(0xffffffffu, m, 0);
-    const int r = split + m * nsplit;
-    if (r >= nrows) break;
-    int h, si;
-    if (r < MAX_BLOCK_ROWS) {
-      const int rtb = S.rowtab[r];
-      h = rtb & 7;
-      si = rtb >> 3;
-    } else {   // pathological density: beyond the table
-      row_of(S.W, r, h, si);
-    }
-    const int s = cand_j[si];
-    const int ti = __float_as_int(cand[si].w);
-    int nc;
-    const int len = nbr_row_test<true>(S.W, g, W, cand, sl, spos, s, si, h, rt, nbr + (int64_t)s * row_cap, row_cap,
-                                       bc + (int64_t)s * cand_cap, cand_cap, S.rcand2 + ti * nt, rcmax, nc);
-    if (lane == 0) {
-      nbr_len[s] = len < row_cap ? len : row_cap;
-      bc_len[s] = nc < cand_cap ? nc : cand_cap;
-      if (len > row_cap) { set_flag(st, ST_ROW_OVF); atomicMax(&st->max_row, len); }
-      if (nc > cand_cap) { set_flag(st, ST_CAND_OVF); atomicMax(&st->max_cand, nc); }
+    const int G = split + m * nsplit;
+    if (G >= ngroups) break;
+    int h = 0;
+    while (S.gbase[h + 1] <= G) ++h;
+    const int kh = c_win.home_k[h];
+    const int a0 = (G - S.gbase[h]) * NBR_G;
+    const int nrow = min(NBR_G, S.W.cnt[kh] - a0);
+    const int si0 = S.W.slot[kh] + a0;
+    int len[NBR_G], nc[NBR_G];
+    nbr_group_test<true>(S.W, W, cand, sl, spos, si0, nrow, h, g, rt, nbr, row_cap, bc, cand_cap, S.rcand2, nt, rcmax,
+                         len, nc);
+    if (lane < nrow) {
+      int l = len[0], c = nc[0];
+#pragma unroll
+      for (int r = 1; r < NBR_G; ++r)
+        if (lane == r) { l = len[r]; c = nc[r]; }
+      const int s = cand_j[si0 + lane];
+      nbr_len[s] = l < row_cap ? l : row_cap;
+      bc_len[s] = c < cand_cap ? c : cand_cap;
+      if (l > row_cap) { set_flag(st, ST_ROW_OVF); atomicMax(&st->max_row, l); }
+      if (c > cand_cap) { set_flag(st, ST_CAND_OVF); atomicMax(&st->max_cand, c); }
     }
   }
 }
@@ -1329,37 +1503,41 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
 #endif
 }
 
-// un-permute: force[i] = F_sorted[iperm[i]] (int64 fixed point -> fp64)
-__global__ void k_finalize_forces(int n, const int* __restrict__ iperm, const long long* __restrict__ sfx,
-                                  const long long* __restrict__ sfy, const long long* __restrict__ sfz,
-                                  double* __restrict__ force, Status* st) {
+// a8 finalize, one kernel: un-permute the forces, force[i] = F_sorted[iperm[i]]
+// (int64 fixed point -> fp64), and reset the accumulators to zero for the
+// next step; and the energy: block b sums a fixed slice of the nonbonded
+// partials, the last block to finish sums the block partials in block order
+// (deterministic).
+constexpr int FIN_THREADS = 256;
+__global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __restrict__ iperm,
+    unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
+    double* __restrict__ force, int nparts, const double2* __restrict__ epart, double* __restrict__ part,
+    unsigned* __restrict__ ticket, double* __restrict__ energy, Status* st) {
   pdl_wait();
   pdl_trigger();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int s = iperm[i];
-  const double sc = 0x1.0p-35;
-  static_assert(FIX_BITS == 35, "scale");
-  force[3 * (int64_t)i] = (double)sfx[s] * sc;
-  force[3 * (int64_t)i + 1] = (double)sfy[s] * sc;
-  force[3 * (int64_t)i + 2] = (double)sfz[s] * sc;
-}
-
-constexpr int FIN_THREADS = 512;
-constexpr int FIN_ITEMS = 16;
-__global__ void __launch_bounds__(FIN_THREADS) k_finalize_energy(int n, const double2* __restrict__ erow,
-    double* __restrict__ part, unsigned* __restrict__ ticket, double* __restrict__ energy, Status* st) {
-  pdl_wait();
-  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int s = iperm[i];
+    const double sc = 0x1.0p-35;
+    static_assert(FIX_BITS == 35, "scale");
+    force[3 * (int64_t)i] = (double)(long long)sfx[s] * sc;
+    force[3 * (int64_t)i + 1] = (double)(long long)sfy[s] * sc;
+    force[3 * (int64_t)i + 2] = (double)(long long)sfz[s] * sc;
+    sfx[s] = 0ull;
+    sfy[s] = 0ull;
+    sfz[s] = 0ull;
+  }
   __shared__ double red[2][FIN_THREADS / 32];
   __shared__ bool last;
+  const int per = (nparts + gridDim.x - 1) / gridDim.x;
+  const int p0 = blockIdx.x * per, p1 = min(nparts, p0 + per);
   double a = 0.0, b = 0.0;
-  int64_t base = (int64_t)blockIdx.x * FIN_THREADS * FIN_ITEMS;
-  for (int q = 0; q < FIN_ITEMS; ++q) {
-    int64_t i = base + (int64_t)q * FIN_THREADS + threadIdx.x;
-    if (i < n) { double2 v = erow[i]; a += v.x; b += v.y; }
+  for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    const double2 v = epart[p];
+    a += v.x;
+    b += v.y;
   }
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, o);

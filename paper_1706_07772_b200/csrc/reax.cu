@@ -348,7 +348,7 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
   t.sfy = (unsigned long long*)take(sizeof(long long) * N);
   t.sfz = (unsigned long long*)take(sizeof(long long) * N);
   t.erow = (double2*)take(sizeof(double2) * std::max<size_t>(N, (size_t)g.nblock * MAX_SPLIT * NB_WARPS));
-  t.epart = (double*)take(sizeof(double) * 2 * ((size_t)nblk((int64_t)std::max<size_t>(N, (size_t)g.nblock * MAX_SPLIT * NB_WARPS), FIN_THREADS * FIN_ITEMS) + 1));
+  t.epart = (double*)take(sizeof(double) * 2 * ((size_t)nblk((int64_t)std::max<int64_t>(N, 1), FIN_THREADS) + 1));   // k_finalize block partials
   t.ticket = (unsigned*)take(sizeof(unsigned) * 4);
   t.ucol = (int*)take(sizeof(int) * (size_t)c.bond_cap);
   t.ukey = (int*)take(sizeof(int) * (size_t)c.bond_cap);
@@ -606,7 +606,7 @@ reax_status check_common(reax_ctx* c, int64_t n, const double box[3], const reax
 }
 
 // a1-a3: binning and the half list (+ bond candidates)
-void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, int nt, cudaStream_t s) {
+void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, const double* q, int nt, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
   {
@@ -619,15 +619,15 @@ void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, int nt, 
     launch_k(c, k_scatter, nblk(N, TPB), TPB, 0, s, N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
     LAUNCH(c);
     launch_k(c, k_cell_gather, nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s, g.ncell, w.cell_start, w.perm, pos, type, g, nt,
-                                                               w.iperm, w.spos, w.sloc, w.stype);
+                                                               w.iperm, w.spos, w.sloc, w.stype, q, w.st);
     LAUNCH(c);
   }
 }
 
-void launch_lists(reax_ctx* c, int N, const double* pos, const int* type, int nt, cudaStream_t s) {
+void launch_lists(reax_ctx* c, int N, const double* pos, const int* type, const double* q, int nt, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
-  launch_bin(c, N, pos, type, nt, s);
+  launch_bin(c, N, pos, type, q, nt, s);
   {
     Timer t(c, 1, s);
     launch_k(c, k_nbr_build, g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s, 
@@ -689,7 +689,7 @@ reax_status do_build_lists(reax_ctx* c, int64_t n, const double* pos, const int*
   if (r != REAX_OK) return r;
   int N = (int)n;
   if (N > 0) {
-    launch_lists(c, N, pos, type, prm->ntypes, s);
+    launch_lists(c, N, pos, type, nullptr, prm->ntypes, s);
     launch_bonds(c, N, s);
   }
   if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
@@ -712,10 +712,11 @@ reax_status do_bond_orders(reax_ctx* c, const reax_params* prm, const reax_cutof
 }
 
 // a7-a8: nonbonded energies and forces (reads the half list, spos, stype, perm/iperm)
+// q == nullptr: the charges were gathered by k_cell_gather (reax_step)
 void launch_nonbonded(reax_ctx* c, int N, const double* q, double* force, double* energy, int nt, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
-  {
+  if (q) {
     Timer t(c, 5, s);
     launch_k(c, k_nb_prep, nblk(N, TPB), TPB, 0, s, N, q, w.perm, w.spos, w.sfx, w.sfy, w.sfz, w.st);
     LAUNCH(c);
@@ -729,12 +730,9 @@ void launch_nonbonded(reax_ctx* c, int N, const double* q, double* force, double
   }
   {
     Timer t(c, 5, s);
-    launch_k(c, k_finalize_forces, nblk(N, TPB), TPB, 0, s, N, w.iperm, (const long long*)w.sfx, (const long long*)w.sfy,
-                                                  (const long long*)w.sfz, force, w.st);
-    LAUNCH(c);
     const int nparts = g.nblock * c->nsplit * NB_WARPS;   // one energy partial per nonbonded warp
-    launch_k(c, k_finalize_energy, nblk(nparts, FIN_THREADS * FIN_ITEMS), FIN_THREADS, 0, s, nparts, w.erow, w.epart, w.ticket,
-                                                                                   energy, w.st);
+    launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.iperm, w.sfx, w.sfy, w.sfz, force, nparts,
+             w.erow, w.epart, w.ticket, energy, w.st);
     LAUNCH(c);
   }
 }
@@ -787,12 +785,12 @@ reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, 
   // times are not shared between concurrent kernels
   const bool fork = !c->serial;
   cudaStream_t sb = fork ? c->side : s;
-  launch_lists(c, N, pos, type, prm->ntypes, s);
+  launch_lists(c, N, pos, type, q, prm->ntypes, s);   // charges gathered with the positions
   if (fork && (cudaEventRecord(c->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(sb, c->ev_fork, 0) != cudaSuccess))
     return fail_cuda(cudaGetLastError());
   launch_bonds(c, N, sb);
   launch_bond_correct(c, sb);
-  launch_nonbonded(c, N, q, force, energy, prm->ntypes, s);
+  launch_nonbonded(c, N, nullptr, force, energy, prm->ntypes, s);
   if (fork && (cudaEventRecord(c->ev_join, sb) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join, 0) != cudaSuccess))
     return fail_cuda(cudaGetLastError());
   if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
@@ -925,6 +923,10 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   cudaError_t e = cudaMemset(ctx->w.cell_cnt, 0, sizeof(int) * (g.ncell + 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.bdeg, 0, sizeof(int) * (std::max<int64_t>(n, 1) + 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.st, 0, sizeof(Status));
+  // fixed-point force accumulators: zero between steps (k_finalize resets them)
+  if (e == cudaSuccess) e = cudaMemset(ctx->w.sfx, 0, sizeof(long long) * std::max<int64_t>(n, 1));
+  if (e == cudaSuccess) e = cudaMemset(ctx->w.sfy, 0, sizeof(long long) * std::max<int64_t>(n, 1));
+  if (e == cudaSuccess) e = cudaMemset(ctx->w.sfz, 0, sizeof(long long) * std::max<int64_t>(n, 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.ticket, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaMemset(ctx->w.lb_ticket, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();

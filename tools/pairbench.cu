@@ -48,6 +48,75 @@ __global__ void __launch_bounds__(256, MINB) k_pairbench(const DevParams* __rest
   if (acc + fx == 12345.678 || fa[threadIdx.x] == 7u) out[blockIdx.x] = acc;
 }
 
+// P2: the k_nonbonded loop structure without global memory: rows of 150-260
+// entries walked 32 at a time (lanes over entries, last chunk partial), xj
+// and slot info from shared memory, F_i warp-reduced per row, F_j into the
+// fixed-point window.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_rowbench(const DevParams* __restrict__ prm, double* out, int rows_per_warp) {
+  __shared__ double ET[EXP_TBL];
+  __shared__ double2 LT[LOG_TBL];
+  __shared__ NBPair pc[16];
+  __shared__ unsigned fa[3 * 1024];
+  __shared__ int fb[3 * 1024];
+  __shared__ double4 xs[512];
+  for (int t = threadIdx.x; t < EXP_TBL; t += blockDim.x) ET[t] = prm->exp_tbl[t];
+  for (int t = threadIdx.x; t < LOG_TBL; t += blockDim.x) LT[t] = make_double2(prm->log_tbl[2 * t], prm->log_tbl[2 * t + 1]);
+  for (int t = threadIdx.x; t < 16; t += blockDim.x) pc[t] = prm->nb[t];
+  for (int t = threadIdx.x; t < 3 * 1024; t += blockDim.x) { fa[t] = 0; fb[t] = 0; }
+  for (int t = threadIdx.x; t < 512; t += blockDim.x) {
+    unsigned h = t * 2654435761u;
+    xs[t] = make_double4(((h >> 8) & 1023) * 0.02, ((h >> 18) & 1023) * 0.02, (t & 511) * 0.04, 0.3);
+  }
+  __syncthreads();
+  NBConst kc;
+  kc.invR = prm->invR; kc.phalf = 0.5 * prm->p_vdw; kc.inv_p = prm->inv_p; kc.m140invR = -140.0 * prm->invR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double FIXS = c_nb[25], MAGIC = c_nb[26];
+  double ev_acc = 0.0, ec_acc = 0.0;
+  for (int k = 0; k < rows_per_warp; ++k) {
+    const int si = (warp * 97 + k * 31) & 1023;
+    const int len = 150 + ((k * 37 + warp * 11) % 110);
+    const double4 xi = xs[si & 511];
+    const NBPair* pci = pc + (k & 3) * 4;
+    const double cqi = 332.0 * xi.w;
+    double fix = 0.0, fiy = 0.0, fiz = 0.0;
+    for (int e0 = 0; e0 < len; e0 += 32) {
+      const int e = e0 + lane;
+      if (e < len) {
+        const int slot = (si + 1 + e * 3) & 1023;
+        const double4 xj = xs[slot & 511];
+        const double dx = xj.x - xi.x + 3.0, dy = xj.y - xi.y, dz = xj.z - xi.z;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double ev, ec, gg, dE;
+        nb_pair(r2, cqi * xj.w, pci[slot & 3], kc, ET, LT, ev, ec, gg, dE);
+        ev_acc += ev;
+        ec_acc += ec;
+        fix = fma(gg, dx, fix);
+        fiy = fma(gg, dy, fiy);
+        fiz = fma(gg, dz, fiz);
+        const double gs = -gg * FIXS;
+        fix_add(fa + slot, fb + slot, fma(gs, dx, MAGIC));
+        fix_add(fa + 1024 + slot, fb + 1024 + slot, fma(gs, dy, MAGIC));
+        fix_add(fa + 2048 + slot, fb + 2048 + slot, fma(gs, dz, MAGIC));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      fix += __shfl_xor_sync(0xffffffffu, fix, o);
+      fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
+      fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
+    }
+    if (lane == 0) {
+      fix_add(fa + si, fb + si, fma(fix, FIXS, MAGIC));
+      fix_add(fa + 1024 + si, fb + 1024 + si, fma(fiy, FIXS, MAGIC));
+      fix_add(fa + 2048 + si, fb + 2048 + si, fma(fiz, FIXS, MAGIC));
+    }
+  }
+  __syncthreads();
+  if (ev_acc + ec_acc == 12345.678 || fa[threadIdx.x] == 7u) out[blockIdx.x] = ev_acc;
+}
+
 int main() {
   cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0));
   const int sms = p.multiProcessorCount;
@@ -75,6 +144,14 @@ int main() {
     printf("%-28s regs %3d ctas %5d: %.3f ms  %.2f Gpairs/s  (6.63M pairs -> %.1f us)\n", name, fa.numRegs, ctas, ms,
            pairs / ms / 1e6, 6.633e6 / (pairs / ms / 1e3) * 1e6);
   };
+  for (int per : {2, 4}) {
+    const int rpw = 60, ctas = sms * per;
+    k_rowbench<2><<<ctas, 256>>>(d, o, 2);
+    cudaEventRecord(a); k_rowbench<2><<<ctas, 256>>>(d, o, rpw); cudaEventRecord(b);
+    CK(cudaEventSynchronize(b)); float ms; cudaEventElapsedTime(&ms, a, b);
+    double pairs = (double)ctas * 8 * rpw * 205.0;
+    printf("rowbench (rows 150-260, smem xj) ctas %5d: %.3f ms  %.2f Gpairs/s\n", ctas, ms, pairs / ms / 1e6);
+  }
   for (int per : {2, 3, 4, 8}) {
     run("math only, MINB2", k_pairbench<0, 2>, sms * per);
     run("math only, MINB4", k_pairbench<0, 4>, sms * per);
