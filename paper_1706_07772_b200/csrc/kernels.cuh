@@ -761,11 +761,11 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, con
 __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, const int* __restrict__ cell_start,
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
-    int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st) {
+    int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, int blk0, Status* st) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NbrSmem S;
-  const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
+  const int blk = blk0 + blockIdx.x / nsplit, split = blockIdx.x % nsplit;   // blk0: first home block of this launch
   float4* cand = reinterpret_cast<float4*>(dyn);                                // window_cap + 32
   int* cand_j = reinterpret_cast<int*>(cand + window_cap + 32);                  // window_cap + 32
   unsigned char* cand_k = reinterpret_cast<unsigned char*>(cand_j + window_cap + 32);
@@ -1283,7 +1283,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
     unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
-    double2* __restrict__ epart, int nsplit, Status* st) {
+    double2* __restrict__ epart, int nsplit, int blk0, Status* st) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
@@ -1291,7 +1291,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   unsigned long long t_start = 0;
   if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
-  const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
+  const int blk = blk0 + blockIdx.x / nsplit, split = blockIdx.x % nsplit;   // blk0: first home block of this launch
   const int nt = prm->nt;
   double* ET = reinterpret_cast<double*>(dyn);                  // exp table
   double2* LT = reinterpret_cast<double2*>(ET + EXP_TBL);       // log table
@@ -1315,7 +1315,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
       set_flag(st, ST_WIN_OVF);
       atomicMax(&st->max_window, W);
     }
-    if (lane == 0) epart[blockIdx.x * NB_WARPS + warp] = make_double2(0.0, 0.0);
+    if (lane == 0) epart[(blk0 * nsplit + blockIdx.x) * NB_WARPS + warp] = make_double2(0.0, 0.0);
     return;
   }
   const int nwu = c_win.nwu;
@@ -1468,12 +1468,12 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     ev_acc += __shfl_xor_sync(0xffffffffu, ev_acc, o);
     ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
   }
-  if (lane == 0) epart[blockIdx.x * NB_WARPS + warp] = make_double2(ev_acc, ec_acc);
+  if (lane == 0) epart[(blk0 * nsplit + blockIdx.x) * NB_WARPS + warp] = make_double2(ev_acc, ec_acc);
 #ifdef NB_EXP_PROF
   if (lane == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_nbprof[blockIdx.x * 16 + 4 + warp] = t;
+    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 4 + warp] = t;
   }
 #endif
   if (__any_sync(0xffffffffu, bad) && lane == 0) S.bad = 1;
@@ -1495,10 +1495,10 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     unsigned sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    g_nbprof[blockIdx.x * 16 + 0] = t_start;
-    g_nbprof[blockIdx.x * 16 + 1] = t_setup;
-    g_nbprof[blockIdx.x * 16 + 2] = t;
-    g_nbprof[blockIdx.x * 16 + 3] = sm;
+    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 0] = t_start;
+    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 1] = t_setup;
+    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 2] = t;
+    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 3] = sm;
   }
 #endif
 }
