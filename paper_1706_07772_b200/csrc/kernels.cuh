@@ -426,6 +426,7 @@ struct NbrSmem {
   WinSmem W;
   float rcand2[NTP_MAX];
   int gbase[NHOME + 1];   // first row group of each home sub-cell (groups of NBR_G rows)
+  int ncs[NBR_THREADS / 32][4];   // per warp: bond-candidate counters of its group's rows
   int next_row;
 };
 
@@ -597,18 +598,23 @@ __device__ __forceinline__ int nbr_row_test(const WinSmem& W, const Grid& g, int
 // shared by the rows.  r^2 in fp32 against a band of +-m around R^2 (~70x the
 // fp32 error bound), the band settled by the exact FMA-free fp64 test (bit-
 // identical to the oracle's r^2); accepted window slots of row r are compacted
-// with one ballot per row and stored coalesced; with BOND, candidates below the
-// conservative BO' = bo_cut radius likewise.  len[r] may exceed row_cap (the
-// caller flags it).
+// with one ballot per row and stored coalesced.  With BOND, the rare
+// candidates below the conservative BO' = bo_cut radius (~3 per row) are
+// appended per lane through a shared-memory counter of the row: no warp vote
+// (POPC/VOTE issue to the narrow XU pipe on sm_100a, 16 lanes/SM/clk, and
+// bound the list build); their order is irrelevant because k_bond_rank sorts
+// each bond row.  len[r] may exceed row_cap (the caller flags it).
 constexpr int NBR_G = 4;
 template <bool BOND, typename SI>
 __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, const float4* __restrict__ cand, SI sl,
                                                const double4* __restrict__ spos, int si0, int nrow, int h,
                                                const Grid& g, const RowTest& rt, uint16_t* __restrict__ nbr,
                                                int row_cap, int* __restrict__ bc, int cand_cap,
-                                               const float* __restrict__ rc2, int nt, float rcmax,
+                                               const float* __restrict__ rc2, int nt, float rcmax, int* ncs,
                                                int (&len)[NBR_G], int (&nc)[NBR_G]) {
   const int lane = threadIdx.x & 31;
+  if (BOND && lane < NBR_G) ncs[lane] = 0;   // per-row bond-candidate counters (shared, this warp's)
+  __syncwarp();
   const unsigned lt_mask = (1u << lane) - 1u, le_mask = lt_mask | (1u << lane);
   float4 ri[NBR_G];
   int sr[NBR_G];
@@ -735,20 +741,20 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, con
       len[r] += __popc(mk);
       anybond |= in[r] && r2v[r] <= rcmax;
     }
-    if (BOND) {
-      if (__any_sync(0xffffffffu, anybond)) {  // ~3 bond candidates per row
-        const int tj = __float_as_int(c.w);
+    if (BOND && anybond) {   // rare (~3 bond candidates per row): per-lane append, no warp vote
+      const int tj = __float_as_int(c.w);
 #pragma unroll
-        for (int r = 0; r < NBR_G; ++r) {
-          const bool bcand = in[r] && r2v[r] <= rc2[__float_as_int(ri[r].w) * nt + tj];
-          const unsigned mb = __ballot_sync(0xffffffffu, bcand);
-          const int pc = nc[r] + __popc(mb & lt_mask);
-          if (bcand && pc < cand_cap) crowp[r][pc] = sl.J(slot);
-          nc[r] += __popc(mb);
+      for (int r = 0; r < NBR_G; ++r) {
+        if (in[r] && r2v[r] <= rc2[__float_as_int(ri[r].w) * nt + tj]) {
+          const int pc = atomicAdd(ncs + r, 1);
+          if (pc < cand_cap) crowp[r][pc] = sl.J(slot);
         }
       }
     }
   }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < NBR_G; ++r) nc[r] = BOND ? ncs[r] : 0;
 }
 
 // One CTA per (home block, split).  Candidates of the window are staged in
@@ -842,7 +848,7 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
     const int si0 = S.W.slot[kh] + a0;
     int len[NBR_G], nc[NBR_G];
     nbr_group_test<true>(S.W, W, cand, sl, spos, si0, nrow, h, g, rt, nbr, row_cap, bc, cand_cap, S.rcand2, nt, rcmax,
-                         len, nc);
+                         S.ncs[threadIdx.x >> 5], len, nc);
     if (lane < nrow) {
       int l = len[0], c = nc[0];
 #pragma unroll
@@ -854,6 +860,7 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
       if (l > row_cap) { set_flag(st, ST_ROW_OVF); atomicMax(&st->max_row, l); }
       if (c > cand_cap) { set_flag(st, ST_CAND_OVF); atomicMax(&st->max_cand, c); }
     }
+    __syncwarp();   // ncs is reset by the warp's next group
   }
 }
 
@@ -1253,6 +1260,45 @@ __device__ __forceinline__ void fix_add(unsigned* A, int* B, double t) {
   atomicAdd(B, (int)b);
 }
 
+// End of a row (one warp): warp-reduce F_i and the row's energies with a
+// fixed butterfly, add F_i to the shared fixed-point window at slot si, and
+// store the row's (E_vdW, E_Coul) partial at its sorted atom s.  Per-row
+// partials make the energy independent of which warp ran the row (the two
+// nonbonded kernels and any row schedule give identical sums).
+__device__ __forceinline__ void row_reduce_store(double fix, double fiy, double fiz, double ev, double ec, int lane,
+                                                 int si, int s, unsigned* fa, int* fb, int window_cap,
+                                                 double2* __restrict__ erow, bool& bad) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    fix += __shfl_xor_sync(0xffffffffu, fix, o);
+    fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
+    fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
+    ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    ec += __shfl_xor_sync(0xffffffffu, ec, o);
+  }
+  if (lane == 0) {
+    const double FIXS = c_nb[25], MAGIC = c_nb[26], FLIM = c_nb[27];
+    bad |= !(fabs(fix) < FLIM && fabs(fiy) < FLIM && fabs(fiz) < FLIM);
+    fix_add(fa + si, fb + si, fma(fix, FIXS, MAGIC));
+    fix_add(fa + window_cap + si, fb + window_cap + si, fma(fiy, FIXS, MAGIC));
+    fix_add(fa + 2 * window_cap + si, fb + 2 * window_cap + si, fma(fiz, FIXS, MAGIC));
+    erow[s] = make_double2(ev, ec);
+  }
+}
+
+// rows of a (block, split) work unit whose kernel gave up (window overflow):
+// zero their energy partials so the fixed-order energy sum stays defined
+__device__ void zero_rows_erow(const WinSmem& W, int split, int nsplit, double2* __restrict__ erow) {
+  int r0 = 0;
+  for (int h = 0; h < NHOME; ++h) {
+    if (!W.home_ok[h]) continue;
+    const int k = c_win.home_k[h], c = W.cnt[k];
+    for (int q = threadIdx.x; q < c; q += blockDim.x)
+      if ((r0 + q) % nsplit == split) erow[W.start[k] + q] = make_double2(0.0, 0.0);
+    r0 += c;
+  }
+}
+
 constexpr int NB_THREADS = 256;
 constexpr int NB_WARPS = NB_THREADS / 32;
 #ifndef NB_MINB
@@ -1283,7 +1329,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
     unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
-    double2* __restrict__ epart, int nsplit, int blk0, Status* st) {
+    double2* __restrict__ erow, int nsplit, int blk0, Status* st) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
@@ -1315,7 +1361,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
       set_flag(st, ST_WIN_OVF);
       atomicMax(&st->max_window, W);
     }
-    if (lane == 0) epart[(blk0 * nsplit + blockIdx.x) * NB_WARPS + warp] = make_double2(0.0, 0.0);
+    zero_rows_erow(S.W, split, nsplit, erow);
     return;
   }
   const int nwu = c_win.nwu;
@@ -1367,7 +1413,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   const bool has_shift = S.W.has_shift != 0;
   const double FIXS = c_nb[25], MAGIC = c_nb[26], FLIM = c_nb[27];
   bool bad = false;
-  double ev_acc = 0.0, ec_acc = 0.0;
 #ifdef NB_EXP_PROF
   unsigned long long t_setup = 0;
   if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_setup));
@@ -1411,7 +1456,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     const double cqi = C * xi.w;
     asm volatile("cp.async.wait_group 1;" ::: "memory");   // this row's entries have landed
     __syncwarp();
-    double fix = 0.0, fiy = 0.0, fiz = 0.0;
+    double fix = 0.0, fiy = 0.0, fiz = 0.0, ev_acc = 0.0, ec_acc = 0.0;
     int slot = lane < len ? (int)row[lane] : si;
     int2 inf = sinfo[slot];
     double4 xj = spos[inf.x];
@@ -1448,27 +1493,10 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
         fix_add(fa + 2 * window_cap + cslot, fb + 2 * window_cap + cslot, fma(gs, dz, MAGIC));
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      fix += __shfl_xor_sync(0xffffffffu, fix, o);
-      fiy += __shfl_xor_sync(0xffffffffu, fiy, o);
-      fiz += __shfl_xor_sync(0xffffffffu, fiz, o);
-    }
-    if (lane == 0) {
-      bad |= !(fabs(fix) < FLIM && fabs(fiy) < FLIM && fabs(fiz) < FLIM);
-      fix_add(fa + si, fb + si, fma(fix, FIXS, MAGIC));
-      fix_add(fa + window_cap + si, fb + window_cap + si, fma(fiy, FIXS, MAGIC));
-      fix_add(fa + 2 * window_cap + si, fb + 2 * window_cap + si, fma(fiz, FIXS, MAGIC));
-    }
+    row_reduce_store(fix, fiy, fiz, ev_acc, ec_acc, lane, si, ii.x, fa, fb, window_cap, erow, bad);
     __syncwarp();   // the buffer of this row is refilled two rows later
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ev_acc += __shfl_xor_sync(0xffffffffu, ev_acc, o);
-    ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
-  }
-  if (lane == 0) epart[(blk0 * nsplit + blockIdx.x) * NB_WARPS + warp] = make_double2(ev_acc, ec_acc);
 #ifdef NB_EXP_PROF
   if (lane == 0) {
     unsigned long long t;
@@ -1503,29 +1531,46 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
 #endif
 }
 
-// a8 finalize, one kernel: un-permute the forces, force[i] = F_sorted[iperm[i]]
-// (int64 fixed point -> fp64), and reset the accumulators to zero for the
-// next step; and the energy: block b sums a fixed slice of the nonbonded
-// partials, the last block to finish sums the block partials in block order
-// (deterministic).
+// a8 finalize, one kernel: un-permute the forces, force[perm[s]] =
+// F_sorted[s] (int64 fixed point -> fp64; sorted-order reads and resets are
+// coalesced, the 24-byte writes scattered), resetting the accumulators to
+// zero for the next step; and the energy: block b sums a fixed slice of the
+// nonbonded partials, the last block to finish sums the block partials with
+// a fixed-shape tree (strided per-thread sums, then warp and block trees), so
+// the result does not depend on timing (deterministic).
 constexpr int FIN_THREADS = 256;
-__global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __restrict__ iperm,
+__device__ __forceinline__ void fin_block_sum(double& a, double& b, double (*red)[FIN_THREADS / 32]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) { red[0][w] = a; red[1][w] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = 0.0; b = 0.0;
+    for (int k = 0; k < FIN_THREADS / 32; ++k) { a += red[0][k]; b += red[1][k]; }
+  }
+}
+__global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __restrict__ perm,
     unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
     double* __restrict__ force, int nparts, const double2* __restrict__ epart, double* __restrict__ part,
     unsigned* __restrict__ ticket, double* __restrict__ energy, Status* st) {
   pdl_wait();
   pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const int s = iperm[i];
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n) {
+    const int i = perm[s];
     const double sc = 0x1.0p-35;
     static_assert(FIX_BITS == 35, "scale");
-    force[3 * (int64_t)i] = (double)(long long)sfx[s] * sc;
-    force[3 * (int64_t)i + 1] = (double)(long long)sfy[s] * sc;
-    force[3 * (int64_t)i + 2] = (double)(long long)sfz[s] * sc;
+    const double fx = (double)(long long)sfx[s] * sc, fy = (double)(long long)sfy[s] * sc, fz = (double)(long long)sfz[s] * sc;
     sfx[s] = 0ull;
     sfy[s] = 0ull;
     sfz[s] = 0ull;
+    force[3 * (int64_t)i] = fx;
+    force[3 * (int64_t)i + 1] = fy;
+    force[3 * (int64_t)i + 2] = fz;
   }
   __shared__ double red[2][FIN_THREADS / 32];
   __shared__ bool last;
@@ -1537,35 +1582,28 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __re
     a += v.x;
     b += v.y;
   }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  if (lane == 0) { red[0][w] = a; red[1][w] = b; }
-  __syncthreads();
+  fin_block_sum(a, b, red);
   if (threadIdx.x == 0) {
-    double x = 0.0, y = 0.0;
-    for (int k = 0; k < FIN_THREADS / 32; ++k) { x += red[0][k]; y += red[1][k]; }
-    part[2 * blockIdx.x] = x;
-    part[2 * blockIdx.x + 1] = y;
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
     __threadfence();
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
+  a = 0.0; b = 0.0;
+  for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
+    a += __ldcg(part + 2 * k);
+    b += __ldcg(part + 2 * k + 1);
+  }
+  __syncthreads();   // red[] is reused
+  fin_block_sum(a, b, red);
   if (threadIdx.x == 0) {
-    double x = 0.0, y = 0.0;
-    for (unsigned k = 0; k < gridDim.x; ++k) {
-      x += ((volatile double*)part)[2 * k];
-      y += ((volatile double*)part)[2 * k + 1];
-    }
-    energy[0] = x;
-    energy[1] = y;
+    energy[0] = a;
+    energy[1] = b;
     *ticket = 0u;   // ready for the next call
-    if (!(isfinite(x) && isfinite(y))) set_flag(st, ST_NONFINITE_OUT);
+    if (!(isfinite(a) && isfinite(b))) set_flag(st, ST_NONFINITE_OUT);
   }
 }
 

@@ -20,7 +20,6 @@ namespace {
 
 constexpr size_t ALIGN = 256;
 constexpr int MAX_SPLIT = 8;
-constexpr int MAX_PARTS = 8;
 // CTAs per home block for the window kernels: small systems (c0/c1) have too
 // few home blocks to fill 148 SMs, so each block's rows are split over
 // several CTAs (each builds the same window)
@@ -407,12 +406,8 @@ struct reax_ctx {
   int nsplit = 1;
   int nsplit_nbr = 1;
   // fork/join of reax_step (bond chain beside the nonbonded kernel)
-  cudaStream_t side = nullptr, side2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_nb = nullptr;
-  cudaEvent_t ev_part[MAX_PARTS] = {};
-  // list/nonbonded pipeline slabs (REAX_PARTS; measured on c1: 1 is fastest, the
-  // co-resident list-build and nonbonded CTAs slow each other down)
-  int parts = getenv("REAX_PARTS") ? std::max(1, atoi(getenv("REAX_PARTS"))) : 1;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool serial = getenv("REAX_SERIAL") != nullptr;
   bool pdl = getenv("REAX_NO_PDL") == nullptr;   // programmatic dependent launch on the hot path
 };
@@ -737,8 +732,8 @@ void launch_nb_part(reax_ctx* c, int b0, int b1, int nt, cudaStream_t s) {
 void launch_finalize(reax_ctx* c, int N, double* force, double* energy, cudaStream_t s) {
   WS& w = c->w;
   Timer t(c, 5, s);
-  const int nparts = c->g.nblock * c->nsplit * NB_WARPS;   // one energy partial per nonbonded warp
-  launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.iperm, w.sfx, w.sfy, w.sfz, force, nparts,
+  // one energy partial per half-list row (sorted order), summed in fixed order
+  launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.perm, w.sfx, w.sfy, w.sfz, force, N,
            w.erow, w.epart, w.ticket, energy, w.st);
   LAUNCH(c);
 }
@@ -805,33 +800,21 @@ reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, 
   const bool fork = !c->serial;
   const int nt = prm->ntypes;
   launch_bin(c, N, pos, type, q, nt, s);
-  if (!fork) {
-    launch_nbr_part(c, 0, c->g.nblock, s);
-    launch_bonds(c, N, s);
-    launch_bond_correct(c, s);
-    launch_nb_part(c, 0, c->g.nblock, nt, s);
-    launch_finalize(c, N, force, energy, s);
-  } else {
-    // software pipeline over P slabs of home blocks: the list build of slab
-    // k+1 (stream s) runs beside the nonbonded kernel of slab k (side2); the
-    // bond chain (side) starts when all lists are built; s joins both
-    const int P = std::max(1, std::min(c->parts, std::min(MAX_PARTS, c->g.nblock)));
-    for (int k = 0; k < P; ++k) {
-      const int b0 = (int)((int64_t)c->g.nblock * k / P), b1 = (int)((int64_t)c->g.nblock * (k + 1) / P);
-      launch_nbr_part(c, b0, b1, s);
-      if (cudaEventRecord(c->ev_part[k], s) != cudaSuccess || cudaStreamWaitEvent(c->side2, c->ev_part[k], 0) != cudaSuccess)
-        return fail_cuda(cudaGetLastError());
-      launch_nb_part(c, b0, b1, nt, c->side2);
-    }
+  launch_nbr_part(c, 0, c->g.nblock, s);
+  // fork: the bond chain (a4-a6, small latency-bound kernels) on the side
+  // stream beside the nonbonded kernel (a7) on s; join; k_finalize (a8)
+  cudaStream_t sb = s;
+  if (fork) {
     if (cudaEventRecord(c->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(c->side, c->ev_fork, 0) != cudaSuccess)
       return fail_cuda(cudaGetLastError());
-    launch_bonds(c, N, c->side);
-    launch_bond_correct(c, c->side);
-    if (cudaEventRecord(c->ev_join, c->side) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join, 0) != cudaSuccess ||
-        cudaEventRecord(c->ev_nb, c->side2) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_nb, 0) != cudaSuccess)
-      return fail_cuda(cudaGetLastError());
-    launch_finalize(c, N, force, energy, s);
+    sb = c->side;
   }
+  launch_bonds(c, N, sb);
+  launch_bond_correct(c, sb);
+  launch_nb_part(c, 0, c->g.nblock, nt, s);
+  if (fork && (cudaEventRecord(c->ev_join, c->side) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join, 0) != cudaSuccess))
+    return fail_cuda(cudaGetLastError());
+  launch_finalize(c, N, force, energy, s);
   if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
   note_build(c, pos, type, box);
   c->lists_ok = c->bonds_ok = true;
@@ -882,11 +865,8 @@ reax_status reax_create(reax_ctx** out) {
   }
   memset(c->h_st, 0, sizeof(Status));
   bool ok = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) == cudaSuccess &&
-            cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-            cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) == cudaSuccess &&
-            cudaEventCreateWithFlags(&c->ev_nb, cudaEventDisableTiming) == cudaSuccess;
-  for (int k = 0; ok && k < MAX_PARTS; ++k) ok = cudaEventCreateWithFlags(&c->ev_part[k], cudaEventDisableTiming) == cudaSuccess;
+            cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) == cudaSuccess;
   if (!ok) {
     reax_destroy(c);
     return REAX_ERR_CUDA;
@@ -906,12 +886,8 @@ reax_status reax_destroy(reax_ctx* c) {
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_prm) cudaFreeHost(c->h_prm);
   if (c->side) cudaStreamDestroy(c->side);
-  if (c->side2) cudaStreamDestroy(c->side2);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
-  if (c->ev_nb) cudaEventDestroy(c->ev_nb);
-  for (int k = 0; k < MAX_PARTS; ++k)
-    if (c->ev_part[k]) cudaEventDestroy(c->ev_part[k]);
   delete c;
   return REAX_OK;
 }
