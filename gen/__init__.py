@@ -55,6 +55,8 @@ def _get():
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
         lib.gen_params.restype = None
         lib.gen_params.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        lib.gen_bond_params.restype = None
+        lib.gen_bond_params.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p]
         lib.gen_uniforms.restype = None
         lib.gen_uniforms.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p]
         _lib = lib
@@ -139,3 +141,27 @@ def make_params(seed: int = SEED_BASE, ntypes: int = NTYPES) -> Params:
     cols = [np.ascontiguousarray(pt[:, k]) for k in range(11)]
     pcols = [np.ascontiguousarray(pp[:, :, k]) for k in range(7)]
     return Params(ntypes, *cols, val, val.copy(), *pcols)
+
+
+BOND_SEED = SEED_BASE + 7000
+
+
+@dataclass
+class BondParams:
+    """Bond-energy parameters per type pair (NEXT-1; reading 28).
+    De_sigma is Params.De."""
+    De_pi: np.ndarray     # (ntypes, ntypes) symmetric
+    De_pipi: np.ndarray
+    p_be1: np.ndarray
+    p_be2: np.ndarray
+
+    FIELDS = ("De_pi", "De_pipi", "p_be1", "p_be2")
+
+    def copy(self) -> "BondParams":
+        return BondParams(*(getattr(self, f).copy() for f in self.FIELDS))
+
+
+def make_bond_params(seed: int = BOND_SEED, ntypes: int = NTYPES) -> BondParams:
+    pp = np.empty((ntypes, ntypes, 4), np.float64)
+    _get().gen_bond_params(seed, ntypes, pp.ctypes.data)
+    return BondParams(*(np.ascontiguousarray(pp[:, :, k]) for k in range(4)))

@@ -142,3 +142,20 @@ void gen_params(uint64_t seed, int ntypes, double* per_type, double* per_pair) {
         per_pair[(b * ntypes + a) * 7 + k] = v;
       }
 }
+
+/* Bond-energy parameters (NEXT-1; reading 28),
+ * drawn from their own seed so the table above is unchanged.
+ * per_pair: [ntypes][ntypes][4] = De_pi, De_pipi, p_be1, p_be2 per type pair
+ * t1 <= t2 (lexicographic), symmetric.  De_sigma is the table's De. */
+void gen_bond_params(uint64_t seed, int ntypes, double* per_pair) {
+  static const double lo[4] = {20.0, 10.0, -0.8, 0.2};
+  static const double hi[4] = {100.0, 80.0, 0.5, 1.0};
+  sm64 g = {seed};
+  for (int a = 0; a < ntypes; ++a)
+    for (int b = a; b < ntypes; ++b)
+      for (int k = 0; k < 4; ++k) {
+        double v = lo[k] + (hi[k] - lo[k]) * sm64_u(&g);
+        per_pair[(a * ntypes + b) * 4 + k] = v;
+        per_pair[(b * ntypes + a) * 4 + k] = v;
+      }
+}

@@ -38,6 +38,28 @@ class OrcParams(ctypes.Structure):
                 + [(f, ctypes.c_double) for f in ("p_boc1", "p_boc2", "p_vdw1", "coulomb_c")])
 
 
+class OrcBondParams(ctypes.Structure):
+    _fields_ = [(f, _D) for f in ("De_s", "De_p", "De_pp", "p_be1", "p_be2")]
+
+
+class _Q:
+    """Bond-energy parameters (De_s = Params.De) as the oracle's struct."""
+
+    def __init__(self, params, bparams):
+        self.keep = []
+        s = OrcBondParams()
+        for f, a in (("De_s", params.De), ("De_p", bparams.De_pi), ("De_pp", bparams.De_pipi),
+                     ("p_be1", bparams.p_be1), ("p_be2", bparams.p_be2)):
+            a = np.ascontiguousarray(a, dtype=np.float64).ravel()
+            self.keep.append(a)
+            setattr(s, f, a.ctypes.data_as(_D))
+        self.s = s
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.s)
+
+
 class _P:
     """Keeps the numpy buffers alive alongside the ctypes struct."""
 
@@ -89,6 +111,8 @@ def _get():
             "orc_atom_neighbors": (I64, [I64, I64, V, V, DBL, V, I64]),
             "orc_atom_force": (None, [I64, I64, V, V, V, V, V, DBL, V, V]),
             "orc_atom_bonds": (I64, [I64, I64, V, V, V, V, DBL, DBL, V, V, V, I64]),
+            "orc_bond_energy_pair": (None, [DBL, V, DBL, DBL, DBL, DBL, INT, INT, V, V, V]),
+            "orc_bond_energy": (None, [I64, V, V, V, V, V, V, V, V, V, V, V]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -279,3 +303,35 @@ def evaluate(system, params, cut, mode="cells"):
     E, F = nonbonded(pos, system.type, system.q, system.box, params, cut["r_nonb"], hrow, hcol)
     return dict(pos=pos, hrow=hrow, hcol=hcol, brow=brow, bcol=bcol, mirror=mir, raw=raw, delta=dlt,
                 corr=corr, E=E, F=F)
+
+
+def bond_energy_pair(r, raw, di, dboci, dj, dbocj, ti, tj, params, bparams):
+    """One bond (canonical orientation): [e, de/dr|_S, de/dS_i, de/dS_j, dBO'/dr] (O8)."""
+    P, Q = _P(params), _Q(params, bparams)
+    raw = _a(raw, np.float64)
+    out = np.empty(5)
+    _get().orc_bond_energy_pair(float(r), _ptr(raw), float(di), float(dboci), float(dj), float(dbocj),
+                                int(ti), int(tj), P.ref, Q.ref, _ptr(out))
+    return out
+
+
+def bond_energy(pos, type_, box, params, bparams, brow, bcol, raw, dlt):
+    """O8 (NEXT-1): E_bond and its forces F (n,3) at a fixed bond set."""
+    P, Q = _P(params), _Q(params, bparams)
+    pos, type_, box = _a(pos, np.float64), _a(type_, np.int32), _a(box, np.float64)
+    n = len(pos)
+    F = np.empty((n, 3))
+    E = ctypes.c_double()
+    _get().orc_bond_energy(n, _ptr(pos), _ptr(type_), _ptr(box), P.ref, Q.ref, _ptr(_a(brow, np.int64)),
+                           _ptr(_a(bcol, np.int32)), _ptr(_a(raw, np.float64)), _ptr(_a(dlt, np.float64)),
+                           _ptr(F), ctypes.addressof(E))
+    return E.value, F
+
+
+def evaluate_bond_energy(system, params, bparams, cut, ref=None):
+    """Lists and bond orders (evaluate()), then O8.  Returns (E_bond, F_bond, ref)."""
+    if ref is None:
+        ref = evaluate(system, params, cut)
+    E, F = bond_energy(ref["pos"], system.type, system.box, params, bparams, ref["brow"], ref["bcol"],
+                       ref["raw"], ref["delta"])
+    return E, F, ref

@@ -19,6 +19,8 @@
  *   O5 corrected bond orders f1..f5 (B4-B8)           PAPER.md:160 (§3.3); north_star
  *   O6 tapered shielded vdW + Coulomb (N1-N6),
  *      Alg. 1/Alg. 2 pair loop with F_i += f, F_k -= f PAPER.md:87-110 (Alg. 1), 162-196 (Alg. 2)
+ *   O8 (NEXT-1) bond energy E1 and its forces through the bond-order
+ *      derivatives (the bond part of "Aggregate Forces")  PAPER.md:160, 285 (§3.3, Table 2)
  *
  * PARITY NOTE.  PAPER.md states no ReaxFF equations (it cites refs [6,7],
  * PAPER.md:37); the functional forms B1-B8 / N1-N6 are the standard published
@@ -445,4 +447,141 @@ int64_t orc_atom_bonds(int64_t i, int64_t n, const double* pos, const int32_t* t
   delta[0] = s - P->val[type[i]];
   delta[1] = s - P->val_boc[type[i]];
   return m;
+}
+
+/* ------------------------------------------------------- O8 bond energy (NEXT-1)
+ * the bond energy of the corrected bond orders and its
+ * forces through the chain rule of B1-B8 (the bond part of "Aggregate Forces",
+ * PAPER.md:160, 285).  Form (standard ReaxFF, ref [6]; reading 28):
+ *   (E1) e_ij = -De_s BOs exp[p_be1 (1 - BOs^p_be2)] - De_p BOpi - De_pp BOpipi,
+ *        BOs^p_be2 := 0 for BOs <= 0,
+ * summed once per bond (canonical i < j).  Bonds are those of O3 (reading 2A:
+ * BO' >= bo_cut), held fixed: E is differentiated at a fixed bond set.
+ * Every bond order of bond b = (i, j) depends on its own distance r_b (B1) and
+ * on the sums S_i = sum_k BO'_ik, S_j (through Delta'_i = S_i - Val_i and
+ * Delta'boc_i = S_i - Val^boc_i in f1, f4, f5).  Hence
+ *   dE/dr_b = de_b/dr_b |_S + (D_i + D_j) dBO'_b/dr_b,   D_i = sum_{b' ni i} de_b'/dS_i,
+ * and the forces are central along each bond: F_i += g d, F_j -= g d with
+ * g = (dE/dr_b)/r_b, d = minimum-image(x_j - x_i) (F = -grad E, as O6). */
+
+/* d/dr of the three B1 terms at distance r: out = {dBO'sigma, dBO'pi, dBO'pipi}/dr,
+ * from BO'_k = exp(pa (r/r0)^pb): dBO'_k/dr = BO'_k pa pb (r/r0)^pb / r. */
+static void orc_bo_raw_dr(double r, int ti, int tj, const orc_params* P, const double raw[4], double out[3]) {
+  int nt = P->ntypes, tp = ti * nt + tj;
+  double r0[3] = {0.5 * (P->r_sigma[ti] + P->r_sigma[tj]), 0.5 * (P->r_pi[ti] + P->r_pi[tj]),
+                  0.5 * (P->r_pipi[ti] + P->r_pipi[tj])};
+  double pa[3] = {P->p_bo1[tp], P->p_bo3[tp], P->p_bo5[tp]};
+  double pb[3] = {P->p_bo2[tp], P->p_bo4[tp], P->p_bo6[tp]};
+  for (int k = 0; k < 3; ++k) out[k] = raw[k] * pa[k] * pb[k] * pow(r / r0[k], pb[k]) / r;
+}
+
+/* One bond (i, j) in canonical orientation: its energy e (E1) and the partial
+ * derivatives de/dr|_S (at fixed S_i, S_j), de/dS_i, de/dS_j, plus dBO'/dr.
+ * Follows B4-B8 as orc_bo_corr_pair and differentiates each factor:
+ *   f2 = e^{-p1 Di} + e^{-p1 Dj}           df2/dDi = -p1 e^{-p1 Di}
+ *   f3 = -(1/p2) ln(1/2 (e^{-p2 Di} + e^{-p2 Dj}))
+ *                                          df3/dDi = e^{-p2 Di} / (e^{-p2 Di} + e^{-p2 Dj})
+ *   f1 = 1/2 (u_i + u_j), u_a = (V_a + f2)/(V_a + f2 + f3)
+ *                                          du_a/df2 = f3 / (V_a+f2+f3)^2,
+ *                                          du_a/df3 = -(V_a + f2) / (V_a+f2+f3)^2
+ *   f4 = 1/(1 + e^{z4}), z4 = -p3 (p4 BO'^2 - Dboc_i) + p5
+ *                                          df4/dBO' = f4 (1-f4) 2 p3 p4 BO',  df4/dS_i = -f4 (1-f4) p3
+ *   BO = BO' A, BOpi = BO'pi f1 A, BOpipi = BO'pipi f1 A, A = f1 f4 f5, BOs = BO - BOpi - BOpipi. */
+void orc_bond_energy_pair(double r, const double raw[4], double di, double dboci, double dj, double dbocj,
+                          int ti, int tj, const orc_params* P, const orc_bond_params* Q, double out[5]) {
+  int tp = ti * P->ntypes + tj;
+  double p1 = P->p_boc1, p2 = P->p_boc2;
+  double vi = P->val[ti], vj = P->val[tj];
+  double p3 = sqrt(P->b132[ti] * P->b132[tj]);
+  double p4 = sqrt(P->b131[ti] * P->b131[tj]);
+  double p5 = sqrt(P->b133[ti] * P->b133[tj]);
+  double bpi = raw[1], bpp = raw[2], bo = raw[3];
+  /* B4-B8 */
+  double ei1 = exp(-p1 * di), ej1 = exp(-p1 * dj);
+  double ei2 = exp(-p2 * di), ej2 = exp(-p2 * dj);
+  double f2 = ei1 + ej1;
+  double f3 = -(1.0 / p2) * log(0.5 * (ei2 + ej2));
+  double ni = vi + f2 + f3, nj = vj + f2 + f3;
+  double f1 = 0.5 * ((vi + f2) / ni + (vj + f2) / nj);
+  double f4 = 1.0 / (1.0 + exp(-p3 * (p4 * bo * bo - dboci) + p5));
+  double f5 = 1.0 / (1.0 + exp(-p3 * (p4 * bo * bo - dbocj) + p5));
+  double A = f1 * f4 * f5;
+  double BO = bo * A, BOpi = bpi * f1 * A, BOpp = bpp * f1 * A;
+  double BOs = BO - BOpi - BOpp;
+  /* E1 and its partials in BOs, BOpi, BOpipi */
+  double Ds = Q->De_s[tp], Dp = Q->De_p[tp], Dpp = Q->De_pp[tp], b1 = Q->p_be1[tp], b2 = Q->p_be2[tp];
+  double sp = BOs > 0.0 ? pow(BOs, b2) : 0.0;
+  double ex = exp(b1 * (1.0 - sp));
+  double e = -Ds * BOs * ex - Dp * BOpi - Dpp * BOpp;
+  double e_s = -Ds * ex * (1.0 - b1 * b2 * sp);
+  double c_bo = e_s, c_pi = -Dp - e_s, c_pp = -Dpp - e_s;   /* de/dBO, de/dBOpi, de/dBOpipi */
+  /* through A = f1 f4 f5 and the explicit f1 of BOpi, BOpipi */
+  double w = c_pi * bpi + c_pp * bpp;
+  double de_dA = c_bo * bo + w * f1;
+  double de_df1 = de_dA * f4 * f5 + w * A;
+  double de_df4 = de_dA * f1 * f5;
+  double de_df5 = de_dA * f1 * f4;
+  /* f1 in Delta'_i, Delta'_j */
+  double du_i_df2 = f3 / (ni * ni), du_i_df3 = -(vi + f2) / (ni * ni);
+  double du_j_df2 = f3 / (nj * nj), du_j_df3 = -(vj + f2) / (nj * nj);
+  double df2_di = -p1 * ei1, df2_dj = -p1 * ej1;
+  double df3_di = ei2 / (ei2 + ej2), df3_dj = ej2 / (ei2 + ej2);
+  double df1_di = 0.5 * ((du_i_df2 + du_j_df2) * df2_di + (du_i_df3 + du_j_df3) * df3_di);
+  double df1_dj = 0.5 * ((du_i_df2 + du_j_df2) * df2_dj + (du_i_df3 + du_j_df3) * df3_dj);
+  /* f4, f5 in S (through Delta'boc) and in BO' */
+  double df4_dS = -f4 * (1.0 - f4) * p3, df5_dS = -f5 * (1.0 - f5) * p3;
+  double df4_dbo = f4 * (1.0 - f4) * 2.0 * p3 * p4 * bo, df5_dbo = f5 * (1.0 - f5) * 2.0 * p3 * p4 * bo;
+  double de_dSi = de_df1 * df1_di + de_df4 * df4_dS;
+  double de_dSj = de_df1 * df1_dj + de_df5 * df5_dS;
+  /* direct r dependence at fixed S: each raw term of BO, BOpi, BOpipi, and BO' in f4, f5 */
+  double dr[3];
+  orc_bo_raw_dr(r, ti, tj, P, raw, dr);
+  double X = de_df4 * df4_dbo + de_df5 * df5_dbo;   /* de/dBO' through f4, f5 */
+  double de_dr = (c_bo * A + X) * dr[0] + (c_bo * A + c_pi * f1 * A + X) * dr[1] +
+                 (c_bo * A + c_pp * f1 * A + X) * dr[2];
+  out[0] = e;
+  out[1] = de_dr;
+  out[2] = de_dSi;
+  out[3] = de_dSj;
+  out[4] = (dr[0] + dr[1]) + dr[2];   /* dBO'/dr */
+}
+
+/* O8: E1 over the bonds of O3 (canonical i < j, ascending), Neumaier-summed;
+ * forces [n][3] (overwritten) by the two passes stated above: D_i summed over
+ * the canonical bonds in order, then g per bond.  raw: [B][4] BO' terms of
+ * O3; delta: [n][2] of O4. */
+void orc_bond_energy(int64_t n, const double* pos, const int32_t* type, const double box[3],
+                     const orc_params* P, const orc_bond_params* Q, const int64_t* brow,
+                     const int32_t* bcol, const double* raw, const double* delta, double* force,
+                     double* energy) {
+  double* D = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+  orc_ksum E = {0.0, 0.0};
+  double d[3], out[5];
+  for (int64_t k = 0; k < 3 * n; ++k) force[k] = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = brow[i]; e < brow[i + 1]; ++e) {
+      int64_t j = bcol[e];
+      if (j < i) continue;
+      double r = sqrt(orc_dist2(pos, i, j, box, d));
+      orc_bond_energy_pair(r, &raw[4 * e], delta[2 * i], delta[2 * i + 1], delta[2 * j], delta[2 * j + 1],
+                           type[i], type[j], P, Q, out);
+      ks_add(&E, out[0]);
+      D[i] += out[2];
+      D[j] += out[3];
+    }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = brow[i]; e < brow[i + 1]; ++e) {
+      int64_t j = bcol[e];
+      if (j < i) continue;
+      double r = sqrt(orc_dist2(pos, i, j, box, d));
+      orc_bond_energy_pair(r, &raw[4 * e], delta[2 * i], delta[2 * i + 1], delta[2 * j], delta[2 * j + 1],
+                           type[i], type[j], P, Q, out);
+      double g = (out[1] + (D[i] + D[j]) * out[4]) / r;
+      for (int k = 0; k < 3; ++k) {
+        force[3 * i + k] += g * d[k];
+        force[3 * j + k] -= g * d[k];
+      }
+    }
+  *energy = E.s + E.c;
+  free(D);
 }

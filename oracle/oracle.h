@@ -14,4 +14,9 @@ typedef struct {
   double p_boc1, p_boc2, p_vdw1, coulomb_c;
 } orc_params;
 
+/* Bond-energy parameters (NEXT-1), per type pair [ntypes*ntypes], symmetric. */
+typedef struct {
+  const double *De_s, *De_p, *De_pp, *p_be1, *p_be2;
+} orc_bond_params;
+
 #endif
