@@ -86,6 +86,13 @@ typedef struct {
   double p_boc1, p_boc2, p_vdw1, coulomb_c;
 } reax_params;
 
+/* Bond-energy parameters (NEXT-1), per type pair [host],
+ * ntypes*ntypes row-major, symmetric: De_pi, De_pipi (kcal/mol), p_be1,
+ * p_be2 (> 0).  De_sigma is reax_params.De.  DESIGN.md reading 28. */
+typedef struct {
+  const double *De_pi, *De_pipi, *p_be1, *p_be2;
+} reax_bond_params;
+
 typedef struct reax_ctx reax_ctx;
 
 /* Capacities of a bound workspace.  Zero fields mean "library default". */
@@ -134,6 +141,24 @@ reax_status reax_build_lists(reax_ctx* ctx, int64_t n, const double* pos, const 
 reax_status reax_bond_orders(reax_ctx* ctx, const reax_params* params, const reax_cutoffs* cut,
                              void* stream);
 
+/* NEXT-1: bond energy and its forces — the bond part of "Aggregate Forces"
+ * (§3.3, Table 2 row PAPER.md:285).  Per bond of the current
+ * bond list (each unordered bond once), from the corrected bond orders of a6
+ * (standard ReaxFF form, reading 28):
+ *   E1  e = -De_s BOs exp[p_be1 (1 - BOs^p_be2)] - De_pi BOpi - De_pipi BOpipi
+ * (BOs^p_be2 := 0 for BOs <= 0).  Forces F = -dE_bond/dx at the fixed bond
+ * set, through the bond-order derivatives: every bond order depends on its
+ * r (B1) and on Delta'_i, Delta'_j (f1, f4, f5, B4-B7), so each bond carries a
+ * central force (dE/dr_b)/r_b d with dE/dr_b = de_b/dr_b|_Delta +
+ * (D_i + D_j) dBO'_b/dr_b, D_i = sum over i's bonds of de/dDelta'_i.
+ * Precondition: reax_bond_orders (or reax_step) on this ctx; the parameters
+ * must be those of that build.  force [dev] n*3 fp64 (overwritten, input
+ * order); energy [dev] 1 fp64 {E_bond} (overwritten).  REAX_ERR_PARAM for a
+ * non-finite or asymmetric table or p_be2 <= 0; REAX_ERR_RANGE if a force
+ * component of one bond reaches 65536 kcal/mol/A. */
+reax_status reax_bond_energy(reax_ctx* ctx, const reax_params* params, const reax_bond_params* bond_params,
+                             double* force, double* energy, void* stream);
+
 /* a7-a8: Alg. 2 over the half list: tapered shielded vdW + Coulomb (N1-N6)
  * at the given charges.  q [dev] n fp64; force [dev] n*3 fp64 (overwritten,
  * input order, F = -dE/dx); energy [dev] 2 fp64 {E_vdW, E_Coul}
@@ -164,8 +189,9 @@ reax_status reax_check(reax_ctx* ctx, void* stream);
  * groups: 0 "bin" (wrap + counting sort), 1 "nbr" (k_nbr_build), 2 "bonds"
  * (bond evaluation, scan, fill, row sort + Delta'), 3 "bond_orders"
  * (k_bond_correct), 4 "nonbonded" (k_nonbonded alone), 5 "other" (charge
- * gather, force un-permute, energy reduction). */
-#define REAX_NKERNELS 6
+ * gather, force un-permute, energy reduction), 6 "bond_energy" (NEXT-1,
+ * reax_bond_energy). */
+#define REAX_NKERNELS 7
 reax_status reax_set_timing(reax_ctx* ctx, int enable);
 /* Accumulated milliseconds and launch counts per kernel group since the last
  * reset (synchronises the last recorded events).  reset = 0: accumulate and

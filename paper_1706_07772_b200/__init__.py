@@ -20,12 +20,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("REAX_LIBRARY", os.path.join(_HERE, "libreax.so"))
 
 OK, ERR_ARG, ERR_BOX, ERR_CUTOFF, ERR_PARAM, ERR_CAPACITY, ERR_NONFINITE, ERR_CUDA, ERR_STATE, ERR_RANGE = range(10)
-KERNEL_GROUPS = ("bin", "nbr", "bonds", "bond_orders", "nonbonded", "other")
+KERNEL_GROUPS = ("bin", "nbr", "bonds", "bond_orders", "nonbonded", "other", "bond_energy")
 EXPORTED = ("reax_status_str", "reax_create", "reax_destroy", "reax_workspace_bytes", "reax_bind_workspace",
             "reax_required", "reax_build_lists", "reax_bond_orders", "reax_nonbonded", "reax_step",
             "reax_step_host", "reax_set_async", "reax_check", "reax_set_timing", "reax_kernel_ms",
             "reax_launches_per_step", "reax_pair_count", "reax_export_pairs", "reax_export_nbr_digest",
-            "reax_export_bonds", "reax_selftest_math", "reax_last_cuda_error")
+            "reax_export_bonds", "reax_selftest_math", "reax_last_cuda_error", "reax_bond_energy")
 
 
 class ReaxError(RuntimeError):
@@ -50,6 +50,13 @@ GLOBALS = ("p_boc1", "p_boc2", "p_vdw1", "coulomb_c")
 class Params(ctypes.Structure):
     _fields_ = ([("ntypes", ctypes.c_int32)] + [(f, _D) for f in PER_TYPE] + [(f, _D) for f in PER_PAIR]
                 + [(f, ctypes.c_double) for f in GLOBALS])
+
+
+BOND_PAIR = ("De_pi", "De_pipi", "p_be1", "p_be2")
+
+
+class BondParams(ctypes.Structure):
+    _fields_ = [(f, _D) for f in BOND_PAIR]
 
 
 class Capacity(ctypes.Structure):
@@ -79,6 +86,7 @@ def load_library(path: str = LIB_PATH):
         "reax_required": (ctypes.c_int, [V, P]),
         "reax_build_lists": (ctypes.c_int, [V, I64, P, P, P, P, P, P]),
         "reax_bond_orders": (ctypes.c_int, [V, P, P, P]),
+        "reax_bond_energy": (ctypes.c_int, [V, P, P, P, P, P]),
         "reax_nonbonded": (ctypes.c_int, [V, I64, P, P, P, P, P, P, P, P, P]),
         "reax_step": (ctypes.c_int, [V, I64, P, P, P, P, P, P, P, P, P]),
         "reax_step_host": (ctypes.c_int, [V, I64, P, P, P, P, P, P, P, P, P]),
@@ -236,6 +244,19 @@ class Reax:
                "reax_nonbonded")
         return force, energy
 
+    def bond_energy(self, bond_params, force=None, energy=None, stream=None):
+        """reax_bond_energy (NEXT-1): E_bond and its forces at the current bond list."""
+        import numpy as np
+        force = force if force is not None else torch.empty((self.n, 3), dtype=torch.float64, device=self.device)
+        energy = energy if energy is not None else torch.empty(1, dtype=torch.float64, device=self.device)
+        keep = [np.ascontiguousarray(getattr(bond_params, f), dtype=np.float64).ravel() for f in BOND_PAIR]
+        bp = BondParams(*[a.ctypes.data_as(_D) for a in keep])
+        _check(self.lib.reax_bond_energy(self.ctx, self.params.ref, ctypes.byref(bp),
+                                         _dptr(force, torch.float64, (self.n, 3), "force"),
+                                         _dptr(energy, torch.float64, (1,), "energy"), _stream_ptr(stream)),
+               "reax_bond_energy")
+        return force, energy
+
     def step(self, pos, type_, q, force=None, energy=None, stream=None):
         force = force if force is not None else torch.empty((self.n, 3), dtype=torch.float64, device=self.device)
         energy = energy if energy is not None else torch.empty(2, dtype=torch.float64, device=self.device)
@@ -269,8 +290,8 @@ class Reax:
         _check(self.lib.reax_set_timing(self.ctx, int(bool(enable))), "reax_set_timing")
 
     def kernel_ms(self, reset=False, peek=False):
-        ms = (ctypes.c_double * 6)()
-        nl = (ctypes.c_int64 * 6)()
+        ms = (ctypes.c_double * len(KERNEL_GROUPS))()
+        nl = (ctypes.c_int64 * len(KERNEL_GROUPS))()
         _check(self.lib.reax_kernel_ms(self.ctx, ms, nl, 2 if peek else int(reset)), "reax_kernel_ms")
         return {k: (ms[i], nl[i]) for i, k in enumerate(KERNEL_GROUPS)}
 

@@ -64,6 +64,11 @@ struct BOPair {      // bond-order constants per type pair (B1, B7)
   double pboc3, pboc4, pboc5;
 };
 
+struct BEPair {      // bond-energy constants per type pair (NEXT-1, E1)
+  double Ds, Dp, Dpp;  // De_sigma (reax_params.De), De_pi, De_pipi
+  double pbe1, pbe2;
+};
+
 struct DevParams {
   int nt;
   double R, R2, rb2, bo_cut;
@@ -145,6 +150,10 @@ struct WS {
   double* h_q;
   double* h_force;
   double* h_energy;  // 2
+  // NEXT-1 bond energy (reax_bond_energy)
+  BEPair* bep;       // NTP_MAX
+  double* bD;        // n   D_i = sum over the row's bonds of de/dS_i
+  double4* bde;      // bond_cap per entry {de/dr|S, dBO'/dr, e, de/dS_owner}: aliases uraw (dead after the bond fill)
 };
 
 }  // namespace rx

@@ -1556,7 +1556,7 @@ __device__ __forceinline__ void fin_block_sum(double& a, double& b, double (*red
 __global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __restrict__ perm,
     unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
     double* __restrict__ force, int nparts, const double2* __restrict__ epart, double* __restrict__ part,
-    unsigned* __restrict__ ticket, double* __restrict__ energy, Status* st) {
+    unsigned* __restrict__ ticket, double* __restrict__ energy, int ne, Status* st) {
   pdl_wait();
   pdl_trigger();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1601,10 +1601,151 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __re
   fin_block_sum(a, b, red);
   if (threadIdx.x == 0) {
     energy[0] = a;
-    energy[1] = b;
+    if (ne > 1) energy[1] = b;
     *ticket = 0u;   // ready for the next call
     if (!(isfinite(a) && isfinite(b))) set_flag(st, ST_NONFINITE_OUT);
   }
+}
+
+// ============================================ NEXT-1 bond energy (E1)
+// SURVEY.md §8(f) NEXT-1, the bond part of "Aggregate Forces" (PAPER.md:160,
+// 285).  E1 per bond (standard ReaxFF, ref [6]; reading 28):
+//   e = -De_s BOs exp[p_be1 (1 - BOs^p_be2)] - De_p BOpi - De_pp BOpipi,
+// BOs^p_be2 := 0 for BOs <= 0, at the bond set of a6 (held fixed).  Every bond
+// order of bond b = (i, j) depends on r_b (B1) and on S_i = sum_k BO'_ik, S_j
+// (f1, f4, f5), so dE/dr_b = de_b/dr_b|_S + (D_i + D_j) dBO'_b/dr_b with
+// D_i = sum_{b' at i} de_b'/dS_i, and the forces are central along the bonds.
+// Three passes: per bond (canonical entry, orientation as k_bond_correct) the
+// terms; per atom row D_i and the row's energy (fixed order); per bond the
+// force, added to the int64 fixed-point accumulators (order-free).
+
+// bond vector d = minimum-image(x_b - x_a) and r, exactly as k_bond_eval
+__device__ __forceinline__ double bond_vec(const double4& xa, const double4& xb, const Grid& g, double d[3]) {
+  d[0] = min_image(__dsub_rn(xb.x, xa.x), g.L[0]);
+  d[1] = min_image(__dsub_rn(xb.y, xa.y), g.L[1]);
+  d[2] = min_image(__dsub_rn(xb.z, xa.z), g.L[2]);
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
+}
+
+__global__ void k_bond_energy_terms(const int* __restrict__ perm, const int* __restrict__ stype,
+                                    const double4* __restrict__ spos, Grid g, const DevParams* __restrict__ prm,
+                                    const BEPair* __restrict__ bep, const int* __restrict__ bcol,
+                                    const int* __restrict__ bkey, const int* __restrict__ bown,
+                                    const int* __restrict__ bmir, const double* __restrict__ bo,
+                                    const double2* __restrict__ delta, double4* __restrict__ bde, long long bond_cap,
+                                    const Status* __restrict__ st) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ BOPair sbo[NTP_MAX];
+  __shared__ BEPair sbe[NTP_MAX];
+  __shared__ double sval[NT_MAX];
+  const int nt = prm->nt;
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) { sbo[t] = prm->bo[t]; sbe[t] = bep[t]; }
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) sval[t] = prm->val[t];
+  __syncthreads();
+  const long long B = st->bonds < bond_cap ? st->bonds : bond_cap;
+  const double p1 = prm->p_boc1, p2 = prm->p_boc2, inv_p2 = 1.0 / p2;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
+    const int s = bown[e], j = bcol[e];
+    if (!(perm[s] < bkey[e])) continue;   // the canonical entry writes both
+    const int ta = stype[s], tb = stype[j];
+    const BOPair& c = sbo[ta * nt + tb];
+    const BEPair& q = sbe[ta * nt + tb];
+    double d[3];
+    const double r = bond_vec(spos[s], spos[j], g, d);
+    const double* raw = bo + 8 * e;
+    const double bpi = raw[1], bpp = raw[2], bp = raw[3];
+    const double2 da = delta[s], db = delta[j];
+    // B4-B8 (as k_bond_correct) and the derivative of every factor
+    const double ea1 = exp(-p1 * da.x), eb1 = exp(-p1 * db.x);
+    const double ea2 = exp(-p2 * da.x), eb2 = exp(-p2 * db.x);
+    const double f2 = ea1 + eb1;
+    const double f3 = -inv_p2 * log(0.5 * (ea2 + eb2));
+    const double va = sval[ta], vb = sval[tb];
+    const double na = va + f2 + f3, nb = vb + f2 + f3;
+    const double f1 = 0.5 * ((va + f2) / na + (vb + f2) / nb);
+    const double bb = c.pboc4 * bp * bp;
+    const double f4 = 1.0 / (1.0 + exp(-c.pboc3 * (bb - da.y) + c.pboc5));
+    const double f5 = 1.0 / (1.0 + exp(-c.pboc3 * (bb - db.y) + c.pboc5));
+    const double A = f1 * f4 * f5;
+    const double BOs = bp * A - bpi * f1 * A - bpp * f1 * A;
+    // E1 and its partials
+    const double sp = BOs > 0.0 ? exp(q.pbe2 * log(BOs)) : 0.0;
+    const double ex = exp(q.pbe1 * (1.0 - sp));
+    const double en = -q.Ds * BOs * ex - q.Dp * bpi * f1 * A - q.Dpp * bpp * f1 * A;
+    const double e_s = -q.Ds * ex * (1.0 - q.pbe1 * q.pbe2 * sp);
+    const double c_pi = -q.Dp - e_s, c_pp = -q.Dpp - e_s;
+    const double w = c_pi * bpi + c_pp * bpp;
+    const double de_dA = e_s * bp + w * f1;
+    const double de_df1 = de_dA * f4 * f5 + w * A;
+    const double de_df4 = de_dA * f1 * f5, de_df5 = de_dA * f1 * f4;
+    const double sa2 = f3 / (na * na) + f3 / (nb * nb);
+    const double sa3 = -(va + f2) / (na * na) - (vb + f2) / (nb * nb);
+    const double df1_da = 0.5 * (sa2 * (-p1 * ea1) + sa3 * (ea2 / (ea2 + eb2)));
+    const double df1_db = 0.5 * (sa2 * (-p1 * eb1) + sa3 * (eb2 / (ea2 + eb2)));
+    const double g4 = f4 * (1.0 - f4), g5 = f5 * (1.0 - f5);
+    const double dSa = de_df1 * df1_da - de_df4 * g4 * c.pboc3;
+    const double dSb = de_df1 * df1_db - de_df5 * g5 * c.pboc3;
+    // dBO'_k/dr = BO'_k pa pb (r/r0)^pb / r, (r/r0)^pb = exp(pb (ln r - ln r0))
+    const double lr = log(r), ir = 1.0 / r;
+    double dr[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dr[k] = raw[k] * c.pa[k] * c.pb[k] * exp(c.pb[k] * (lr - c.lr0[k])) * ir;
+    const double X = (de_df4 * g4 + de_df5 * g5) * 2.0 * c.pboc3 * c.pboc4 * bp;
+    const double cA = e_s * A + X;
+    const double de_dr = cA * dr[0] + (cA + c_pi * f1 * A) * dr[1] + (cA + c_pp * f1 * A) * dr[2];
+    bde[e] = make_double4(de_dr, (dr[0] + dr[1]) + dr[2], en, dSa);
+    bde[bmir[e]] = make_double4(0.0, 0.0, 0.0, dSb);
+  }
+}
+
+// per atom row (sorted order): D_i and the row's bond energy, in row order
+__global__ void k_bond_energy_rows(int n, const int* __restrict__ brow, const double4* __restrict__ bde,
+                                   double* __restrict__ bD, double2* __restrict__ erow, long long bond_cap) {
+  pdl_wait();
+  pdl_trigger();
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double D = 0.0, E = 0.0;
+  const long long e1 = min((long long)brow[s + 1], bond_cap);
+  for (long long e = brow[s]; e < e1; ++e) {
+    const double4 v = bde[e];
+    D += v.w;
+    E += v.z;
+  }
+  bD[s] = D;
+  erow[s] = make_double2(E, 0.0);
+}
+
+// per bond (canonical entry): g = (de/dr|S + (D_i + D_j) dBO'/dr) / r, F_i += g d, F_j -= g d
+__global__ void k_bond_energy_force(const int* __restrict__ perm, const double4* __restrict__ spos, Grid g,
+                                    const int* __restrict__ bcol, const int* __restrict__ bkey,
+                                    const int* __restrict__ bown, const double4* __restrict__ bde,
+                                    const double* __restrict__ bD, unsigned long long* __restrict__ sfx,
+                                    unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
+                                    long long bond_cap, Status* st) {
+  pdl_wait();
+  pdl_trigger();
+  const long long B = st->bonds < bond_cap ? st->bonds : bond_cap;
+  bool bad = false;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
+    const int s = bown[e], j = bcol[e];
+    if (!(perm[s] < bkey[e])) continue;
+    double d[3];
+    const double r = bond_vec(spos[s], spos[j], g, d);
+    const double4 v = bde[e];
+    const double gg = (v.x + (bD[s] + bD[j]) * v.y) / r;
+    unsigned long long* f[3] = {sfx, sfy, sfz};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double c = gg * d[k];
+      bad |= !(fabs(c) < c_nb[27]);
+      const long long fv = __double2ll_rn(c * c_nb[25]);
+      atomicAdd(&f[k][s], (unsigned long long)fv);
+      atomicAdd(&f[k][j], (unsigned long long)(-fv));
+    }
+  }
+  if (bad) set_flag(st, ST_RANGE);
 }
 
 // ================================================================= export

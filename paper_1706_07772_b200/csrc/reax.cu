@@ -366,6 +366,9 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
   t.h_q = (double*)take(sizeof(double) * N);
   t.h_force = (double*)take(sizeof(double) * 3 * N);
   t.h_energy = (double*)take(sizeof(double) * 2);
+  t.bep = (BEPair*)take(sizeof(BEPair) * NTP_MAX);
+  t.bD = (double*)take(sizeof(double) * N);
+  t.bde = t.uraw;   // per-entry bond-energy terms reuse the fill buffer (dead after k_bond_rank)
   if (w) *w = t;
   return o;
 }
@@ -385,6 +388,9 @@ struct reax_ctx {
   // pinned host
   Status* h_st = nullptr;
   DevParams* h_prm = nullptr;
+  BEPair* h_bep = nullptr;   // staging of the bond-energy parameters (reax_bond_energy)
+  bool bep_valid = false;    // device copy matches h_bep
+  int bep_nt = 0;
   bool prm_valid = false;  // device copy matches *h_prm
   std::vector<double> prm_key;  // raw reax_params + cutoffs of the last successful build
   // state
@@ -734,7 +740,7 @@ void launch_finalize(reax_ctx* c, int N, double* force, double* energy, cudaStre
   Timer t(c, 5, s);
   // one energy partial per half-list row (sorted order), summed in fixed order
   launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.perm, w.sfx, w.sfy, w.sfz, force, N,
-           w.erow, w.epart, w.ticket, energy, w.st);
+           w.erow, w.epart, w.ticket, energy, 2, w.st);
   LAUNCH(c);
 }
 
@@ -823,6 +829,62 @@ reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, 
   return r;
 }
 
+// NEXT-1: bond energy E1 and its forces at the bond set of the last
+// reax_bond_orders / reax_step (reading 28)
+reax_status do_bond_energy(reax_ctx* c, const reax_params* prm, const reax_bond_params* bp, double* force,
+                           double* energy, cudaStream_t s) {
+  if (!c || !prm || !bp || !energy) return REAX_ERR_ARG;
+  if (!c->bound || !c->lists_ok || !c->bonds_ok) return REAX_ERR_STATE;
+  if (c->n > 0 && !force) return REAX_ERR_ARG;
+  const int nt = prm->ntypes;
+  if (nt < 1 || nt > REAX_MAX_TYPES || !prm->De || !bp->De_pi || !bp->De_pipi || !bp->p_be1 || !bp->p_be2)
+    return REAX_ERR_PARAM;
+  const double* tab[5] = {prm->De, bp->De_pi, bp->De_pipi, bp->p_be1, bp->p_be2};
+  for (int k = 0; k < 5; ++k)
+    for (int t = 0; t < nt * nt; ++t) {
+      const double v = tab[k][t];
+      if (!std::isfinite(v) || v != tab[k][(t % nt) * nt + t / nt]) return REAX_ERR_PARAM;   // finite, symmetric
+      if (k == 4 && !(v > 0.0)) return REAX_ERR_PARAM;                                    // BOs^p_be2: p_be2 > 0
+    }
+  reax_status r = upload_params(c, prm, &c->cut, s);
+  if (r != REAX_OK) return r;
+  if (c->n == 0) {
+    if (cudaError_t e_ = cudaMemsetAsync(energy, 0, sizeof(double), s)) return fail_cuda(e_);
+    return REAX_OK;
+  }
+  WS& w = c->w;
+  bool same = c->bep_valid && c->bep_nt == nt;
+  for (int t = 0; same && t < nt * nt; ++t) {
+    const BEPair v{prm->De[t], bp->De_pi[t], bp->De_pipi[t], bp->p_be1[t], bp->p_be2[t]};
+    same = memcmp(&v, &c->h_bep[t], sizeof(BEPair)) == 0;
+  }
+  if (!same) {   // the pinned staging is only rewritten when the table changes (it may back an in-flight copy)
+    if (c->bep_valid && cudaStreamSynchronize(s) != cudaSuccess) return fail_cuda(cudaGetLastError());
+    for (int t = 0; t < nt * nt; ++t) c->h_bep[t] = BEPair{prm->De[t], bp->De_pi[t], bp->De_pipi[t], bp->p_be1[t], bp->p_be2[t]};
+    if (cudaError_t e_ = cudaMemcpyAsync(w.bep, c->h_bep, sizeof(BEPair) * nt * nt, cudaMemcpyHostToDevice, s))
+      return fail_cuda(e_);
+    c->bep_valid = true;
+    c->bep_nt = nt;
+  }
+  const int N = (int)c->n;
+  {
+    Timer t(c, 6, s);
+    launch_k(c, k_bond_energy_terms, 148 * 8, TPB, 0, s, w.perm, w.stype, w.spos, c->g, w.prm, w.bep, w.bcol, w.bkey,
+             w.bown, w.bmir, w.bo, w.delta, w.bde, c->cap.bond_cap, w.st);
+    LAUNCH(c);
+    launch_k(c, k_bond_energy_rows, nblk(N, TPB), TPB, 0, s, N, w.brow, w.bde, w.bD, w.erow, c->cap.bond_cap);
+    LAUNCH(c);
+    launch_k(c, k_bond_energy_force, 148 * 8, TPB, 0, s, w.perm, w.spos, c->g, w.bcol, w.bkey, w.bown, w.bde, w.bD,
+             w.sfx, w.sfy, w.sfz, c->cap.bond_cap, w.st);
+    LAUNCH(c);
+    launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.perm, w.sfx, w.sfy, w.sfz, force, N,
+             w.erow, w.epart, w.ticket, energy, 1, w.st);
+    LAUNCH(c);
+  }
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  return read_status(c, s, !c->async);
+}
+
 }  // namespace
 
 // ==================================================================== ABI
@@ -858,7 +920,9 @@ reax_status reax_create(reax_ctx** out) {
   if (ensure_tables() != cudaSuccess) return REAX_ERR_CUDA;
   reax_ctx* c = new reax_ctx();
   if (cudaHostAlloc((void**)&c->h_st, sizeof(Status), cudaHostAllocDefault) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->h_prm, sizeof(DevParams), cudaHostAllocDefault) != cudaSuccess) {
+      cudaHostAlloc((void**)&c->h_prm, sizeof(DevParams), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->h_bep, sizeof(BEPair) * NTP_MAX, cudaHostAllocDefault) != cudaSuccess) {
+    if (c->h_prm) cudaFreeHost(c->h_prm);
     if (c->h_st) cudaFreeHost(c->h_st);
     delete c;
     return REAX_ERR_CUDA;
@@ -885,6 +949,7 @@ reax_status reax_destroy(reax_ctx* c) {
     }
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_prm) cudaFreeHost(c->h_prm);
+  if (c->h_bep) cudaFreeHost(c->h_bep);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -941,6 +1006,7 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   if (const char* e = getenv("REAX_NBR_SPLIT")) ctx->nsplit_nbr = std::max(1, std::min(MAX_SPLIT, atoi(e)));
   ctx->cut = *cut;
   ctx->prm_valid = false;
+  ctx->bep_valid = false;
   ctx->lists_ok = ctx->bonds_ok = false;
   // zero the counters that kernels keep self-cleaning
   cudaError_t e = cudaMemset(ctx->w.cell_cnt, 0, sizeof(int) * (g.ncell + 1));
@@ -973,6 +1039,11 @@ reax_status reax_build_lists(reax_ctx* ctx, int64_t n, const double* pos, const 
 
 reax_status reax_bond_orders(reax_ctx* ctx, const reax_params* params, const reax_cutoffs* cut, void* stream) {
   return do_bond_orders(ctx, params, cut, (cudaStream_t)stream);
+}
+
+reax_status reax_bond_energy(reax_ctx* ctx, const reax_params* params, const reax_bond_params* bond_params,
+                             double* force, double* energy, void* stream) {
+  return do_bond_energy(ctx, params, bond_params, force, energy, (cudaStream_t)stream);
 }
 
 reax_status reax_nonbonded(reax_ctx* ctx, int64_t n, const double* pos, const int32_t* type, const double* q,
