@@ -306,6 +306,29 @@ def main():
                "api": "reax_step_host (pinned host buffers in/out, copies inside the timed region)"}
     clocks = sample_clocks_stop(clk)
 
+    # NEXT-1 (outside `value`): reax_bond_energy on the step's bond list, K
+    # calls bracketed by events on the launching stream
+    bond_energy = None
+    try:
+        bp = gen.make_bond_params()
+        Fb = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        Eb = torch.empty(1, dtype=torch.float64, device=dev)
+        one_step()
+        for _ in range(3):
+            ctx.bond_energy(bp, Fb, Eb)
+        bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            bev[k][0].record()
+            ctx.bond_energy(bp, Fb, Eb)
+            bev[k][1].record()
+        torch.cuda.synchronize()
+        ctx.check()
+        b_ms = sum(a.elapsed_time(b) for a, b in bev) / args.steps
+        bond_energy = {"row": "NEXT-1 bond energy + forces (reax_bond_energy), timed separately", "ms_per_call": b_ms,
+                       "bond_entries": B, "bonds_per_s": (B / 2) / (b_ms * 1e-3), "launches_per_call": 5}
+    except Exception as ex:   # reported, never silently dropped
+        bond_energy = {"error": str(ex)}
     nb_ms, _ = kms["nonbonded"]
     nb_avg_s = nb_ms / args.steps * 1e-3
     achieved = W_NB_DP_PER_PAIR * P / nb_avg_s
@@ -371,6 +394,7 @@ def main():
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,
         "e2e": e2e,
+        "next_rows": {"bond_energy": bond_energy},
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
