@@ -1312,19 +1312,21 @@ struct NBSmem {
   int rlen0[NB_MAX_ROWS];        // row lengths in home order (ranking input)
   int order[NB_MAX_ROWS];        // row window slots, longest row first
   int rlen[NB_MAX_ROWS];         // their lengths
+  int next_row;                  // dynamic row counter
 };
 
 // One CTA per (home block, split) (Alg. 2, re-designed): a
 // warp streams the half-list entries of its rows 32 at a time (lanes over
 // j), with the next chunk's entries, slot info and positions in flight while
-// the current chunk is evaluated.  Rows are ranked longest first and dealt to
-// the warps in snake order (w, 2W-1-w, 2W+w, ...).  F_i stays in registers
-// and is warp-reduced once per row; F_j is accumulated in a shared-memory
-// fixed-point window (the block's private force array, the GPU form of the
-// paper's thread-private tprivForce) and flushed to the global int64 sorted
-// force array once per CTA.  Energies: per-lane sums in a fixed pair order,
-// one partial per warp, reduced later in fixed order.  Forces and energies
-// are bitwise reproducible.
+// the current chunk is evaluated — across row boundaries too (the last chunk
+// of a row loads the next row's first chunk).  Rows are ranked longest first
+// and taken dynamically by the warps (the CTA's rows finish together).  F_i
+// stays in registers and is warp-reduced once per row; F_j is accumulated in
+// a shared-memory fixed-point window (the block's private force array, the
+// GPU form of the paper's thread-private tprivForce) and flushed to the
+// global int64 sorted force array once per CTA.  Energies: per-lane sums in
+// the row's pair order, one partial per row, reduced later in fixed order.
+// Forces and energies are bitwise reproducible.
 __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const int* __restrict__ cell_start,
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
@@ -1389,7 +1391,10 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     uint4* z = reinterpret_cast<uint4*>(fa);          // fa and fb are contiguous: 6 window_cap words
     for (int t = threadIdx.x; t < (6 * window_cap) / 4; t += blockDim.x) z[t] = make_uint4(0u, 0u, 0u, 0u);
   }
-  if (threadIdx.x == 0) S.bad = 0;
+  if (threadIdx.x == 0) {
+    S.bad = 0;
+    S.next_row = 0;
+  }
   __syncthreads();
   // phase 2: slot info (flattened over slots: the type loads are independent),
   // row ranking (longest first; ties by home order)
@@ -1420,8 +1425,12 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   // per-warp double buffer of row entries in shared memory: row k+1 is
   // copied (cp.async) while row k is evaluated
   uint16_t* rb = rbuf + warp * 2 * rb_cap;
-  auto row_info = [&](int kr, int& si, int& len) -> bool {
-    const int r = kr * NB_WARPS + ((kr & 1) ? NB_WARPS - 1 - warp : warp);
+  // rows are taken dynamically, longest first (per-row energy partials make
+  // the result independent of which warp runs a row)
+  auto row_info = [&](int& si, int& len) -> bool {
+    int r = 0;
+    if (lane == 0) r = atomicAdd(&S.next_row, 1);
+    r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= nrows) return false;
     if (r < nsorted) {
       si = S.order[r];
@@ -1442,24 +1451,33 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     asm volatile("cp.async.commit_group;");
   };
   int si_n = 0, len_n = 0;
-  bool have_n = row_info(0, si_n, len_n);
+  bool have_n = row_info(si_n, len_n);
   if (have_n) row_fetch(si_n, len_n, rb);
+  // the chunk in flight: (slot, slot info, position) per lane; across a row
+  // boundary it holds the next row's first chunk (pre)
+  int slot = 0;
+  int2 inf = make_int2(0, 0);
+  double4 xj = make_double4(0.0, 0.0, 0.0, 0.0);
+  bool pre = false;
   for (int kr = 0; have_n; ++kr) {
     const int si = si_n, len = len_n;
     const uint16_t* row = rb + (kr & 1) * rb_cap;
-    have_n = row_info(kr + 1, si_n, len_n);
+    have_n = row_info(si_n, len_n);
     if (have_n) row_fetch(si_n, len_n, rb + ((kr + 1) & 1) * rb_cap);
     else asm volatile("cp.async.commit_group;");
     const int2 ii = sinfo[si];
     const double4 xi = spos[ii.x];
     const NBPair* pci = pc + (ii.y >> 8) * nt;
     const double cqi = C * xi.w;
-    asm volatile("cp.async.wait_group 1;" ::: "memory");   // this row's entries have landed
-    __syncwarp();
+    if (!pre) {
+      asm volatile("cp.async.wait_group 1;" ::: "memory");   // this row's entries have landed
+      __syncwarp();
+      slot = lane < len ? (int)row[lane] : si;
+      inf = sinfo[slot];
+      xj = spos[inf.x];
+    }
+    pre = false;
     double fix = 0.0, fiy = 0.0, fiz = 0.0, ev_acc = 0.0, ec_acc = 0.0;
-    int slot = lane < len ? (int)row[lane] : si;
-    int2 inf = sinfo[slot];
-    double4 xj = spos[inf.x];
     for (int e0 = 0; e0 < len; e0 += 32) {
       const int cslot = slot;
       const int2 cinf = inf;
@@ -1469,6 +1487,14 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
         slot = e0 + 32 + lane < len ? (int)row[e0 + 32 + lane] : si;
         inf = sinfo[slot];
         xj = spos[inf.x];
+      } else if (have_n) {   // last chunk: the next row's first chunk in flight
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        const uint16_t* nrow = rb + ((kr + 1) & 1) * rb_cap;
+        slot = lane < len_n ? (int)nrow[lane] : si_n;
+        inf = sinfo[slot];
+        xj = spos[inf.x];
+        pre = true;
       }
       double dx = cxj.x - xi.x, dy = cxj.y - xi.y, dz = cxj.z - xi.z;
       if (has_shift) {   // block-uniform
