@@ -412,7 +412,16 @@ struct reax_ctx {
   int nsplit = 1;
   int nsplit_nbr = 1;
   // fork/join of reax_step (bond chain beside the nonbonded kernel)
+  // reax_step_host replays one CUDA graph (copies in, step, copies out) per
+  // unchanged (host buffers, box, parameters, workspace, mode)
+  cudaGraphExec_t hg_exec = nullptr;
+  std::vector<double> hg_key;
+  const void* hg_ptr[5] = {};
+  char* hg_ws = nullptr;
+  bool hg_async = false;
+  bool hg_off = getenv("REAX_NO_HOST_GRAPH") != nullptr;
   cudaStream_t side = nullptr;
+  cudaStream_t cap_s = nullptr;   // capture stream of the reax_step_host graph
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool serial = getenv("REAX_SERIAL") != nullptr;
   bool pdl = getenv("REAX_NO_PDL") == nullptr;   // programmatic dependent launch on the hot path
@@ -517,12 +526,20 @@ cudaError_t scan(reax_ctx* c, const TI* in, int64_t n, TO* out, cudaStream_t s) 
   return cudaGetLastError();
 }
 
+reax_status interpret_status(reax_ctx* c, cudaStream_t s);
+
 reax_status read_status(reax_ctx* c, cudaStream_t s, bool sync) {
   cudaError_t e = cudaMemcpyAsync(c->h_st, c->w.st, sizeof(Status), cudaMemcpyDeviceToHost, s);
   if (e != cudaSuccess) return fail_cuda(e);
   if (!sync) return REAX_OK;
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return fail_cuda(e);
+  return interpret_status(c, s);
+}
+
+// the status block read back into h_st (stream synchronised): OK, or the
+// error it latched (the device copy is cleared for the next call)
+reax_status interpret_status(reax_ctx* c, cudaStream_t s) {
   int f = c->h_st->flags;
   if (f == 0) return REAX_OK;
   if (f & (ST_ROW_OVF | ST_CAND_OVF | ST_BOND_OVF | ST_WIN_OVF)) {
@@ -929,6 +946,7 @@ reax_status reax_create(reax_ctx** out) {
   }
   memset(c->h_st, 0, sizeof(Status));
   bool ok = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->cap_s, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) == cudaSuccess;
   if (!ok) {
@@ -950,7 +968,9 @@ reax_status reax_destroy(reax_ctx* c) {
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_prm) cudaFreeHost(c->h_prm);
   if (c->h_bep) cudaFreeHost(c->h_bep);
+  if (c->hg_exec) cudaGraphExecDestroy(c->hg_exec);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->cap_s) cudaStreamDestroy(c->cap_s);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
@@ -1062,6 +1082,24 @@ reax_status reax_step(reax_ctx* ctx, int64_t n, const double* pos, const int32_t
   return r;
 }
 
+// copies in, reax_step, copies out (no synchronisation)
+reax_status step_host_enqueue(reax_ctx* ctx, int64_t n, const double* pos, const int32_t* type, const double* q,
+                              const double box[3], const reax_params* params, const reax_cutoffs* cut, double* force,
+                              cudaStream_t s) {
+  WS& w = ctx->w;
+  if (n > 0) {
+    if (cudaMemcpyAsync(w.h_pos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(w.h_type, type, sizeof(int) * n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(w.h_q, q, sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return fail_cuda(cudaGetLastError());
+  }
+  reax_status r = reax_step(ctx, n, w.h_pos, w.h_type, w.h_q, box, params, cut, w.h_force, w.h_energy, s);
+  if (r != REAX_OK) return r;
+  if (n > 0 && cudaMemcpyAsync(force, w.h_force, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return fail_cuda(cudaGetLastError());
+  return REAX_OK;
+}
+
 reax_status reax_step_host(reax_ctx* ctx, int64_t n, const double* pos, const int32_t* type, const double* q,
                            const double box[3], const reax_params* params, const reax_cutoffs* cut, double* force,
                            double* energy, void* stream) {
@@ -1071,19 +1109,56 @@ reax_status reax_step_host(reax_ctx* ctx, int64_t n, const double* pos, const in
   if (!energy || (n > 0 && (!pos || !type || !q || !force))) return REAX_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   WS& w = ctx->w;
-  if (n > 0) {
-    if (cudaMemcpyAsync(w.h_pos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(w.h_type, type, sizeof(int) * n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(w.h_q, q, sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
-      return REAX_ERR_CUDA;
+  std::vector<double> key;
+  const bool keyed = n > 0 && !ctx->hg_off && box && params_key(params, cut, key);
+  if (keyed) key.insert(key.end(), box, box + 3);
+  const void* ptr[5] = {pos, type, q, force, energy};
+  if (keyed && ctx->hg_exec && key == ctx->hg_key && memcmp(ptr, ctx->hg_ptr, sizeof(ptr)) == 0 &&
+      ctx->hg_ws == ctx->ws_base && ctx->hg_async == ctx->async) {
+    // replay: H2D copies, the whole step (side-stream fork included), D2H copies
+    if (cudaError_t e_ = cudaGraphLaunch(ctx->hg_exec, s)) return fail_cuda(e_);
+    if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
+    return ctx->async ? REAX_OK : interpret_status(ctx, s);
   }
-  reax_status r = reax_step(ctx, n, w.h_pos, w.h_type, w.h_q, box, params, cut, w.h_force, w.h_energy, stream);
+  // direct path (validates, sizes, reports errors); then capture the same
+  // sequence for the next calls with these buffers
+  reax_status r = step_host_enqueue(ctx, n, pos, type, q, box, params, cut, force, s);
   if (r != REAX_OK) return r;
-  if (n > 0 && cudaMemcpyAsync(force, w.h_force, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    return REAX_ERR_CUDA;
   if (cudaMemcpyAsync(energy, w.h_energy, sizeof(double) * 2, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    return REAX_ERR_CUDA;
+    return fail_cuda(cudaGetLastError());
   if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
+  if (!keyed) return REAX_OK;
+  if (ctx->hg_exec) {
+    cudaGraphExecDestroy(ctx->hg_exec);
+    ctx->hg_exec = nullptr;
+  }
+  const bool was_async = ctx->async;
+  ctx->async = true;   // no host synchronisation inside the captured step
+  // captured on the context's own stream (the caller's may be the legacy
+  // stream, which cannot be captured); replays are launched on the caller's.
+  // The status block copy-back (read_status) is part of the captured step.
+  cudaGraph_t graph = nullptr;
+  cudaStream_t hs = ctx->cap_s;
+  bool ok = cudaStreamBeginCapture(hs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    r = step_host_enqueue(ctx, n, pos, type, q, box, params, cut, force, hs);
+    ok = r == REAX_OK &&
+         cudaMemcpyAsync(energy, w.h_energy, sizeof(double) * 2, cudaMemcpyDeviceToHost, hs) == cudaSuccess;
+    ok = (cudaStreamEndCapture(hs, &graph) == cudaSuccess) && ok && graph;
+  }
+  ctx->async = was_async;
+  if (ok) ok = cudaGraphInstantiate(&ctx->hg_exec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  if (!ok) {   // not capturable here: keep the direct path
+    ctx->hg_exec = nullptr;
+    ctx->hg_off = true;
+    cudaGetLastError();
+    return REAX_OK;
+  }
+  ctx->hg_key.swap(key);
+  memcpy(ctx->hg_ptr, ptr, sizeof(ptr));
+  ctx->hg_ws = ctx->ws_base;
+  ctx->hg_async = was_async;
   return REAX_OK;
 }
 
