@@ -82,6 +82,24 @@ def sample_clocks_stop(p):
             "reasons": sorted(reasons)}
 
 
+def max_over_ranks(vals, world, device):
+    """Element-wise max over the ranks (a multi-GPU job takes as long as its
+    slowest rank; timings are device-measured per rank, never wall clock)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def replica_throughput(n_atoms, steps, world, max_ms):
+    """Whole-job atom-steps/s of `world` independent replicas (weak scaling,
+    DESIGN.md "Multi-GPU": replicas only): every rank evaluates n_atoms per
+    step; the job time is the slowest rank's."""
+    return n_atoms * steps * world / (max_ms * 1e-3)
+
+
 def run_cpu_oracle(k, evals):
     import gen
     import oracle
@@ -273,12 +291,8 @@ def main():
     ctx.check()
     pass2_ms = sum(a.elapsed_time(b) for a, b in ev2) / args.steps
     kms = {name: (kms_acc[name], args.steps) for name in kms_acc}
-    tot_ms = sum(step_ms)
-    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    tot_ms_max = float(t.item())
-    value = n * args.steps * world / (tot_ms_max * 1e-3)
+    tot_ms_max = max_over_ranks([sum(step_ms)], world, dev)[0]
+    value = replica_throughput(n, args.steps, world, tot_ms_max)
 
     e2e = None
     if not args.no_e2e:
@@ -297,10 +311,8 @@ def main():
             eev[k][1].record()
         torch.cuda.synchronize()
         e_ms = sum(a.elapsed_time(b) for a, b in eev)
-        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n * args.steps * world / (float(te.item()) * 1e-3), "unit": "atom-steps/s",
+        e_ms_max = max_over_ranks([e_ms], world, dev)[0]
+        e2e = {"value": replica_throughput(n, args.steps, world, e_ms_max), "unit": "atom-steps/s",
                "h2d_bytes_per_step": hp.numel() * 8 + ht.numel() * 4 + hq.numel() * 8,
                "d2h_bytes_per_step": hF.numel() * 8 + hE.numel() * 8,
                "api": "reax_step_host (pinned host buffers in/out, copies inside the timed region)"}
