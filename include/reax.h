@@ -52,7 +52,9 @@ typedef enum {
   REAX_ERR_BOX = 2,       /* a box length not finite or not > 2 r_nonb */
   REAX_ERR_CUTOFF = 3,    /* r_bond > r_nonb, r <= 0, or bo_cut not in (0,1) */
   REAX_ERR_PARAM = 4,     /* non-finite or out-of-domain parameter */
-  REAX_ERR_CAPACITY = 5,  /* workspace too small; see reax_required() */
+  REAX_ERR_CAPACITY = 5,  /* workspace too small; see reax_required().  Also, with
+                             no regrow that clears it, when one home block's neighbour window
+                             exceeds the per-CTA shared memory (~3x the PETN density) */
   REAX_ERR_NONFINITE = 6, /* NaN/Inf in positions, charges or computed energies */
   REAX_ERR_CUDA = 7,      /* a CUDA runtime error */
   REAX_ERR_STATE = 8,     /* call order / binding violated (no workspace, stale lists) */

@@ -297,7 +297,7 @@ void resolve_caps(int64_t n, const double box[3], const reax_cutoffs* cut, const
   double rho = vol > 0 ? (double)n / vol : 0.0;
   double R = cut->r_nonb;
   double mean = 2.0 * M_PI / 3.0 * rho * R * R * R;
-  int rc = (int)std::ceil(2.0 * mean + 96.0);
+  int rc = (int)std::ceil(1.3 * mean + 96.0);   // rows: about mean +- 5 sigma plus the own-cell part; overflow regrows
   rc = (rc + 31) / 32 * 32;
   c.row_cap = in->row_cap > 0 ? in->row_cap : std::min(rc, 65535);
   c.row_cap = std::min((c.row_cap + 7) & ~7, 65528);   // 16-byte rows (asynchronous row copies)
@@ -389,6 +389,7 @@ struct reax_ctx {
   Status* h_st = nullptr;
   DevParams* h_prm = nullptr;
   BEPair* h_bep = nullptr;   // staging of the bond-energy parameters (reax_bond_energy)
+  size_t maxsm = 0;          // opt-in shared memory per block (bound device)
   bool bep_valid = false;    // device copy matches h_bep
   int bep_nt = 0;
   bool prm_valid = false;  // device copy matches *h_prm
@@ -582,9 +583,14 @@ bool params_key(const reax_params* p, const reax_cutoffs* cut, std::vector<doubl
   return true;
 }
 
+size_t nb_smem(int wcap, int row_cap, int nt);
+
 reax_status upload_params(reax_ctx* c, const reax_params* p, const reax_cutoffs* cut, cudaStream_t s) {
   std::vector<double> key;
   if (!params_key(p, cut, key)) return p ? REAX_ERR_PARAM : REAX_ERR_ARG;
+  // the nonbonded kernel's shared memory with this table's nt (bind checked
+  // nt = 1): windows denser than that are unsupported (REAX_ERR_CAPACITY)
+  if (nb_smem(c->cap.window_cap, c->cap.row_cap, p->ntypes) + sizeof(NBSmem) > c->maxsm) return REAX_ERR_CAPACITY;
   if (c->prm_valid && key.size() == c->prm_key.size() &&
       memcmp(key.data(), c->prm_key.data(), key.size() * sizeof(double)) == 0)
     return REAX_OK;
@@ -607,7 +613,7 @@ size_t nbr_smem(int wcap, int row_cap = 0) {
   (void)row_cap;
   return (size_t)(wcap + 32) * (sizeof(float4) + sizeof(int) + 1) + 64;
 }
-size_t nb_smem(int wcap, int row_cap, int nt = NT_MAX) {
+size_t nb_smem(int wcap, int row_cap, int nt) {
   return sizeof(double) * (EXP_TBL + 2 * LOG_TBL) + sizeof(NBPair) * nt * nt + (size_t)wcap * (sizeof(int2) + 6 * sizeof(int) + 1) +
          16 + (size_t)NB_WARPS * 2 * ((row_cap + 7) & ~7) * sizeof(uint16_t) + 64;
 }
@@ -1008,13 +1014,18 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  size_t s1 = nbr_smem(c.window_cap, c.row_cap) + sizeof(NbrSmem), s2 = nb_smem(c.window_cap, c.row_cap) + sizeof(NBSmem);
+  // shared memory of the window kernels: the nonbonded kernel's also holds
+  // the nt*nt pair table, checked with the real nt when parameters arrive
+  // (upload_params); here with nt = 1
+  size_t s1 = nbr_smem(c.window_cap, c.row_cap) + sizeof(NbrSmem), s2 = nb_smem(c.window_cap, c.row_cap, 1) + sizeof(NBSmem);
   if ((size_t)maxsm < s1 || (size_t)maxsm < s2) return REAX_ERR_CAPACITY;
+  size_t nb_attr = std::min<size_t>(nb_smem(c.window_cap, c.row_cap, NT_MAX), (size_t)maxsm - sizeof(NBSmem));
   if (ensure_smem(k_nbr_build, nbr_smem(c.window_cap, c.row_cap)) != cudaSuccess ||
-      ensure_smem(k_nonbonded, nb_smem(c.window_cap, c.row_cap)) != cudaSuccess ||
+      ensure_smem(k_nonbonded, nb_attr) != cudaSuccess ||
       ensure_smem(k_export_pairs, exp_smem(c.window_cap)) != cudaSuccess)
     return REAX_ERR_CUDA;
 
+  ctx->maxsm = (size_t)maxsm;
   ctx->ws_base = (char*)ws;
   ctx->ws_bytes = bytes;
   layout(n, g, c, ctx->ws_base, &ctx->w);

@@ -241,10 +241,10 @@ def test_step_host_graph_replay(params):
 
 
 def test_dense_system_regrows(params):
-    """2.7x the PETN density (0.25 atoms/A^3, RSA with the 0.9 A minimum
-    separation): rows of ~1050 entries, windows of ~5400 atoms and more bond
-    candidates than the defaults hold — every capacity regrows and the result
-    is still exact against the oracle."""
+    """2.6x the PETN density (0.25 atoms/A^3, RSA with the 0.9 A minimum
+    separation): rows of ~520 entries and windows of ~5400 atoms, beyond the
+    default window capacity (it regrows; the nonbonded kernel's shared memory
+    still fits) — the result is still exact against the oracle."""
     s = gen.make_system(2662, (22.0, 22.0, 22.0), gen.SEED_BASE + 321)
     ctx, _, _, _ = full_parity(s, params)
-    assert ctx.cap.row_cap > 1000 and ctx.cap.window_cap > 2048
+    assert ctx.cap.row_cap > 512 and ctx.cap.window_cap > 2048
