@@ -6,9 +6,6 @@
 namespace rx {
 
 __constant__ WindowTables c_win;
-#ifdef NB_EXP_PROF
-__device__ unsigned long long g_nbprof[16 * 8192];   // experiments: per-CTA phase timestamps
-#endif
 
 __device__ __forceinline__ void set_flag(Status* st, int f) { atomicOr(&st->flags, f); }
 
@@ -383,16 +380,6 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
   return W.slot[nwu];
 }
 
-// window cell holding slot t: largest k with W.slot[k] <= t (binary search)
-__device__ __forceinline__ int cell_of_slot(const WinSmem& W, int nwu, int t) {
-  int lo = 0, hi = nwu - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (W.slot[mid] <= t) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
 // rows of the block: home sub-cell h, slot range [slot[home_k[h]], slot[home_k[h]+1])
 __device__ __forceinline__ bool row_of(const WinSmem& W, int r, int& h, int& si) {
   for (h = 0; h < NHOME; ++h) {
@@ -454,136 +441,6 @@ struct SlotJK {
   __device__ __forceinline__ int J(int t) const { return j[t]; }
   __device__ __forceinline__ int K(int t) const { return k[t]; }
 };
-struct SlotInfo {
-  const int2* s;
-  __device__ __forceinline__ int J(int t) const { return s[t].x; }
-  __device__ __forceinline__ int K(int t) const { return s[t].y & 255; }
-};
-
-// One row's half-list candidate test (one warp; Write Lists).
-// The candidate stream of row i (window slot si, home sub-cell h) is the
-// concatenation of intervals, one per lane: the forward runs of its
-// sub-cell's half stencil (rows of cells along x), each trimmed to the cells
-// whose x-extent meets [x_i - w, x_i + w] with w = sqrt(R^2 - d_yz^2) (d_yz:
-// distance from atom i to the run's y-z cross-section, so no partner is ever
-// trimmed), plus its own cell after i.  Lanes walk the stream 32 candidates
-// at a time: r^2 in fp32 against a band of +-m around R^2 (~70x the fp32
-// error bound), the band settled by the exact FMA-free fp64 test (bit-
-// identical to the oracle's r^2); accepted window slots are compacted with a
-// ballot and stored coalesced to row[].  With BOND, candidates below the
-// conservative BO' = bo_cut radius are compacted the same way into crow[].
-// Returns the row length (which may exceed row_cap: the caller flags it).
-template <bool BOND, typename SI>
-__device__ __forceinline__ int nbr_row_test(const WinSmem& W, const Grid& g, int Wslots, const float4* __restrict__ cand,
-                                            SI sl, const double4* __restrict__ spos, int s, int si, int h,
-                                            const RowTest& rt, uint16_t* row, int row_cap, int* crow, int cand_cap,
-                                            const float* rc2row, float rcmax, int& nc_out) {
-  const int lane = threadIdx.x & 31;
-  const unsigned lt_mask = (1u << lane) - 1u, le_mask = lt_mask | (1u << lane);
-  const float4 ri = cand[si];
-  const int kh = c_win.home_k[h];
-  // ---- intervals: lane q < nrun trims run q, lane nrun takes the own cell
-  const int nrun = c_win.nrun1[h];
-  int ia = 0, il = 0;
-  if (lane < nrun) {
-    const int ka = c_win.run1_a[h][lane], kb = c_win.run1_b[h][lane];
-    const int wba = c_win.wu[ka];
-    const int wxa = wba % WB - SR;                   // x cell offset (block frame) of the run's first cell
-    const float oy = (float)((wba / WB % WB - SR) * g.h[1]);
-    const float oz = (float)((wba / (WB * WB) - SR) * g.h[2]);
-    const float dy = fmaxf(0.f, fmaxf(oy - ri.y, ri.y - (oy + rt.hy)));
-    const float dz = fmaxf(0.f, fmaxf(oz - ri.z, ri.z - (oz + rt.hz)));
-    const float w2 = rt.Rt * rt.Rt - (dy * dy + dz * dz);
-    if (w2 >= 0.f) {
-      const float w = sqrtf(w2) + 1e-3f;
-      // cells c (block frame) with [c hx, (c+1) hx] meeting [x - w, x + w]
-      const int c0 = max(wxa, (int)floorf((ri.x - w) * rt.ihx));
-      const int c1 = min(wxa + (kb - ka), (int)floorf((ri.x + w) * rt.ihx));
-      if (c0 <= c1) {
-        // the run's atoms are x-sorted (cells along x, atoms by x within a
-        // cell): cut [ta, tb) to x in [x_i - w, x_i + w] by binary search
-        int lo = W.slot[ka + (c0 - wxa)], hi = W.slot[ka + (c1 - wxa) + 1];
-        const float xlo = ri.x - w, xhi = ri.x + w;
-        int l = lo, u = hi;
-        while (l < u) {
-          const int mid = (l + u) >> 1;
-          if (cand[mid].x < xlo) l = mid + 1; else u = mid;
-        }
-        int l2 = l, u2 = hi;
-        while (l2 < u2) {
-          const int mid = (l2 + u2) >> 1;
-          if (cand[mid].x <= xhi) l2 = mid + 1; else u2 = mid;
-        }
-        ia = l;
-        il = l2 - l;
-      }
-    }
-  } else if (lane == nrun) {
-    ia = si + 1;
-    il = W.slot[kh + 1] - ia;
-  }
-  // compact the non-empty intervals, then exclusive offsets
-  const unsigned ne = __ballot_sync(0xffffffffu, il > 0);
-  int inc = il;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  const int total = __shfl_sync(0xffffffffu, inc, 31);
-  const int start_q = inc - il;                       // stream position where my interval starts
-  // compacted interval table: lane t holds the t-th non-empty interval's
-  // (start position, slot - position shift); intervals keep their order
-  const unsigned src = __fns(ne, 0, lane + 1);      // lane of the (lane+1)-th set bit
-  const int srcl = src < 32 ? (int)src : 0;
-  const int cstart = __shfl_sync(0xffffffffu, start_q, srcl);
-  const int cshift = __shfl_sync(0xffffffffu, ia - start_q, srcl);
-  const int nint = __popc(ne);
-  int len = 0, nc = 0;
-  for (int p0 = 0; p0 < total; p0 += 32) {
-    // interval of each lane: the intervals starting inside this chunk mark
-    // their start position; lane l belongs to the latest start <= p0 + l
-    const int rel = cstart - p0;
-    const bool here = lane < nint && rel >= 0 && rel < 32;
-    const unsigned M = __reduce_or_sync(0xffffffffu, here ? (1u << rel) : 0u);
-    const int before = __popc(__ballot_sync(0xffffffffu, lane < nint && rel < 0));
-    const int q = before + __popc(M & le_mask) - 1;
-    const int p = p0 + lane;
-    const int slot = p + __shfl_sync(0xffffffffu, cshift, q);
-    const bool valid = p < total;
-    const float4 c = cand[valid ? slot : Wslots];   // Wslots: sentinel
-    const float dx = c.x - ri.x, dy = c.y - ri.y, dz = c.z - ri.z;
-    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    bool in = r2 < rt.R2lo;
-    const bool band = fabsf(r2 - rt.R2mid) <= rt.R2half && !in;
-    if (__any_sync(0xffffffffu, band)) {
-      if (band) {  // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
-        const double4 xi = spos[s];
-        const double4 xj = spos[sl.J(slot)];
-        const double4 sh = W.shift[sl.K(slot)];
-        const double ex = __dadd_rn(__dsub_rn(xj.x, xi.x), sh.x);
-        const double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), sh.y);
-        const double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), sh.z);
-        const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
-        in = d2 <= rt.R2;
-      }
-    }
-    const unsigned mk = __ballot_sync(0xffffffffu, in);
-    const int pp = len + __popc(mk & lt_mask);
-    if (in && pp < row_cap) row[pp] = (uint16_t)slot;
-    len += __popc(mk);
-    if (BOND) {
-      if (__any_sync(0xffffffffu, in && r2 <= rcmax)) {  // rare: ~3 bond candidates per row
-        const bool bcand = in && r2 <= rc2row[__float_as_int(c.w)];
-        const unsigned mb = __ballot_sync(0xffffffffu, bcand);
-        const int pc = nc + __popc(mb & lt_mask);
-        if (bcand && pc < cand_cap) crow[pc] = sl.J(slot);
-        nc += __popc(mb);
-      }
-    }
-  }
-  nc_out = nc;
-  return len;
-}
 
 // A group of up to NBR_G consecutive rows (atoms) of one home sub-cell,
 // tested by one warp (Write Lists).  The atoms of a cell are
@@ -759,8 +616,8 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, con
 
 // One CTA per (home block, split).  Candidates of the window are staged in
 // shared memory as fp32 coordinates relative to the block origin.  A warp
-// takes one row (atom) at a time and runs nbr_row_test on it (with bond
-// candidates).
+// takes a group of NBR_G rows of one home sub-cell at a time (dynamically)
+// and runs nbr_group_test on it (with bond candidates).
 #ifndef NBR_MINB
 #define NBR_MINB 3
 #endif
@@ -1335,10 +1192,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
-#ifdef NB_EXP_PROF
-  unsigned long long t_start = 0;
-  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-#endif
   const int blk = blk0 + blockIdx.x / nsplit, split = blockIdx.x % nsplit;   // blk0: first home block of this launch
   const int nt = prm->nt;
   double* ET = reinterpret_cast<double*>(dyn);                  // exp table
@@ -1418,10 +1271,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   const bool has_shift = S.W.has_shift != 0;
   const double FIXS = c_nb[25], MAGIC = c_nb[26], FLIM = c_nb[27];
   bool bad = false;
-#ifdef NB_EXP_PROF
-  unsigned long long t_setup = 0;
-  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_setup));
-#endif
   // per-warp double buffer of row entries in shared memory: row k+1 is
   // copied (cp.async) while row k is evaluated
   uint16_t* rb = rbuf + warp * 2 * rb_cap;
@@ -1523,13 +1372,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     __syncwarp();   // the buffer of this row is refilled two rows later
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-#ifdef NB_EXP_PROF
-  if (lane == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 4 + warp] = t;
-  }
-#endif
   if (__any_sync(0xffffffffu, bad) && lane == 0) S.bad = 1;
   __syncthreads();
   if (threadIdx.x == 0 && S.bad) set_flag(st, ST_RANGE);
@@ -1542,19 +1384,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
       if (v != 0) atomicAdd(&gf[c][j], (unsigned long long)v);
     }
   }
-#ifdef NB_EXP_PROF
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    unsigned sm;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 0] = t_start;
-    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 1] = t_setup;
-    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 2] = t;
-    g_nbprof[(blk0 * nsplit + blockIdx.x) * 16 + 3] = sm;
-  }
-#endif
 }
 
 // a8 finalize, one kernel: un-permute the forces, force[perm[s]] =

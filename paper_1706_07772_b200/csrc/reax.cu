@@ -915,11 +915,6 @@ extern "C" {
 
 const char* reax_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda); }
 
-#ifdef NB_EXP_PROF
-int reax_exp_nbprof(unsigned long long* out, int n) {   // experiments only
-  return cudaMemcpyFromSymbol(out, g_nbprof, sizeof(unsigned long long) * 16 * (size_t)n) == cudaSuccess ? 0 : 1;
-}
-#endif
 
 const char* reax_status_str(reax_status s) {
   switch (s) {
