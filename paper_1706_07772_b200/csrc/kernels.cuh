@@ -335,7 +335,17 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
   int base[3] = {bx * HB, by * HB, bz * HB};
   int nwu = c_win.nwu;
   int my_shift = 0;
+  // home sub-cells that exist (an odd cell count per axis leaves the last
+  // block partial): only the union of their half stencils is staged
+  unsigned hok = 0;
+#pragma unroll
+  for (int h = 0; h < NHOME; ++h)
+    hok |= ((base[0] + h % HB < g.nc[0]) && (base[1] + (h / HB) % HB < g.nc[1]) && (base[2] + h / (HB * HB) < g.nc[2]))
+               ? (1u << h) : 0u;
   for (int k = threadIdx.x; k < nwu; k += blockDim.x) {
+    bool need = false;
+#pragma unroll
+    for (int h = 0; h < NHOME; ++h) need |= ((hok >> h) & 1u) && ((c_win.mask[h][k >> 5] >> (k & 31)) & 1u);
     int wb = c_win.wu[k];
     int wv[3] = {wb % WB, (wb / WB) % WB, wb / (WB * WB)};
     int cc[3];
@@ -346,19 +356,15 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
       int m = u >= 0 ? u / g.nc[a] : -((-u + g.nc[a] - 1) / g.nc[a]);  // floor(u / nc)
       cc[a] = u - m * g.nc[a];
       sh[a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
-      my_shift |= (m != 0);
+      my_shift |= need && (m != 0);
     }
     W.shift[k] = make_double4(sh[0], sh[1], sh[2], 0.0);
     int cid = (cc[2] * g.nc[1] + cc[1]) * g.nc[0] + cc[0];
     int s0 = cell_start[cid];
     W.start[k] = s0;
-    W.cnt[k] = cell_start[cid + 1] - s0;
+    W.cnt[k] = need ? cell_start[cid + 1] - s0 : 0;
   }
-  if (threadIdx.x < NHOME) {
-    int h = threadIdx.x;
-    int hv[3] = {h % HB, (h / HB) % HB, h / (HB * HB)};
-    W.home_ok[h] = (base[0] + hv[0] < g.nc[0]) && (base[1] + hv[1] < g.nc[1]) && (base[2] + hv[2] < g.nc[2]);
-  }
+  if (threadIdx.x < NHOME) W.home_ok[threadIdx.x] = (hok >> threadIdx.x) & 1u;
   const int any_shift = __syncthreads_or(my_shift);
   if (threadIdx.x == 0) W.has_shift = any_shift;
   if (threadIdx.x < 32) {  // warp 0: exclusive scan over <= 216 counts
