@@ -338,7 +338,7 @@ def main():
         ctx.check()
         b_ms = sum(a.elapsed_time(b) for a, b in bev) / args.steps
         bond_energy = {"row": "NEXT-1 bond energy + forces (reax_bond_energy), timed separately", "ms_per_call": b_ms,
-                       "bond_entries": B, "bonds_per_s": (B / 2) / (b_ms * 1e-3), "launches_per_call": 5}
+                       "bond_entries": B, "bonds_per_s": (B / 2) / (b_ms * 1e-3), "launches_per_call": 3}
     except Exception as ex:   # reported, never silently dropped
         bond_energy = {"error": str(ex)}
     nb_ms, _ = kms["nonbonded"]

@@ -156,8 +156,7 @@ reax_status reax_bond_orders(reax_ctx* ctx, const reax_params* params, const rea
  * Precondition: reax_bond_orders (or reax_step) on this ctx; the parameters
  * must be those of that build.  force [dev] n*3 fp64 (overwritten, input
  * order); energy [dev] 1 fp64 {E_bond} (overwritten).  REAX_ERR_PARAM for a
- * non-finite or asymmetric table or p_be2 <= 0; REAX_ERR_RANGE if a force
- * component of one bond reaches 65536 kcal/mol/A. */
+ * non-finite or asymmetric table or p_be2 <= 0. */
 reax_status reax_bond_energy(reax_ctx* ctx, const reax_params* params, const reax_bond_params* bond_params,
                              double* force, double* energy, void* stream);
 

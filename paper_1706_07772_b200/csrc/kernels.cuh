@@ -1477,8 +1477,9 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __re
 // (f1, f4, f5), so dE/dr_b = de_b/dr_b|_S + (D_i + D_j) dBO'_b/dr_b with
 // D_i = sum_{b' at i} de_b'/dS_i, and the forces are central along the bonds.
 // Three passes: per bond (canonical entry, orientation as k_bond_correct) the
-// terms; per atom row D_i and the row's energy (fixed order); per bond the
-// force, added to the int64 fixed-point accumulators (order-free).
+// terms, written to both entries of the bond; per atom row D_i (row order);
+// per atom row the force, gathered over the row's bonds (no atomics), and
+// the energy (fixed-shape sums).
 
 // bond vector d = minimum-image(x_b - x_a) and r, exactly as k_bond_eval
 __device__ __forceinline__ double bond_vec(const double4& xa, const double4& xb, const Grid& g, double d[3]) {
@@ -1555,58 +1556,81 @@ __global__ void k_bond_energy_terms(const int* __restrict__ perm, const int* __r
     const double X = (de_df4 * g4 + de_df5 * g5) * 2.0 * c.pboc3 * c.pboc4 * bp;
     const double cA = e_s * A + X;
     const double de_dr = cA * dr[0] + (cA + c_pi * f1 * A) * dr[1] + (cA + c_pp * f1 * A) * dr[2];
-    bde[e] = make_double4(de_dr, (dr[0] + dr[1]) + dr[2], en, dSa);
-    bde[bmir[e]] = make_double4(0.0, 0.0, 0.0, dSb);
+    const double dbo_dr = (dr[0] + dr[1]) + dr[2];
+    bde[e] = make_double4(de_dr, dbo_dr, en, dSa);
+    bde[bmir[e]] = make_double4(de_dr, dbo_dr, 0.0, dSb);
   }
 }
 
-// per atom row (sorted order): D_i and the row's bond energy, in row order
+// per atom row (sorted order): D_i = sum of de/dS_i over the row, in row order
 __global__ void k_bond_energy_rows(int n, const int* __restrict__ brow, const double4* __restrict__ bde,
-                                   double* __restrict__ bD, double2* __restrict__ erow, long long bond_cap) {
+                                   double* __restrict__ bD, long long bond_cap) {
   pdl_wait();
   pdl_trigger();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
-  double D = 0.0, E = 0.0;
+  double D = 0.0;
   const long long e1 = min((long long)brow[s + 1], bond_cap);
-  for (long long e = brow[s]; e < e1; ++e) {
-    const double4 v = bde[e];
-    D += v.w;
-    E += v.z;
-  }
+  for (long long e = brow[s]; e < e1; ++e) D += bde[e].w;
   bD[s] = D;
-  erow[s] = make_double2(E, 0.0);
 }
 
-// per bond (canonical entry): g = (de/dr|S + (D_i + D_j) dBO'/dr) / r, F_i += g d, F_j -= g d
-__global__ void k_bond_energy_force(const int* __restrict__ perm, const double4* __restrict__ spos, Grid g,
-                                    const int* __restrict__ bcol, const int* __restrict__ bkey,
-                                    const int* __restrict__ bown, const double4* __restrict__ bde,
-                                    const double* __restrict__ bD, unsigned long long* __restrict__ sfx,
-                                    unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
-                                    long long bond_cap, Status* st) {
+// per atom row (sorted order), gathering: F_s = sum over its bonds of g d with
+// g = (de/dr|S + (D_s + D_j) dBO'/dr) / r and d = minimum-image(x_j - x_s)
+// (both entries of a bond give the same g), written straight to the caller's
+// input-order force array; the row's energy (its canonical entries) goes
+// into a fixed-shape block sum and the last block sums the block partials
+// (deterministic, as k_finalize)
+__global__ void __launch_bounds__(FIN_THREADS) k_bond_energy_out(int n, const int* __restrict__ perm,
+    const double4* __restrict__ spos, Grid g, const int* __restrict__ brow, const int* __restrict__ bcol,
+    const double4* __restrict__ bde, const double* __restrict__ bD, long long bond_cap, double* __restrict__ force,
+    double* __restrict__ part, unsigned* __restrict__ ticket, double* __restrict__ energy, Status* st) {
   pdl_wait();
   pdl_trigger();
-  const long long B = st->bonds < bond_cap ? st->bonds : bond_cap;
-  bool bad = false;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
-    const int s = bown[e], j = bcol[e];
-    if (!(perm[s] < bkey[e])) continue;
-    double d[3];
-    const double r = bond_vec(spos[s], spos[j], g, d);
-    const double4 v = bde[e];
-    const double gg = (v.x + (bD[s] + bD[j]) * v.y) / r;
-    unsigned long long* f[3] = {sfx, sfy, sfz};
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  double E = 0.0;
+  if (s < n) {
+    double f[3] = {0.0, 0.0, 0.0};
+    const double4 xs = spos[s];
+    const double Ds = bD[s];
+    const long long e1 = min((long long)brow[s + 1], bond_cap);
+    for (long long e = brow[s]; e < e1; ++e) {
+      const int j = bcol[e];
+      const double4 v = bde[e];
+      double d[3];
+      const double r = bond_vec(xs, spos[j], g, d);
+      const double gg = (v.x + (Ds + bD[j]) * v.y) / r;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const double c = gg * d[k];
-      bad |= !(fabs(c) < c_nb[27]);
-      const long long fv = __double2ll_rn(c * c_nb[25]);
-      atomicAdd(&f[k][s], (unsigned long long)fv);
-      atomicAdd(&f[k][j], (unsigned long long)(-fv));
+      for (int k = 0; k < 3; ++k) f[k] = fma(gg, d[k], f[k]);
+      E += v.z;
     }
+    const int i = perm[s];
+    force[3 * (int64_t)i] = f[0];
+    force[3 * (int64_t)i + 1] = f[1];
+    force[3 * (int64_t)i + 2] = f[2];
   }
-  if (bad) set_flag(st, ST_RANGE);
+  __shared__ double red[2][FIN_THREADS / 32];
+  __shared__ bool last;
+  double b = 0.0;
+  fin_block_sum(E, b, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = E;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  E = 0.0;
+  b = 0.0;
+  for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) E += __ldcg(part + 2 * k);
+  __syncthreads();   // red[] is reused
+  fin_block_sum(E, b, red);
+  if (threadIdx.x == 0) {
+    energy[0] = E;
+    *ticket = 0u;   // ready for the next call
+    if (!isfinite(E)) set_flag(st, ST_NONFINITE_OUT);
+  }
 }
 
 // ================================================================= export

@@ -895,13 +895,10 @@ reax_status do_bond_energy(reax_ctx* c, const reax_params* prm, const reax_bond_
     launch_k(c, k_bond_energy_terms, 148 * 8, TPB, 0, s, w.perm, w.stype, w.spos, c->g, w.prm, w.bep, w.bcol, w.bkey,
              w.bown, w.bmir, w.bo, w.delta, w.bde, c->cap.bond_cap, w.st);
     LAUNCH(c);
-    launch_k(c, k_bond_energy_rows, nblk(N, TPB), TPB, 0, s, N, w.brow, w.bde, w.bD, w.erow, c->cap.bond_cap);
+    launch_k(c, k_bond_energy_rows, nblk(N, TPB), TPB, 0, s, N, w.brow, w.bde, w.bD, c->cap.bond_cap);
     LAUNCH(c);
-    launch_k(c, k_bond_energy_force, 148 * 8, TPB, 0, s, w.perm, w.spos, c->g, w.bcol, w.bkey, w.bown, w.bde, w.bD,
-             w.sfx, w.sfy, w.sfz, c->cap.bond_cap, w.st);
-    LAUNCH(c);
-    launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.perm, w.sfx, w.sfy, w.sfz, force, N,
-             w.erow, w.epart, w.ticket, energy, 1, w.st);
+    launch_k(c, k_bond_energy_out, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.perm, w.spos, c->g, w.brow, w.bcol,
+             w.bde, w.bD, c->cap.bond_cap, force, w.epart, w.ticket, energy, w.st);
     LAUNCH(c);
   }
   if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
