@@ -1593,16 +1593,31 @@ __global__ void __launch_bounds__(FIN_THREADS) k_bond_energy_out(int n, const in
     double f[3] = {0.0, 0.0, 0.0};
     const double4 xs = spos[s];
     const double Ds = bD[s];
-    const long long e1 = min((long long)brow[s + 1], bond_cap);
-    for (long long e = brow[s]; e < e1; ++e) {
-      const int j = bcol[e];
-      const double4 v = bde[e];
-      double d[3];
-      const double r = bond_vec(xs, spos[j], g, d);
-      const double gg = (v.x + (Ds + bD[j]) * v.y) / r;
+    const long long e0 = brow[s], e1 = min((long long)brow[s + 1], bond_cap);
+    // the row's entries in batches of 4 with every load issued before use
+    for (long long eb = e0; eb < e1; eb += 4) {
+      int j[4];
+      double4 v[4], xj[4];
+      double Dj[4];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) f[k] = fma(gg, d[k], f[k]);
-      E += v.z;
+      for (int u = 0; u < 4; ++u) j[u] = eb + u < e1 ? bcol[eb + u] : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int jj = j[u] < 0 ? s : j[u];
+        v[u] = j[u] < 0 ? make_double4(0.0, 0.0, 0.0, 0.0) : bde[eb + u];
+        xj[u] = spos[jj];
+        Dj[u] = bD[jj];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j[u] < 0) continue;
+        double d[3];
+        const double r = bond_vec(xs, xj[u], g, d);
+        const double gg = (v[u].x + (Ds + Dj[u]) * v[u].y) / r;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) f[k] = fma(gg, d[k], f[k]);
+        E += v[u].z;
+      }
     }
     const int i = perm[s];
     force[3 * (int64_t)i] = f[0];
