@@ -625,7 +625,7 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, con
 // takes a group of NBR_G rows of one home sub-cell at a time (dynamically)
 // and runs nbr_group_test on it (with bond candidates).
 #ifndef NBR_MINB
-#define NBR_MINB 3
+#define NBR_MINB 4   // 4 CTAs x 8 warps at <= 64 registers (36 B of spills; measured faster than 3 at 80)
 #endif
 __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, const int* __restrict__ cell_start,
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
