@@ -143,6 +143,7 @@ struct WS {
   long long* exp_off;   // n + 1 (export scratch)
   unsigned long long* lb_status;  // look-back scan tile status
   unsigned* lb_ticket;            // look-back scan tile ticket
+  unsigned* bin_ticket;           // k_bin last-block ticket (fused cell scan)
   DevParams* prm;
   Status* st;
   double* h_pos;     // staging for reax_step_host

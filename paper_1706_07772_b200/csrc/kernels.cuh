@@ -208,30 +208,81 @@ __device__ __forceinline__ void clear_status(unsigned long long* status, int nti
 
 // ================================================================ a1-a2 bin
 // wrap, validate, sub-cell id, histogram
-__global__ void k_bin(int n, const double* __restrict__ pos, const int* __restrict__ type, Grid g,
+// (small grids: BIN_FUSED_SCAN_MAX cells or fewer) the last k_bin block to
+// finish turns the histogram into cell_start itself, saving the scan launch
+constexpr int BIN_FUSED_SCAN_MAX = 4096;
+__global__ void __launch_bounds__(256) k_bin(int n, const double* __restrict__ pos, const int* __restrict__ type, Grid g,
                       int nt, int* __restrict__ cell_of, int* __restrict__ cell_cnt, Status* st,
-                      unsigned long long* __restrict__ scan_status, int scan_tiles) {
+                      unsigned long long* __restrict__ scan_status, int scan_tiles, int* __restrict__ cell_start,
+                      unsigned* __restrict__ ticket) {
   pdl_wait();
   pdl_trigger();
   clear_status(scan_status, scan_tiles);
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int c[3];
-  bool bad = false;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    int c[3];
+    bool bad = false;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    double x = pos[3 * (int64_t)i + k];
-    bad |= !isfinite(x);
-    double w = isfinite(x) ? wrap_coord(x, g.L[k]) : 0.0;
-    int ck = (int)(w * g.inv_h[k]);
-    c[k] = ck >= g.nc[k] ? g.nc[k] - 1 : ck;
+    for (int k = 0; k < 3; ++k) {
+      double x = pos[3 * (int64_t)i + k];
+      bad |= !isfinite(x);
+      double w = isfinite(x) ? wrap_coord(x, g.L[k]) : 0.0;
+      int ck = (int)(w * g.inv_h[k]);
+      c[k] = ck >= g.nc[k] ? g.nc[k] - 1 : ck;
+    }
+    if (bad) set_flag(st, ST_NONFINITE_IN);
+    int t = type[i];
+    if (t < 0 || t >= nt) set_flag(st, ST_TYPE);
+    int cid = (c[2] * g.nc[1] + c[1]) * g.nc[0] + c[0];
+    cell_of[i] = cid;
+    atomicAdd(&cell_cnt[cid], 1);
   }
-  if (bad) set_flag(st, ST_NONFINITE_IN);
-  int t = type[i];
-  if (t < 0 || t >= nt) set_flag(st, ST_TYPE);
-  int cid = (c[2] * g.nc[1] + c[1]) * g.nc[0] + c[0];
-  cell_of[i] = cid;
-  atomicAdd(&cell_cnt[cid], 1);
+  if (!cell_start) return;   // separate scan
+  __shared__ bool last;
+  __shared__ int warp_sum[8];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // exclusive scan of the ncell counts by this block: thread t owns a
+  // contiguous segment of m cells (all its loads in flight at once), a block
+  // scan of the segment sums, then the segment's prefixes
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int m = (g.ncell + 255) / 256;
+  const int k0 = threadIdx.x * m;
+  constexpr int MSEG = BIN_FUSED_SCAN_MAX / 256;
+  int v[MSEG];
+  int seg = 0;
+#pragma unroll
+  for (int q = 0; q < MSEG; ++q) {
+    v[q] = (q < m && k0 + q < g.ncell) ? __ldcg(cell_cnt + k0 + q) : 0;
+    seg += v[q];
+  }
+  int x = seg;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[w] = x;
+  __syncthreads();
+  int run = x - seg;
+  for (int q = 0; q < w; ++q) run += warp_sum[q];
+  int carry = 0;
+  for (int q = 0; q < 8; ++q) carry += warp_sum[q];
+#pragma unroll
+  for (int q = 0; q < MSEG; ++q) {
+    if (q < m && k0 + q < g.ncell) cell_start[k0 + q] = run;
+    run += v[q];
+  }
+  if (threadIdx.x == 0) {
+    cell_start[g.ncell] = carry;
+    *ticket = 0u;   // ready for the next call
+  }
 }
 
 // counting-sort scatter; cell_cnt returns to zero (ready for the next call)

@@ -359,6 +359,7 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
   t.lb_status = (unsigned long long*)take(sizeof(unsigned long long) *
                                           ((size_t)nblk(std::max<int64_t>((int64_t)N + 1, (int64_t)g.ncell + 1), LB_TILE) + 1));
   t.lb_ticket = (unsigned*)take(sizeof(unsigned) * 4);
+  t.bin_ticket = (unsigned*)take(sizeof(unsigned) * 4);
   t.prm = (DevParams*)take(sizeof(DevParams));
   t.st = (Status*)take(sizeof(Status));
   t.h_pos = (double*)take(sizeof(double) * 3 * N);
@@ -641,10 +642,11 @@ void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, const do
   {
     Timer t(c, 0, s);
     const int ctiles = nblk(g.ncell, LB_TILE);
+    const bool fused_scan = g.ncell <= BIN_FUSED_SCAN_MAX;
     launch_k(c, k_bin, nblk(std::max<int64_t>(N, ctiles), TPB), TPB, 0, s, N, pos, type, g, nt, w.cell_of, w.cell_cnt,
-                                                                 w.st, w.lb_status, ctiles);
+             w.st, w.lb_status, ctiles, fused_scan ? w.cell_start : nullptr, w.bin_ticket);
     LAUNCH(c);
-    scan1(c, w.cell_cnt, g.ncell, w.cell_start, w.lb_status, s);
+    if (!fused_scan) scan1(c, w.cell_cnt, g.ncell, w.cell_start, w.lb_status, s);
     launch_k(c, k_scatter, nblk(N, TPB), TPB, 0, s, N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
     LAUNCH(c);
     launch_k(c, k_cell_gather, nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s, g.ncell, w.cell_start, w.perm, pos, type, g, nt,
@@ -1041,6 +1043,7 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   if (e == cudaSuccess) e = cudaMemset(ctx->w.sfz, 0, sizeof(long long) * std::max<int64_t>(n, 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.ticket, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaMemset(ctx->w.lb_ticket, 0, sizeof(unsigned) * 4);
+  if (e == cudaSuccess) e = cudaMemset(ctx->w.bin_ticket, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail_cuda(e);
   ctx->bound = true;
