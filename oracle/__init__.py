@@ -113,6 +113,8 @@ def _get():
             "orc_atom_bonds": (I64, [I64, I64, V, V, V, V, DBL, DBL, V, V, V, I64]),
             "orc_bond_energy_pair": (None, [DBL, V, DBL, DBL, DBL, DBL, INT, INT, V, V, V]),
             "orc_bond_energy": (None, [I64, V, V, V, V, V, V, V, V, V, V, V]),
+            "orc_angles": (I64, [I64, V, V, V, DBL, DBL, V, V, I64]),
+            "orc_hbonds": (I64, [I64, V, V, V, V, DBL, ctypes.c_int32, ctypes.c_uint32, V, V, I64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -335,3 +337,47 @@ def evaluate_bond_energy(system, params, bparams, cut, ref=None):
     E, F = bond_energy(ref["pos"], system.type, system.box, params, bparams, ref["brow"], ref["bcol"],
                        ref["raw"], ref["delta"])
     return E, F, ref
+
+
+# NEXT-3 readings: LAMMPS-ReaxFF-style defaults
+ILIST = dict(thb_cut=0.001, thb_cutsq=0.00001, r_hb=7.5, h_type=1, acc_mask=(1 << 2) | (1 << 3))
+
+
+def angles(brow, bcol, corr, thb_cut, thb_cutsq):
+    """O9 3-body list: (ang_off int64[B+1], ang_k int32[T]) over the full bond CSR."""
+    brow, bcol, corr = _a(brow, np.int64), _a(bcol, np.int32), _a(corr, np.float64)
+    n = len(brow) - 1
+    off = np.empty(len(bcol) + 1, np.int64)
+    cap = max(1, 8 * len(bcol))
+    while True:
+        k = np.empty(cap, np.int32)
+        t = _get().orc_angles(n, _ptr(brow), _ptr(bcol), _ptr(corr), float(thb_cut), float(thb_cutsq), _ptr(off),
+                              _ptr(k), cap)
+        if t <= cap:
+            return off, k[:t].copy()
+        cap = int(t)
+
+
+def hbonds(pos, type_, box, brow, r_hb, h_type, acc_mask):
+    """O9 H-bond list: (hb_off int64[n+1], hb_z int32[H]) by brute force."""
+    pos, type_, box, brow = _a(pos, np.float64), _a(type_, np.int32), _a(box, np.float64), _a(brow, np.int64)
+    n = len(pos)
+    off = np.empty(n + 1, np.int64)
+    cap = max(1, 64 * n)
+    while True:
+        z = np.empty(cap, np.int32)
+        t = _get().orc_hbonds(n, _ptr(pos), _ptr(type_), _ptr(box), _ptr(brow), float(r_hb), int(h_type),
+                              int(acc_mask), _ptr(off), _ptr(z), cap)
+        if t <= cap:
+            return off, z[:t].copy()
+        cap = int(t)
+
+
+def interaction_lists(system, params, cut, ilist=None, ref=None):
+    """Lists and bond orders (evaluate()), then O9.  Returns (ang_off, ang_k, hb_off, hb_z, ref)."""
+    il = dict(ILIST, **(ilist or {}))
+    if ref is None:
+        ref = evaluate(system, params, cut)
+    ao, ak = angles(ref["brow"], ref["bcol"], ref["corr"], il["thb_cut"], il["thb_cutsq"])
+    ho, hz = hbonds(ref["pos"], system.type, system.box, ref["brow"], il["r_hb"], il["h_type"], il["acc_mask"])
+    return ao, ak, ho, hz, ref

@@ -21,6 +21,8 @@
  *      Alg. 1/Alg. 2 pair loop with F_i += f, F_k -= f PAPER.md:87-110 (Alg. 1), 162-196 (Alg. 2)
  *   O8 (NEXT-1) bond energy E1 and its forces through the bond-order
  *      derivatives (the bond part of "Aggregate Forces")  PAPER.md:160, 285 (§3.3, Table 2)
+ *   O9 (NEXT-3) valence-angle (3-body) and hydrogen-bond interaction lists
+ *                                                       PAPER.md:154-158, 198-202 (§3.3)
  *
  * PARITY NOTE.  PAPER.md states no ReaxFF equations (it cites refs [6,7],
  * PAPER.md:37); the functional forms B1-B8 / N1-N6 are the standard published
@@ -584,4 +586,63 @@ void orc_bond_energy(int64_t n, const double* pos, const int32_t* type, const do
     }
   *energy = E.s + E.c;
   free(D);
+}
+
+/* ------------------------------------------------ O9 interaction lists (NEXT-3)
+ * SURVEY.md §8(f) NEXT-3; PAPER.md:198-202 (§3.3 "Three-body Interactions":
+ * angles are identified, a prefix sum gives the offsets, then they are
+ * stored) and PAPER.md:154-158 (the hydrogen-bond list built from the
+ * surroundings of covalently bonded H atoms).  Readings:
+ *   angles   for every entry e = (j, i) of the full bond list (central atom j),
+ *            the partners k of the other entries f = (j, k), f != e, of row j,
+ *            kept iff BO_e > thb_cut, BO_f > thb_cut and BO_e BO_f > thb_cutsq
+ *            (BO = corrected total bond order, a6), in row order (k ascending);
+ *   H-bonds  for every atom i of type h_type with at least one bond, the atoms
+ *            z != i of an acceptor type (bit type(z) of acc_mask) with
+ *            minimum-image r_iz^2 <= r_hb^2 (FMA-free, as O2), z ascending.
+ * Both lists are CSR: off[0] = 0, off[row+1] = off[row] + count (int64). */
+
+/* angles over the bond CSR (rows i ascending, entries sorted by j), BO from
+ * corr[B][4] (BO = corr[4e]).  Writes ang_off[B+1] always, ang_k up to cap;
+ * returns the total. */
+int64_t orc_angles(int64_t n, const int64_t* brow, const int32_t* bcol, const double* corr, double thb_cut,
+                   double thb_cutsq, int64_t* ang_off, int32_t* ang_k, int64_t cap) {
+  int64_t t = 0;
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t e = brow[j]; e < brow[j + 1]; ++e) {
+      ang_off[e] = t;
+      double be = corr[4 * e];
+      if (!(be > thb_cut)) continue;
+      for (int64_t f = brow[j]; f < brow[j + 1]; ++f) {
+        if (f == e) continue;
+        double bf = corr[4 * f];
+        if (bf > thb_cut && be * bf > thb_cutsq) {
+          if (t < cap) ang_k[t] = bcol[f];
+          ++t;
+        }
+      }
+    }
+  ang_off[brow[n]] = t;
+  return t;
+}
+
+/* H-bond lists by brute force over all atom pairs (the definition).  Writes
+ * hb_off[n+1] always, hb_z up to cap; returns the total. */
+int64_t orc_hbonds(int64_t n, const double* pos, const int32_t* type, const double box[3], const int64_t* brow,
+                   double r_hb, int32_t h_type, uint32_t acc_mask, int64_t* hb_off, int32_t* hb_z, int64_t cap) {
+  double d[3], r2max = r_hb * r_hb;
+  int64_t t = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    hb_off[i] = t;
+    if (type[i] != h_type || brow[i + 1] == brow[i]) continue;
+    for (int64_t z = 0; z < n; ++z) {
+      if (z == i || !((acc_mask >> type[z]) & 1u)) continue;
+      if (orc_dist2(pos, i, z, box, d) <= r2max) {
+        if (t < cap) hb_z[t] = (int32_t)z;
+        ++t;
+      }
+    }
+  }
+  hb_off[n] = t;
+  return t;
 }
