@@ -341,6 +341,27 @@ def main():
                        "bond_entries": B, "bonds_per_s": (B / 2) / (b_ms * 1e-3), "launches_per_call": 3}
     except Exception as ex:   # reported, never silently dropped
         bond_energy = {"error": str(ex)}
+    # NEXT-3 (outside `value`): reax_interaction_lists (counts + lists, both
+    # synchronous), K calls bracketed by events
+    ilists = None
+    try:
+        for _ in range(2):
+            ctx.interaction_lists()
+        torch.cuda.synchronize()
+        iev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        sizes = None
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            iev[k][0].record()
+            ao, ak, ho, hz = ctx.interaction_lists()
+            iev[k][1].record()
+            sizes = (len(ak), len(hz))
+        torch.cuda.synchronize()
+        ilists = {"row": "NEXT-3 3-body + H-bond lists (reax_interaction_counts + reax_interaction_lists), timed separately",
+                  "ms_per_call": sum(a.elapsed_time(b) for a, b in iev) / args.steps,
+                  "angle_entries": sizes[0], "hbond_entries": sizes[1]}
+    except Exception as ex:   # reported, never silently dropped
+        ilists = {"error": str(ex)}
     nb_ms, _ = kms["nonbonded"]
     nb_avg_s = nb_ms / args.steps * 1e-3
     achieved = W_NB_DP_PER_PAIR * P / nb_avg_s
@@ -406,7 +427,7 @@ def main():
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,
         "e2e": e2e,
-        "next_rows": {"bond_energy": bond_energy},
+        "next_rows": {"bond_energy": bond_energy, "interaction_lists": ilists},
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -160,6 +160,39 @@ reax_status reax_bond_orders(reax_ctx* ctx, const reax_params* params, const rea
 reax_status reax_bond_energy(reax_ctx* ctx, const reax_params* params, const reax_bond_params* bond_params,
                              double* force, double* energy, void* stream);
 
+/* NEXT-3: interaction lists of the current bond list and
+ * positions — the valence-angle (3-body) list and the hydrogen-bond list
+ * (§3.3: "we first identify which angles are
+ * present ... a per-atom prefix sum is computed ... then computed and stored
+ * using the global array offsets").  Readings:
+ *   angles   for every entry e = (j, i) of the exported full bond list
+ *            (reax_export_bonds order), the partners k of the other entries
+ *            f = (j, k) of row j with BO_e > thb_cut, BO_f > thb_cut and
+ *            BO_e BO_f > thb_cutsq (corrected total BO), in row order;
+ *   H-bonds  for every atom i of type h_type with at least one bond, the atoms
+ *            z != i whose type t has bit t set in acceptor_mask and whose
+ *            minimum-image distance is <= r_hb (exact fp64 test), ascending.
+ * Defaults (LAMMPS ReaxFF style): thb_cut 0.001, thb_cutsq 0.00001, r_hb
+ * 7.5 A, H = type 1, acceptors N, O = types 2, 3.  r_hb must be <= 2 sub-cell
+ * sides (>= r_nonb) and < L/2 (REAX_ERR_CUTOFF). */
+typedef struct {
+  double thb_cut, thb_cutsq, r_hb;
+  int32_t h_type;
+  uint32_t acceptor_mask;
+} reax_ilist_params;
+
+/* List sizes (synchronises): n_angles 3-body entries, n_hbonds H-bond entries.
+ * Precondition: reax_bond_orders (or reax_step) on this ctx. */
+reax_status reax_interaction_counts(reax_ctx* ctx, const reax_ilist_params* params, int64_t* n_angles,
+                                    int64_t* n_hbonds, void* stream);
+/* The lists as CSR in input order (synchronises): ang_off [dev] B+1 int64 over
+ * the exported bond entries, ang_k [dev] n_angles int32 (partner k), hb_off
+ * [dev] n+1 int64 over the atoms, hb_z [dev] n_hbonds int32 (acceptor z).
+ * ang_k / hb_z may be NULL (offsets only).  REAX_ERR_CAPACITY if one H atom has
+ * more than 1024 H-bond partners. */
+reax_status reax_interaction_lists(reax_ctx* ctx, const reax_ilist_params* params, int64_t* ang_off, int32_t* ang_k,
+                                   int64_t* hb_off, int32_t* hb_z, void* stream);
+
 /* a7-a8: Alg. 2 over the half list: tapered shielded vdW + Coulomb (N1-N6)
  * at the given charges.  q [dev] n fp64; force [dev] n*3 fp64 (overwritten,
  * input order, F = -dE/dx); energy [dev] 2 fp64 {E_vdW, E_Coul}

@@ -115,6 +115,7 @@ def _get():
             "orc_bond_energy": (None, [I64, V, V, V, V, V, V, V, V, V, V, V]),
             "orc_angles": (I64, [I64, V, V, V, DBL, DBL, V, V, I64]),
             "orc_hbonds": (I64, [I64, V, V, V, V, DBL, ctypes.c_int32, ctypes.c_uint32, V, V, I64]),
+            "orc_atom_hbonds": (I64, [I64, I64, V, V, V, INT, DBL, ctypes.c_int32, ctypes.c_uint32, V, I64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -381,3 +382,13 @@ def interaction_lists(system, params, cut, ilist=None, ref=None):
     ao, ak = angles(ref["brow"], ref["bcol"], ref["corr"], il["thb_cut"], il["thb_cutsq"])
     ho, hz = hbonds(ref["pos"], system.type, system.box, ref["brow"], il["r_hb"], il["h_type"], il["acc_mask"])
     return ao, ak, ho, hz, ref
+
+
+def atom_hbonds(i, pos, type_, box, has_bond, r_hb, h_type, acc_mask):
+    """O9 H-bond list of one atom (brute force)."""
+    pos, type_, box = _a(pos, np.float64), _a(type_, np.int32), _a(box, np.float64)
+    out = np.empty(4096, np.int32)
+    m = _get().orc_atom_hbonds(int(i), len(pos), _ptr(pos), _ptr(type_), _ptr(box), int(bool(has_bond)), float(r_hb),
+                               int(h_type), int(acc_mask), _ptr(out), 4096)
+    assert m <= 4096
+    return out[:m].copy()

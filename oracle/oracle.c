@@ -646,3 +646,21 @@ int64_t orc_hbonds(int64_t n, const double* pos, const int32_t* type, const doub
   hb_off[n] = t;
   return t;
 }
+
+/* O9 for one atom (sampled checks at large sizes): the H-bond list of atom i
+ * by brute force; has_bond says whether i has a bond.  Returns the count,
+ * writes up to cap partners ascending. */
+int64_t orc_atom_hbonds(int64_t i, int64_t n, const double* pos, const int32_t* type, const double box[3],
+                        int has_bond, double r_hb, int32_t h_type, uint32_t acc_mask, int32_t* out, int64_t cap) {
+  double d[3], r2max = r_hb * r_hb;
+  int64_t t = 0;
+  if (type[i] != h_type || !has_bond) return 0;
+  for (int64_t z = 0; z < n; ++z) {
+    if (z == i || !((acc_mask >> type[z]) & 1u)) continue;
+    if (orc_dist2(pos, i, z, box, d) <= r2max) {
+      if (t < cap) out[t] = (int32_t)z;
+      ++t;
+    }
+  }
+  return t;
+}

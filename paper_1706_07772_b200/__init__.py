@@ -25,7 +25,8 @@ EXPORTED = ("reax_status_str", "reax_create", "reax_destroy", "reax_workspace_by
             "reax_required", "reax_build_lists", "reax_bond_orders", "reax_nonbonded", "reax_step",
             "reax_step_host", "reax_set_async", "reax_check", "reax_set_timing", "reax_kernel_ms",
             "reax_launches_per_step", "reax_pair_count", "reax_export_pairs", "reax_export_nbr_digest",
-            "reax_export_bonds", "reax_selftest_math", "reax_last_cuda_error", "reax_bond_energy")
+            "reax_export_bonds", "reax_selftest_math", "reax_last_cuda_error", "reax_bond_energy",
+            "reax_interaction_counts", "reax_interaction_lists")
 
 
 class ReaxError(RuntimeError):
@@ -59,6 +60,15 @@ class BondParams(ctypes.Structure):
     _fields_ = [(f, _D) for f in BOND_PAIR]
 
 
+class IListParams(ctypes.Structure):
+    _fields_ = [("thb_cut", ctypes.c_double), ("thb_cutsq", ctypes.c_double), ("r_hb", ctypes.c_double),
+                ("h_type", ctypes.c_int32), ("acceptor_mask", ctypes.c_uint32)]
+
+
+# NEXT-3 defaults (LAMMPS ReaxFF style; readings 30-31)
+ILIST_DEFAULTS = dict(thb_cut=0.001, thb_cutsq=0.00001, r_hb=7.5, h_type=1, acceptor_mask=(1 << 2) | (1 << 3))
+
+
 class Capacity(ctypes.Structure):
     _fields_ = [("row_cap", ctypes.c_int32), ("cand_cap", ctypes.c_int32), ("bond_cap", ctypes.c_int64),
                 ("window_cap", ctypes.c_int32)]
@@ -87,6 +97,8 @@ def load_library(path: str = LIB_PATH):
         "reax_build_lists": (ctypes.c_int, [V, I64, P, P, P, P, P, P]),
         "reax_bond_orders": (ctypes.c_int, [V, P, P, P]),
         "reax_bond_energy": (ctypes.c_int, [V, P, P, P, P, P]),
+        "reax_interaction_counts": (ctypes.c_int, [V, P, ctypes.POINTER(I64), ctypes.POINTER(I64), P]),
+        "reax_interaction_lists": (ctypes.c_int, [V, P, P, P, P, P, P]),
         "reax_nonbonded": (ctypes.c_int, [V, I64, P, P, P, P, P, P, P, P, P]),
         "reax_step": (ctypes.c_int, [V, I64, P, P, P, P, P, P, P, P, P]),
         "reax_step_host": (ctypes.c_int, [V, I64, P, P, P, P, P, P, P, P, P]),
@@ -256,6 +268,26 @@ class Reax:
                                          _dptr(energy, torch.float64, (1,), "energy"), _stream_ptr(stream)),
                "reax_bond_energy")
         return force, energy
+
+    def interaction_lists(self, stream=None, **kw):
+        """reax_interaction_counts + reax_interaction_lists (NEXT-3): the
+        3-body (valence-angle) and H-bond lists as CSR in input order:
+        (ang_off int64[B+1], ang_k int32[T], hb_off int64[n+1], hb_z int32[H])."""
+        p = dict(ILIST_DEFAULTS, **kw)
+        ip = IListParams(float(p["thb_cut"]), float(p["thb_cutsq"]), float(p["r_hb"]), int(p["h_type"]),
+                         int(p["acceptor_mask"]))
+        na, nh = ctypes.c_int64(), ctypes.c_int64()
+        _check(self.lib.reax_interaction_counts(self.ctx, ctypes.byref(ip), ctypes.byref(na), ctypes.byref(nh),
+                                                _stream_ptr(stream)), "reax_interaction_counts")
+        _, B = self.pair_count(stream)
+        ao = torch.empty(B + 1, dtype=torch.int64, device=self.device)
+        ak = torch.empty(max(na.value, 1), dtype=torch.int32, device=self.device)
+        ho = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
+        hz = torch.empty(max(nh.value, 1), dtype=torch.int32, device=self.device)
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr())
+        _check(self.lib.reax_interaction_lists(self.ctx, ctypes.byref(ip), ptr(ao), ptr(ak), ptr(ho), ptr(hz),
+                                               _stream_ptr(stream)), "reax_interaction_lists")
+        return ao, ak[:na.value], ho, hz[:nh.value]
 
     def step(self, pos, type_, q, force=None, energy=None, stream=None):
         force = force if force is not None else torch.empty((self.n, 3), dtype=torch.float64, device=self.device)

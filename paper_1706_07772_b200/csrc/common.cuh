@@ -94,6 +94,7 @@ enum : int {
   ST_WIN_OVF = 32,
   ST_NONFINITE_OUT = 64,
   ST_RANGE = 128,           // a force contribution outside the fixed-point range
+  ST_HB_OVF = 512,          // an H atom's H-bond list beyond HB_CAP entries
 };
 
 struct Status {
@@ -144,6 +145,7 @@ struct WS {
   unsigned long long* lb_status;  // look-back scan tile status
   unsigned* lb_ticket;            // look-back scan tile ticket
   unsigned* bin_ticket;           // k_bin last-block ticket (fused cell scan)
+  unsigned long long* ilist_tot;  // 2: interaction-list totals (reax_interaction_counts)
   DevParams* prm;
   Status* st;
   double* h_pos;     // staging for reax_step_host

@@ -1699,6 +1699,155 @@ __global__ void __launch_bounds__(FIN_THREADS) k_bond_energy_out(int n, const in
   }
 }
 
+// ============================== NEXT-3 interaction lists (angles, H-bonds)
+// SURVEY.md §8(f) NEXT-3; PAPER.md:198-202 (§3.3 "Three-body Interactions":
+// the angles present are identified, a prefix sum gives every list its
+// offset, then they are stored) and PAPER.md:154-158 (the H-bond list from
+// the surroundings of covalently bonded H atoms).  Readings:
+// the angle partners of a full-bond-list entry e = (j, i) are the partners k
+// of the other entries f of row j with BO_e > thb_cut, BO_f > thb_cut and
+// BO_e BO_f > thb_cutsq (corrected BO), in row order; the H-bond list of an H
+// atom with a bond holds the acceptor atoms within r_hb, ascending.  Both are
+// written in the exported (input) order: angle lists over the entries of the
+// exported bond list, H-bond lists over the atoms.
+struct IList {
+  double thb_cut, thb_cutsq, r_hb2;
+  int h_type;
+  unsigned acc_mask;
+};
+
+// per bond entry (grid-stride): the number of angle partners, stored at the
+// entry's exported position (acnt) and/or summed into *total
+__global__ void k_ang_count(const int* __restrict__ brow, const int* __restrict__ bown, const int* __restrict__ perm,
+                            const double* __restrict__ bo, const long long* __restrict__ orow, int* __restrict__ acnt,
+                            unsigned long long* __restrict__ total, long long bond_cap, IList il,
+                            const Status* __restrict__ st) {
+  const long long B = st->bonds < bond_cap ? st->bonds : bond_cap;
+  unsigned long long mine = 0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
+    const int s = bown[e];
+    const int f0 = brow[s], f1 = brow[s + 1];
+    const double be = bo[8 * e + 4];
+    int c = 0;
+    if (be > il.thb_cut)
+      for (int f = f0; f < f1; ++f) {
+        const double bf = bo[8 * (long long)f + 4];
+        c += (f != e && bf > il.thb_cut && be * bf > il.thb_cutsq);
+      }
+    if (acnt) acnt[orow[perm[s]] + (e - f0)] = c;
+    mine += c;
+  }
+  if (total) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(total, mine);
+  }
+}
+
+// per bond entry: its angle partners (original indices, row order) at ang_off
+__global__ void k_ang_fill(const int* __restrict__ brow, const int* __restrict__ bown, const int* __restrict__ perm,
+                           const int* __restrict__ bkey, const double* __restrict__ bo,
+                           const long long* __restrict__ orow, const long long* __restrict__ ang_off,
+                           int* __restrict__ ang_k, long long bond_cap, IList il, const Status* __restrict__ st) {
+  const long long B = st->bonds < bond_cap ? st->bonds : bond_cap;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
+    const int s = bown[e];
+    const int f0 = brow[s], f1 = brow[s + 1];
+    const double be = bo[8 * e + 4];
+    if (!(be > il.thb_cut)) continue;
+    long long o = ang_off[orow[perm[s]] + (e - f0)];
+    for (int f = f0; f < f1; ++f) {
+      const double bf = bo[8 * (long long)f + 4];
+      if (f != e && bf > il.thb_cut && be * bf > il.thb_cutsq) ang_k[o++] = bkey[f];
+    }
+  }
+}
+
+// H-bond list of one atom per warp (sorted order): candidates from the 5^3
+// sub-cell stencil (r_hb <= 2 h), the exact FMA-free fp64 r^2 (bit-identical
+// to the oracle's), acceptors only; counting (hcnt / total) or filling (sorted
+// by original index through a rank sort in the warp's shared buffer)
+constexpr int HB_THREADS = 256;
+constexpr int HB_CAP = 1024;   // entries of one H atom's list (ST_HB_OVF beyond)
+__global__ void __launch_bounds__(HB_THREADS) k_hb_list(int n, Grid g, const int* __restrict__ cell_start,
+    const double4* __restrict__ spos, const int* __restrict__ stype, const int* __restrict__ brow,
+    const int* __restrict__ perm, IList il, int* __restrict__ hcnt, unsigned long long* __restrict__ total,
+    const long long* __restrict__ hb_off, int* __restrict__ hb_z, Status* st) {
+  __shared__ int buf[HB_THREADS / 32][HB_CAP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (s >= n) return;
+  const int i = perm[s];
+  const bool is_h = stype[s] == il.h_type && brow[s + 1] > brow[s];
+  if (!is_h) {
+    if (hcnt && lane == 0) hcnt[i] = 0;
+    return;
+  }
+  const double4 xs = spos[s];
+  int cs[3];
+  const double xw[3] = {xs.x, xs.y, xs.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int c = (int)(xw[a] * g.inv_h[a]);
+    cs[a] = c >= g.nc[a] ? g.nc[a] - 1 : c;
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  int cnt = 0;
+  int* b = buf[warp];
+  for (int oz = -SR; oz <= SR; ++oz)
+    for (int oy = -SR; oy <= SR; ++oy)
+      for (int ox = -SR; ox <= SR; ++ox) {
+        const int u[3] = {cs[0] + ox, cs[1] + oy, cs[2] + oz};
+        int cc[3];
+        double sh[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const int m = u[a] >= 0 ? u[a] / g.nc[a] : -((-u[a] + g.nc[a] - 1) / g.nc[a]);   // floor(u / nc)
+          cc[a] = u[a] - m * g.nc[a];
+          sh[a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
+        }
+        const int cid = (cc[2] * g.nc[1] + cc[1]) * g.nc[0] + cc[0];
+        const int a0 = cell_start[cid], a1 = cell_start[cid + 1];
+        for (int q0 = a0; q0 < a1; q0 += 32) {
+          const int q = q0 + lane;
+          bool hit = false;
+          if (q < a1 && q != s && ((il.acc_mask >> stype[q]) & 1u)) {
+            const double4 xq = spos[q];
+            const double dx = __dadd_rn(__dsub_rn(xq.x, xs.x), sh[0]);
+            const double dy = __dadd_rn(__dsub_rn(xq.y, xs.y), sh[1]);
+            const double dz = __dadd_rn(__dsub_rn(xq.z, xs.z), sh[2]);
+            const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            hit = r2 <= il.r_hb2;
+          }
+          const unsigned mk = __ballot_sync(0xffffffffu, hit);
+          if (hb_z && hit) {
+            const int p = cnt + __popc(mk & lt);
+            if (p < HB_CAP) b[p] = perm[q];
+          }
+          cnt += __popc(mk);
+        }
+      }
+  if (hcnt) {
+    if (lane == 0) {
+      hcnt[i] = cnt;
+      if (total) atomicAdd(total, (unsigned long long)cnt);
+    }
+    return;
+  }
+  if (cnt > HB_CAP) {
+    if (lane == 0) set_flag(st, ST_HB_OVF);
+    return;
+  }
+  __syncwarp();
+  const long long o = hb_off[i];
+  for (int p = lane; p < cnt; p += 32) {   // rank sort by original index (all distinct)
+    const int v = b[p];
+    int r = 0;
+    for (int t = 0; t < cnt; ++t) r += b[t] < v;
+    hb_z[o + r] = v;
+  }
+}
+
 // ================================================================= export
 __device__ __forceinline__ uint64_t mix64(uint64_t a, uint64_t b) {
   uint64_t z = (a << 32) ^ b;

@@ -321,7 +321,8 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
     return base ? base + r : nullptr;
   };
   size_t N = (size_t)std::max<int64_t>(n, 1);
-  size_t nscan = (size_t)nblk(std::max<int64_t>(std::max<int64_t>(N + 1, (int64_t)g.ncell + 1), 1), SCAN_TILE) + 2;
+  // scan partials: atoms, cells or bond entries (the interaction-list scan runs over the bond list)
+  size_t nscan = (size_t)nblk(std::max<int64_t>(std::max<int64_t>(N + 1, (int64_t)g.ncell + 1), c.bond_cap + 1), SCAN_TILE) + 2;
   WS t;
   t.cell_cnt = (int*)take(sizeof(int) * (g.ncell + 1));
   t.cell_start = (int*)take(sizeof(int) * (g.ncell + 1));
@@ -360,6 +361,7 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
                                           ((size_t)nblk(std::max<int64_t>((int64_t)N + 1, (int64_t)g.ncell + 1), LB_TILE) + 1));
   t.lb_ticket = (unsigned*)take(sizeof(unsigned) * 4);
   t.bin_ticket = (unsigned*)take(sizeof(unsigned) * 4);
+  t.ilist_tot = (unsigned long long*)take(sizeof(unsigned long long) * 2);
   t.prm = (DevParams*)take(sizeof(DevParams));
   t.st = (Status*)take(sizeof(Status));
   t.h_pos = (double*)take(sizeof(double) * 3 * N);
@@ -556,6 +558,7 @@ reax_status interpret_status(reax_ctx* c, cudaStream_t s) {
   }
   cudaMemsetAsync(c->w.st, 0, sizeof(Status), s);
   if (f & ST_TYPE) { c->lists_ok = c->bonds_ok = false; return REAX_ERR_ARG; }
+  if (f & ST_HB_OVF) return REAX_ERR_CAPACITY;
   if (f & (ST_NONFINITE_IN | ST_NONFINITE_OUT)) return REAX_ERR_NONFINITE;
   return REAX_ERR_RANGE;
 }
@@ -907,6 +910,97 @@ reax_status do_bond_energy(reax_ctx* c, const reax_params* prm, const reax_bond_
   return read_status(c, s, !c->async);
 }
 
+// NEXT-3: interaction lists (3-body angles, H-bonds) of the current bond
+// list and positions (readings 30-31)
+reax_status ilist_prepare(reax_ctx* c, const reax_ilist_params* p, IList& il) {
+  if (!c || !p) return REAX_ERR_ARG;
+  if (!c->bound || !c->lists_ok || !c->bonds_ok) return REAX_ERR_STATE;
+  if (!(std::isfinite(p->thb_cut) && p->thb_cut >= 0.0 && std::isfinite(p->thb_cutsq) && p->thb_cutsq >= 0.0))
+    return REAX_ERR_PARAM;
+  const double hmin = std::min(c->g.h[0], std::min(c->g.h[1], c->g.h[2]));
+  const double lmin = std::min(c->g.L[0], std::min(c->g.L[1], c->g.L[2]));
+  // the H-bond search covers +-SR sub-cells; one periodic image within r_hb
+  if (!(std::isfinite(p->r_hb) && p->r_hb > 0.0 && p->r_hb <= SR * hmin && 2.0 * p->r_hb < lmin)) return REAX_ERR_CUTOFF;
+  if (p->h_type < 0 || p->h_type >= NT_MAX) return REAX_ERR_PARAM;
+  il.thb_cut = p->thb_cut;
+  il.thb_cutsq = p->thb_cutsq;
+  il.r_hb2 = p->r_hb * p->r_hb;
+  il.h_type = p->h_type;
+  il.acc_mask = p->acceptor_mask;
+  return REAX_OK;
+}
+
+reax_status do_ilist_counts(reax_ctx* c, const reax_ilist_params* p, int64_t* n_angles, int64_t* n_hbonds,
+                            cudaStream_t s) {
+  IList il;
+  reax_status r = ilist_prepare(c, p, il);
+  if (r != REAX_OK) return r;
+  unsigned long long tot[2] = {0, 0};
+  const int N = (int)c->n;
+  if (N > 0) {
+    WS& w = c->w;
+    if (cudaError_t e_ = cudaMemsetAsync(w.ilist_tot, 0, sizeof(tot), s)) return fail_cuda(e_);
+    k_ang_count<<<148 * 8, TPB, 0, s>>>(w.brow, w.bown, w.perm, w.bo, nullptr, nullptr, w.ilist_tot,
+                                        c->cap.bond_cap, il, w.st);
+    k_hb_list<<<nblk((int64_t)N * 32, HB_THREADS), HB_THREADS, 0, s>>>(N, c->g, w.cell_start, w.spos, w.stype, w.brow,
+                                                                      w.perm, il, w.bc_len, w.ilist_tot + 1, nullptr,
+                                                                      nullptr, w.st);
+    if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+    if (cudaError_t e_ = cudaMemcpyAsync(tot, w.ilist_tot, sizeof(tot), cudaMemcpyDeviceToHost, s)) return fail_cuda(e_);
+    if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
+  }
+  if (n_angles) *n_angles = (int64_t)tot[0];
+  if (n_hbonds) *n_hbonds = (int64_t)tot[1];
+  return REAX_OK;
+}
+
+reax_status do_ilist_lists(reax_ctx* c, const reax_ilist_params* p, int64_t* ang_off, int32_t* ang_k, int64_t* hb_off,
+                           int32_t* hb_z, cudaStream_t s) {
+  IList il;
+  reax_status r = ilist_prepare(c, p, il);
+  if (r != REAX_OK) return r;
+  if (!ang_off || !hb_off) return REAX_ERR_ARG;
+  const int N = (int)c->n;
+  WS& w = c->w;
+  if (N == 0) {
+    if (cudaMemsetAsync(ang_off, 0, sizeof(int64_t), s) != cudaSuccess ||
+        cudaMemsetAsync(hb_off, 0, sizeof(int64_t), s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+      return fail_cuda(cudaGetLastError());
+    return REAX_OK;
+  }
+  int B = 0;
+  if (cudaMemcpyAsync(&B, w.brow + N, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return fail_cuda(cudaGetLastError());
+  // angles: exported row offsets of the bond list, per-entry counts at the
+  // exported positions, prefix sum, fill
+  k_export_bond_deg<<<nblk(N, TPB), TPB, 0, s>>>(N, w.iperm, w.brow, w.bc_len);
+  if (scan<int, long long>(c, w.bc_len, N, w.exp_off, s) != cudaSuccess) return fail_cuda(cudaGetLastError());
+  k_ang_count<<<148 * 8, TPB, 0, s>>>(w.brow, w.bown, w.perm, w.bo, w.exp_off, w.ucol, nullptr, c->cap.bond_cap, il,
+                                      w.st);
+  if (B > 0) {
+    if (scan<int, long long>(c, w.ucol, B, reinterpret_cast<long long*>(ang_off), s) != cudaSuccess)
+      return fail_cuda(cudaGetLastError());
+    if (ang_k)
+      k_ang_fill<<<148 * 8, TPB, 0, s>>>(w.brow, w.bown, w.perm, w.bkey, w.bo, w.exp_off,
+                                         reinterpret_cast<const long long*>(ang_off), ang_k, c->cap.bond_cap, il, w.st);
+  } else if (cudaMemsetAsync(ang_off, 0, sizeof(int64_t), s) != cudaSuccess) {
+    return fail_cuda(cudaGetLastError());
+  }
+  // H-bonds: per-atom counts, prefix sum, fill
+  k_hb_list<<<nblk((int64_t)N * 32, HB_THREADS), HB_THREADS, 0, s>>>(N, c->g, w.cell_start, w.spos, w.stype, w.brow, w.perm,
+                                                                    il, w.bc_len, nullptr, nullptr, nullptr, w.st);
+  if (scan<int, long long>(c, w.bc_len, N, reinterpret_cast<long long*>(hb_off), s) != cudaSuccess)
+    return fail_cuda(cudaGetLastError());
+  if (hb_z)
+    k_hb_list<<<nblk((int64_t)N * 32, HB_THREADS), HB_THREADS, 0, s>>>(N, c->g, w.cell_start, w.spos, w.stype, w.brow,
+                                                                      w.perm, il, nullptr, nullptr,
+                                                                      reinterpret_cast<const long long*>(hb_off), hb_z,
+                                                                      w.st);
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  return read_status(c, s, true);
+}
+
 }  // namespace
 
 // ==================================================================== ABI
@@ -1235,6 +1329,16 @@ reax_status reax_selftest_math(reax_ctx* ctx, int64_t n, const double* x, double
   if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
   if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
   return REAX_OK;
+}
+
+reax_status reax_interaction_counts(reax_ctx* ctx, const reax_ilist_params* params, int64_t* n_angles,
+                                    int64_t* n_hbonds, void* stream) {
+  return do_ilist_counts(ctx, params, n_angles, n_hbonds, (cudaStream_t)stream);
+}
+
+reax_status reax_interaction_lists(reax_ctx* ctx, const reax_ilist_params* params, int64_t* ang_off, int32_t* ang_k,
+                                   int64_t* hb_off, int32_t* hb_z, void* stream) {
+  return do_ilist_lists(ctx, params, ang_off, ang_k, hb_off, hb_z, (cudaStream_t)stream);
 }
 
 reax_status reax_pair_count(reax_ctx* ctx, int64_t* n_half_pairs, int64_t* n_bond_entries, void* stream) {
