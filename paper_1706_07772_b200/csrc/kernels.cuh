@@ -1794,39 +1794,68 @@ __global__ void __launch_bounds__(HB_THREADS) k_hb_list(int n, Grid g, const int
   const unsigned lt = (1u << lane) - 1u;
   int cnt = 0;
   int* b = buf[warp];
-  for (int oz = -SR; oz <= SR; ++oz)
-    for (int oy = -SR; oy <= SR; ++oy)
-      for (int ox = -SR; ox <= SR; ++ox) {
-        const int u[3] = {cs[0] + ox, cs[1] + oy, cs[2] + oz};
-        int cc[3];
-        double sh[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const int m = u[a] >= 0 ? u[a] / g.nc[a] : -((-u[a] + g.nc[a] - 1) / g.nc[a]);   // floor(u / nc)
-          cc[a] = u[a] - m * g.nc[a];
-          sh[a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
-        }
-        const int cid = (cc[2] * g.nc[1] + cc[1]) * g.nc[0] + cc[0];
-        const int a0 = cell_start[cid], a1 = cell_start[cid + 1];
-        for (int q0 = a0; q0 < a1; q0 += 32) {
-          const int q = q0 + lane;
-          bool hit = false;
-          if (q < a1 && q != s && ((il.acc_mask >> stype[q]) & 1u)) {
-            const double4 xq = spos[q];
-            const double dx = __dadd_rn(__dsub_rn(xq.x, xs.x), sh[0]);
-            const double dy = __dadd_rn(__dsub_rn(xq.y, xs.y), sh[1]);
-            const double dz = __dadd_rn(__dsub_rn(xq.z, xs.z), sh[2]);
-            const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-            hit = r2 <= il.r_hb2;
-          }
-          const unsigned mk = __ballot_sync(0xffffffffu, hit);
-          if (hb_z && hit) {
-            const int p = cnt + __popc(mk & lt);
-            if (p < HB_CAP) b[p] = perm[q];
-          }
-          cnt += __popc(mk);
-        }
+  // the stencil as (2 SR + 1)^2 runs of sub-cells along x (contiguous in the
+  // sorted order unless the run wraps: then two pieces); lane r < 25 fetches
+  // run r's bounds up front, so the scan below has no dependent index loads
+  constexpr int NR = (2 * SR + 1) * (2 * SR + 1);
+  int pa0 = 0, pa1 = 0, pb0 = 0, pb1 = 0;
+  double shy = 0.0, shz = 0.0, sxa = 0.0, sxb = 0.0;
+  if (lane < NR) {
+    const int oy = lane % (2 * SR + 1) - SR, oz = lane / (2 * SR + 1) - SR;
+    int cy = cs[1] + oy, cz = cs[2] + oz;
+    const int my = cy >= 0 ? cy / g.nc[1] : -((-cy + g.nc[1] - 1) / g.nc[1]);
+    const int mz = cz >= 0 ? cz / g.nc[2] : -((-cz + g.nc[2] - 1) / g.nc[2]);
+    cy -= my * g.nc[1];
+    cz -= mz * g.nc[2];
+    shy = my == 0 ? 0.0 : (my > 0 ? g.L[1] : -g.L[1]);
+    shz = mz == 0 ? 0.0 : (mz > 0 ? g.L[2] : -g.L[2]);
+    const int row = (cz * g.nc[1] + cy) * g.nc[0];
+    const int xa = cs[0] - SR, xb = cs[0] + SR;   // unwrapped x-cell range: nc >= 4, so one end wraps at most
+    if (xa < 0) {   // [nc + xa, nc) with -L, then [0, xb]
+      pa0 = cell_start[row + g.nc[0] + xa]; pa1 = cell_start[row + g.nc[0]]; sxa = -g.L[0];
+      pb0 = cell_start[row]; pb1 = cell_start[row + xb + 1]; sxb = 0.0;
+    } else if (xb >= g.nc[0]) {   // [xa, nc), then [0, xb - nc] with +L
+      pa0 = cell_start[row + xa]; pa1 = cell_start[row + g.nc[0]]; sxa = 0.0;
+      pb0 = cell_start[row]; pb1 = cell_start[row + xb - g.nc[0] + 1]; sxb = g.L[0];
+    } else {
+      pa0 = cell_start[row + xa]; pa1 = cell_start[row + xb + 1]; sxa = 0.0;
+    }
+  }
+  auto scan_piece = [&](int q0, int q1, double sx, double sy, double sz) {
+    for (int qb = q0; qb < q1; qb += 64) {   // two chunks of 32 in flight
+      const int qa = qb + lane, qc = qb + 32 + lane;
+      const bool va = qa < q1 && qa != s, vc = qc < q1 && qc != s;
+      const double4 xa4 = spos[va ? qa : s], xc4 = spos[vc ? qc : s];
+      const int ta = va ? stype[qa] : -1, tc = vc ? stype[qc] : -1;
+      bool ha = false, hc = false;
+      if (va && ((il.acc_mask >> ta) & 1u)) {
+        const double dx = __dadd_rn(__dsub_rn(xa4.x, xs.x), sx);
+        const double dy = __dadd_rn(__dsub_rn(xa4.y, xs.y), sy);
+        const double dz = __dadd_rn(__dsub_rn(xa4.z, xs.z), sz);
+        ha = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)) <= il.r_hb2;
       }
+      if (vc && ((il.acc_mask >> tc) & 1u)) {
+        const double dx = __dadd_rn(__dsub_rn(xc4.x, xs.x), sx);
+        const double dy = __dadd_rn(__dsub_rn(xc4.y, xs.y), sy);
+        const double dz = __dadd_rn(__dsub_rn(xc4.z, xs.z), sz);
+        hc = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)) <= il.r_hb2;
+      }
+      const unsigned ma = __ballot_sync(0xffffffffu, ha), mc = __ballot_sync(0xffffffffu, hc);
+      if (hb_z) {
+        if (ha) { const int p = cnt + __popc(ma & lt); if (p < HB_CAP) b[p] = perm[qa]; }
+        if (hc) { const int p = cnt + __popc(ma) + __popc(mc & lt); if (p < HB_CAP) b[p] = perm[qc]; }
+      }
+      cnt += __popc(ma) + __popc(mc);
+    }
+  };
+  for (int r = 0; r < NR; ++r) {
+    const int a0 = __shfl_sync(0xffffffffu, pa0, r), a1 = __shfl_sync(0xffffffffu, pa1, r);
+    const int b0 = __shfl_sync(0xffffffffu, pb0, r), b1 = __shfl_sync(0xffffffffu, pb1, r);
+    const double sy = __shfl_sync(0xffffffffu, shy, r), sz = __shfl_sync(0xffffffffu, shz, r);
+    const double xa = __shfl_sync(0xffffffffu, sxa, r), xb = __shfl_sync(0xffffffffu, sxb, r);
+    scan_piece(a0, a1, xa, sy, sz);
+    scan_piece(b0, b1, xb, sy, sz);
+  }
   if (hcnt) {
     if (lane == 0) {
       hcnt[i] = cnt;
