@@ -23,7 +23,9 @@ constexpr int MAX_SPLIT = 8;
 // CTAs per home block for the window kernels: small systems (c0/c1) have too
 // few home blocks to fill 148 SMs, so each block's rows are split over
 // several CTAs (each builds the same window)
-// (measured on c1: nonbonded best at 4 CTA-units per SM, list build at 4)
+// (measured on c1: the step is fastest with the nonbonded at 2 CTA-units per
+// SM — one CTA per home block, leaving the side-stream bond chain room — and
+// the list build at 4)
 int choose_split(int nblock, int per_sm, const char* env) {
   if (const char* e = getenv(env)) per_sm = std::max(1, atoi(e));   // tuning experiments
   int target = 148 * per_sm;
@@ -1120,7 +1122,7 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   ctx->g = g;
   ctx->n = n;
   ctx->cap = c;
-  ctx->nsplit = choose_split(g.nblock, 4, "REAX_CTAS_PER_SM");
+  ctx->nsplit = choose_split(g.nblock, 2, "REAX_CTAS_PER_SM");
   ctx->nsplit_nbr = choose_split(g.nblock, 4, "REAX_NBR_CTAS_PER_SM");
   if (const char* e = getenv("REAX_NBR_SPLIT")) ctx->nsplit_nbr = std::max(1, std::min(MAX_SPLIT, atoi(e)));
   ctx->cut = *cut;
