@@ -380,6 +380,19 @@ def main():
     lctx.check()
     lk = lctx.kernel_ms(reset=True)
     nbr_avg_s = lk["nbr"][0] / 10 * 1e-3
+    # k_nonbonded on its own (the reax_nonbonded path: no concurrent bond
+    # chain), same lists, for the kernel's isolated roofline line
+    lctx.bond_orders()
+    Fi = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    Ei = torch.empty(2, dtype=torch.float64, device=dev)
+    lctx.nonbonded(pos, typ, q, Fi, Ei)
+    lctx.kernel_ms(reset=True)
+    for k in range(10):
+        flush.fill_(float(k))
+        lctx.nonbonded(pos, typ, q, Fi, Ei)
+    torch.cuda.synchronize()
+    lctx.check()
+    nb_iso_s = lctx.kernel_ms(reset=True)["nonbonded"][0] / 10 * 1e-3
     del lctx
     nbr_bytes = n * NBR_BYTES_PER_ATOM_FIXED + P * NBR_BYTES_PER_PAIR + 2.9 * n * NBR_BYTES_PER_BONDCAND
     hbm_peak = None
@@ -420,6 +433,10 @@ def main():
             {"kernel": "k_nbr_build (a3-a4; reax_build_lists path, timed separately)", "bound": "hbm", "achieved": nbr_bytes / nbr_avg_s / 1e9, "peak": hbm_peak,
              "unit": "GB/s", "frac": nbr_bytes / nbr_avg_s / 1e9 / hbm_peak, "avg_launch_ms": nbr_avg_s * 1e3,
              "bytes_per_launch": nbr_bytes, "traffic": nbr_traffic},
+            {"kernel": "k_nonbonded (a7) on its own (reax_nonbonded path, no concurrent bond chain)", "bound": "alu",
+             "achieved": W_NB_DP_PER_PAIR * P / nb_iso_s / 1e12, "peak": peak_dfma / 1e12,
+             "unit": "T FP64-pipe thread-instructions/s", "frac": W_NB_DP_PER_PAIR * P / nb_iso_s / peak_dfma,
+             "avg_launch_ms": nb_iso_s * 1e3},
         ],
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kms.items()},
         "timing_pass_ms_per_step": pass2_ms,
