@@ -470,7 +470,7 @@ struct NbrSmem {
   WinSmem W;
   float rcand2[NTP_MAX];
   int gbase[NHOME + 1];   // first row group of each home sub-cell (groups of NBR_G rows)
-  int ncs[NBR_THREADS / 32][4];   // per warp: bond-candidate counters of its group's rows
+  int ncs[NBR_THREADS / 32][8];   // per warp: bond-candidate counters of its group's rows
   int next_row;
 };
 
@@ -518,7 +518,10 @@ struct SlotJK {
 // (POPC/VOTE issue to the narrow XU pipe on sm_100a, 16 lanes/SM/clk, and
 // bound the list build); their order is irrelevant because k_bond_rank sorts
 // each bond row.  len[r] may exceed row_cap (the caller flags it).
-constexpr int NBR_G = 4;
+#ifndef NBR_GROUP
+#define NBR_GROUP 2   // measured at 4 CTAs/SM, 64 registers: 2 beats 1, 3, 4, 6 (c1 70 vs 75 us for 4)
+#endif
+constexpr int NBR_G = NBR_GROUP;   // rows sharing one candidate stream
 template <bool BOND, typename SI>
 __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, const float4* __restrict__ cand, SI sl,
                                                const double4* __restrict__ spos, int si0, int nrow, int h,
