@@ -684,11 +684,11 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, con
 __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, const int* __restrict__ cell_start,
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
-    int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, int blk0, Status* st) {
+    int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NbrSmem S;
-  const int blk = blk0 + blockIdx.x / nsplit, split = blockIdx.x % nsplit;   // blk0: first home block of this launch
+  const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
   float4* cand = reinterpret_cast<float4*>(dyn);                                // window_cap + 32
   int* cand_j = reinterpret_cast<int*>(cand + window_cap + 32);                  // window_cap + 32
   unsigned char* cand_k = reinterpret_cast<unsigned char*>(cand_j + window_cap + 32);
@@ -1248,11 +1248,11 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
     unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
-    double2* __restrict__ erow, int nsplit, int blk0, Status* st) {
+    double2* __restrict__ erow, int nsplit, Status* st) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
-  const int blk = blk0 + blockIdx.x / nsplit, split = blockIdx.x % nsplit;   // blk0: first home block of this launch
+  const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
   const int nt = prm->nt;
   double* ET = reinterpret_cast<double*>(dyn);                  // exp table
   double2* LT = reinterpret_cast<double2*>(ET + EXP_TBL);       // log table

@@ -660,21 +660,20 @@ void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, const do
   }
 }
 
-// a3-a4 over home blocks [b0, b1)
-void launch_nbr_part(reax_ctx* c, int b0, int b1, cudaStream_t s) {
-  if (b1 <= b0) return;
+// a3-a4: the half list and the bond candidates
+void launch_nbr(reax_ctx* c, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
   Timer t(c, 1, s);
-  launch_k(c, k_nbr_build, (b1 - b0) * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s,
+  launch_k(c, k_nbr_build, g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s,
            g, w.cell_start, w.sloc, w.spos, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, w.bc, w.bc_len,
-           c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, b0, w.st);
+           c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st);
   LAUNCH(c);
 }
 
 void launch_lists(reax_ctx* c, int N, const double* pos, const int* type, const double* q, int nt, cudaStream_t s) {
   launch_bin(c, N, pos, type, q, nt, s);
-  launch_nbr_part(c, 0, c->g.nblock, s);
+  launch_nbr(c, s);
 }
 
 // a4-a5: full bond list with BO' and Delta' (reads spos x/y/z, stype, bond candidates)
@@ -752,15 +751,14 @@ reax_status do_bond_orders(reax_ctx* c, const reax_params* prm, const reax_cutof
 }
 
 // a7-a8: nonbonded energies and forces (reads the half list, spos, stype, perm/iperm)
-// a7 over home blocks [b0, b1)
-void launch_nb_part(reax_ctx* c, int b0, int b1, int nt, cudaStream_t s) {
-  if (b1 <= b0) return;
+// a7: one CTA per (home block, split)
+void launch_nb(reax_ctx* c, int nt, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
   Timer t(c, 4, s);
-  launch_k(c, k_nonbonded, (b1 - b0) * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s,
+  launch_k(c, k_nonbonded, g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s,
            g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy,
-           w.sfz, w.erow, c->nsplit, b0, w.st);
+           w.sfz, w.erow, c->nsplit, w.st);
   LAUNCH(c);
 }
 
@@ -783,7 +781,7 @@ void launch_nonbonded(reax_ctx* c, int N, const double* q, double* force, double
     launch_k(c, k_nb_prep, nblk(N, TPB), TPB, 0, s, N, q, w.perm, w.spos, w.sfx, w.sfy, w.sfz, w.st);
     LAUNCH(c);
   }
-  launch_nb_part(c, 0, g.nblock, nt, s);
+  launch_nb(c, nt, s);
   launch_finalize(c, N, force, energy, s);
 }
 
@@ -836,7 +834,7 @@ reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, 
   const bool fork = !c->serial;
   const int nt = prm->ntypes;
   launch_bin(c, N, pos, type, q, nt, s);
-  launch_nbr_part(c, 0, c->g.nblock, s);
+  launch_nbr(c, s);
   // fork: the bond chain (a4-a6, small latency-bound kernels) on the side
   // stream beside the nonbonded kernel (a7) on s; join; k_finalize (a8)
   cudaStream_t sb = s;
@@ -847,7 +845,7 @@ reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, 
   }
   launch_bonds(c, N, sb);
   launch_bond_correct(c, sb);
-  launch_nb_part(c, 0, c->g.nblock, nt, s);
+  launch_nb(c, nt, s);
   if (fork && (cudaEventRecord(c->ev_join, c->side) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join, 0) != cudaSuccess))
     return fail_cuda(cudaGetLastError());
   launch_finalize(c, N, force, energy, s);
