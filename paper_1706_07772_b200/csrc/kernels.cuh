@@ -1260,9 +1260,11 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   int2* sinfo = reinterpret_cast<int2*>(pc + nt * nt);          // slot -> {sorted atom, window cell | type << 8}
   unsigned* fa = reinterpret_cast<unsigned*>(sinfo + window_cap);   // F window, low words [3][window_cap]
   int* fb = reinterpret_cast<int*>(fa + 3 * window_cap);            // F window, high words [3][window_cap]
-  unsigned char* kmap = reinterpret_cast<unsigned char*>(fb + 3 * window_cap);   // slot -> window cell
+  // the row buffers follow the 16-byte aligned F window directly (window_cap is
+  // a multiple of 32), typed from the shared base: shared-space loads (LDS)
   const int rb_cap = (row_cap + 7) & ~7;                                          // row buffer entries (16-byte multiple)
-  uint16_t* rbuf = reinterpret_cast<uint16_t*>(((uintptr_t)(kmap + window_cap) + 15) & ~(uintptr_t)15);  // [NB_WARPS][2][rb_cap]
+  uint16_t* rbuf = reinterpret_cast<uint16_t*>(fb + 3 * window_cap);              // [NB_WARPS][2][rb_cap]
+  unsigned char* kmap = reinterpret_cast<unsigned char*>(rbuf + NB_WARPS * 2 * rb_cap);   // slot -> window cell
   for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) pc[t] = prm->nb[t];
   for (int t = threadIdx.x; t < EXP_TBL; t += blockDim.x) ET[t] = prm->exp_tbl[t];
   for (int t = threadIdx.x; t < LOG_TBL; t += blockDim.x) LT[t] = make_double2(prm->log_tbl[2 * t], prm->log_tbl[2 * t + 1]);
