@@ -248,3 +248,25 @@ def test_dense_system_regrows(params):
     s = gen.make_system(2662, (22.0, 22.0, 22.0), gen.SEED_BASE + 321)
     ctx, _, _, _ = full_parity(s, params)
     assert ctx.cap.row_cap > 512 and ctx.cap.window_cap > 2048
+
+
+def test_gpu_invariances(params):
+    """GPU-only invariants at c1: a rigid translation (then
+    wrap) and a relabelling of the atoms leave the pair and bond counts, the
+    energies (1e-10 relative) and the forces (1e-8 (1 + |F|), permuted) as
+    they were; the net force vanishes."""
+    s = gen.make_config(1)
+    ctx, F, E = gpu_run(s, params)
+    P, B = ctx.pair_count()
+    assert np.all(np.abs(F.sum(0)) <= 1e-11 * np.abs(F).sum())
+    t = gen.System(oracle.wrap(s.pos + np.array([13.7, -21.1, 5.3]), s.box), s.type, s.q, s.box)
+    ctx2, F2, E2 = gpu_run(t, params)
+    assert ctx2.pair_count() == (P, B)
+    assert np.all(np.abs(E2 - E) <= 1e-10 * np.abs(E))
+    assert np.all(np.abs(F2 - F) <= 1e-8 * (1 + np.abs(F)))
+    perm = np.random.default_rng(9).permutation(len(s.pos))
+    r = gen.System(s.pos[perm].copy(), s.type[perm].copy(), s.q[perm].copy(), s.box)
+    ctx3, F3, E3 = gpu_run(r, params)
+    assert ctx3.pair_count() == (P, B)
+    assert np.all(np.abs(E3 - E) <= 1e-10 * np.abs(E))
+    assert np.all(np.abs(F3 - F[perm]) <= 1e-8 * (1 + np.abs(F[perm])))
