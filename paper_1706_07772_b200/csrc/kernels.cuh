@@ -1774,20 +1774,37 @@ __global__ void k_ang_fill(const int* __restrict__ brow, const int* __restrict__
 // by original index through a rank sort in the warp's shared buffer)
 constexpr int HB_THREADS = 256;
 constexpr int HB_CAP = 1024;   // entries of one H atom's list (ST_HB_OVF beyond)
-__global__ void __launch_bounds__(HB_THREADS) k_hb_list(int n, Grid g, const int* __restrict__ cell_start,
-    const double4* __restrict__ spos, const int* __restrict__ stype, const int* __restrict__ brow,
-    const int* __restrict__ perm, IList il, int* __restrict__ hcnt, unsigned long long* __restrict__ total,
+// the H atoms with a bond, compacted into hlist (warp-aggregated slots; the
+// order is irrelevant: every H atom writes its own rows); zero counts for
+// the others
+__global__ void k_hb_collect(int n, const int* __restrict__ stype, const int* __restrict__ brow,
+                             const int* __restrict__ perm, int h_type, int* __restrict__ hcnt, int* __restrict__ hlist,
+                             unsigned* __restrict__ hn) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool is_h = s < n && stype[s] == h_type && brow[s + 1] > brow[s];
+  if (s < n && hcnt && !is_h) hcnt[perm[s]] = 0;
+  const unsigned mk = __ballot_sync(0xffffffffu, is_h);
+  if (!mk) return;
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(hn, (unsigned)__popc(mk));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (is_h) hlist[base + __popc(mk & ((1u << lane) - 1u))] = s;
+}
+
+// one warp per H atom of hlist (grid-stride over the warps)
+__global__ void __launch_bounds__(HB_THREADS) k_hb_list(const int* __restrict__ hlist, const unsigned* __restrict__ hn,
+    Grid g, const int* __restrict__ cell_start,
+    const double4* __restrict__ spos, const int* __restrict__ stype, const int* __restrict__ perm, IList il,
+    int* __restrict__ hcnt, unsigned long long* __restrict__ total,
     const long long* __restrict__ hb_off, int* __restrict__ hb_z, Status* st) {
   __shared__ int buf[HB_THREADS / 32][HB_CAP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  if (s >= n) return;
+  const int nh = (int)*hn;
+  for (int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); w < nh;
+       w += (int)((gridDim.x * (int64_t)blockDim.x) >> 5)) {
+  const int s = hlist[w];
   const int i = perm[s];
-  const bool is_h = stype[s] == il.h_type && brow[s + 1] > brow[s];
-  if (!is_h) {
-    if (hcnt && lane == 0) hcnt[i] = 0;
-    return;
-  }
   const double4 xs = spos[s];
   int cs[3];
   const double xw[3] = {xs.x, xs.y, xs.z};
@@ -1866,11 +1883,11 @@ __global__ void __launch_bounds__(HB_THREADS) k_hb_list(int n, Grid g, const int
       hcnt[i] = cnt;
       if (total) atomicAdd(total, (unsigned long long)cnt);
     }
-    return;
+    continue;
   }
   if (cnt > HB_CAP) {
     if (lane == 0) set_flag(st, ST_HB_OVF);
-    return;
+    continue;
   }
   __syncwarp();
   const long long o = hb_off[i];
@@ -1879,6 +1896,8 @@ __global__ void __launch_bounds__(HB_THREADS) k_hb_list(int n, Grid g, const int
     int r = 0;
     for (int t = 0; t < cnt; ++t) r += b[t] < v;
     hb_z[o + r] = v;
+  }
+  __syncwarp();   // b is reused by the warp's next atom
   }
 }
 

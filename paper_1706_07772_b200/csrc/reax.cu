@@ -363,7 +363,7 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
                                           ((size_t)nblk(std::max<int64_t>((int64_t)N + 1, (int64_t)g.ncell + 1), LB_TILE) + 1));
   t.lb_ticket = (unsigned*)take(sizeof(unsigned) * 4);
   t.bin_ticket = (unsigned*)take(sizeof(unsigned) * 4);
-  t.ilist_tot = (unsigned long long*)take(sizeof(unsigned long long) * 2);
+  t.ilist_tot = (unsigned long long*)take(sizeof(unsigned long long) * 4);   // [2]: H-atom count (k_hb_collect)
   t.prm = (DevParams*)take(sizeof(DevParams));
   t.st = (Status*)take(sizeof(Status));
   t.h_pos = (double*)take(sizeof(double) * 3 * N);
@@ -939,12 +939,13 @@ reax_status do_ilist_counts(reax_ctx* c, const reax_ilist_params* p, int64_t* n_
   const int N = (int)c->n;
   if (N > 0) {
     WS& w = c->w;
-    if (cudaError_t e_ = cudaMemsetAsync(w.ilist_tot, 0, sizeof(tot), s)) return fail_cuda(e_);
+    if (cudaError_t e_ = cudaMemsetAsync(w.ilist_tot, 0, 4 * sizeof(unsigned long long), s)) return fail_cuda(e_);
     k_ang_count<<<148 * 8, TPB, 0, s>>>(w.brow, w.bown, w.perm, w.bo, nullptr, nullptr, w.ilist_tot,
                                         c->cap.bond_cap, il, w.st);
-    k_hb_list<<<nblk((int64_t)N * 32, HB_THREADS), HB_THREADS, 0, s>>>(N, c->g, w.cell_start, w.spos, w.stype, w.brow,
-                                                                      w.perm, il, w.bc_len, w.ilist_tot + 1, nullptr,
-                                                                      nullptr, w.st);
+    unsigned* hn = reinterpret_cast<unsigned*>(w.ilist_tot + 2);
+    k_hb_collect<<<nblk(N, TPB), TPB, 0, s>>>(N, w.stype, w.brow, w.perm, il.h_type, w.bc_len, w.cell_of, hn);
+    k_hb_list<<<148 * 8, HB_THREADS, 0, s>>>(w.cell_of, hn, c->g, w.cell_start, w.spos, w.stype, w.perm, il, w.bc_len,
+                                             w.ilist_tot + 1, nullptr, nullptr, w.st);
     if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
     if (cudaError_t e_ = cudaMemcpyAsync(tot, w.ilist_tot, sizeof(tot), cudaMemcpyDeviceToHost, s)) return fail_cuda(e_);
     if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
@@ -988,15 +989,16 @@ reax_status do_ilist_lists(reax_ctx* c, const reax_ilist_params* p, int64_t* ang
     return fail_cuda(cudaGetLastError());
   }
   // H-bonds: per-atom counts, prefix sum, fill
-  k_hb_list<<<nblk((int64_t)N * 32, HB_THREADS), HB_THREADS, 0, s>>>(N, c->g, w.cell_start, w.spos, w.stype, w.brow, w.perm,
-                                                                    il, w.bc_len, nullptr, nullptr, nullptr, w.st);
+  unsigned* hn = reinterpret_cast<unsigned*>(w.ilist_tot + 2);
+  if (cudaError_t e_ = cudaMemsetAsync(hn, 0, sizeof(unsigned), s)) return fail_cuda(e_);
+  k_hb_collect<<<nblk(N, TPB), TPB, 0, s>>>(N, w.stype, w.brow, w.perm, il.h_type, w.bc_len, w.cell_of, hn);
+  k_hb_list<<<148 * 8, HB_THREADS, 0, s>>>(w.cell_of, hn, c->g, w.cell_start, w.spos, w.stype, w.perm, il, w.bc_len,
+                                           nullptr, nullptr, nullptr, w.st);
   if (scan<int, long long>(c, w.bc_len, N, reinterpret_cast<long long*>(hb_off), s) != cudaSuccess)
     return fail_cuda(cudaGetLastError());
   if (hb_z)
-    k_hb_list<<<nblk((int64_t)N * 32, HB_THREADS), HB_THREADS, 0, s>>>(N, c->g, w.cell_start, w.spos, w.stype, w.brow,
-                                                                      w.perm, il, nullptr, nullptr,
-                                                                      reinterpret_cast<const long long*>(hb_off), hb_z,
-                                                                      w.st);
+    k_hb_list<<<148 * 8, HB_THREADS, 0, s>>>(w.cell_of, hn, c->g, w.cell_start, w.spos, w.stype, w.perm, il, nullptr,
+                                             nullptr, reinterpret_cast<const long long*>(hb_off), hb_z, w.st);
   if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
   return read_status(c, s, true);
 }
