@@ -145,6 +145,10 @@ struct WS {
   unsigned long long* lb_status;  // look-back scan tile status
   unsigned* lb_ticket;            // look-back scan tile ticket
   unsigned* bin_ticket;           // k_bin last-block ticket (fused cell scan)
+  int* blk_pairs;    // nblock  half-list entries per home block (list build; nonbonded plan)
+  int* blkrow;       // nblock  shared row counters of split home blocks
+  int* units;        // NB_UNIT_SPLIT * nblock  planned nonbonded units (block | n_b << 24)
+  int* nunits;       // 4       [0]: planned unit count
   unsigned long long* ilist_tot;  // 2: interaction-list totals (reax_interaction_counts)
   DevParams* prm;
   Status* st;

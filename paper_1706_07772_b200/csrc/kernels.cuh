@@ -16,6 +16,45 @@ __device__ __forceinline__ void set_flag(Status* st, int f) { atomicOr(&st->flag
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// CTA timeline instrumentation (measurement builds only, -DREAX_TIMELINE):
+// per CTA of k_nbr_build (kind 0) and k_nonbonded (kind 1), the SM and the
+// global-timer stamps at start, end of setup and end; read by
+// reax_timeline_read (tools/timeline.py).
+#ifdef REAX_TIMELINE
+constexpr int TL_MAX = 1 << 16;
+__device__ unsigned long long g_tl[2][TL_MAX][8];   // 0 start, 1 setup done, 2 end, 3 SM | work << 16, 4-7 kernel phases
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_mark(int kind, int slot, unsigned long long work = 0) {
+  if (threadIdx.x == 0 && blockIdx.x < TL_MAX) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    g_tl[kind][blockIdx.x][slot] = tl_now();
+    if (slot == 0) {
+      g_tl[kind][blockIdx.x][6] = ~0ull;
+      g_tl[kind][blockIdx.x][7] = 0ull;
+    }
+    if (slot == 1) g_tl[kind][blockIdx.x][3] = sm | (work << 16);   // SM, work units of the CTA
+  }
+}
+#define TL_MARK(kind, slot, ...) tl_mark(kind, slot, ##__VA_ARGS__)
+// per-warp extremes (slot 6: first warp done, atomicMin; slot 7: last warp done)
+__device__ __forceinline__ void tl_warp_done(int kind) {
+  if ((threadIdx.x & 31) == 0 && blockIdx.x < TL_MAX) {
+    const unsigned long long t = tl_now();
+    atomicMin(&g_tl[kind][blockIdx.x][6], t);
+    atomicMax(&g_tl[kind][blockIdx.x][7], t);
+  }
+}
+#define TL_WARP_DONE(kind) tl_warp_done(kind)
+#else
+#define TL_MARK(kind, slot, ...) ((void)0)
+#define TL_WARP_DONE(kind) ((void)0)
+#endif
+
 // a1: x <- x - L floor(x/L), a result equal to L (or below 0 by rounding) -> 0.
 // Explicitly rounded operations keep it bit-identical to any IEEE scalar code.
 __device__ __forceinline__ double wrap_coord(double x, double L) {
@@ -305,9 +344,14 @@ __device__ __forceinline__ double wrap_key(double x, double L) { return isfinite
 __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int* __restrict__ perm,
                               const double* __restrict__ pos, const int* __restrict__ type, Grid g, int nt,
                               int* __restrict__ iperm, double4* __restrict__ spos, float4* __restrict__ sloc,
-                              int* __restrict__ stype, const double* __restrict__ qin, Status* st) {
+                              int* __restrict__ stype, const double* __restrict__ qin, Status* st,
+                              int* __restrict__ blk_pairs, int nblock) {
   pdl_wait();
   pdl_trigger();
+  if (blk_pairs) {   // per-block pair counts of the next list build start at zero
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < nblock) blk_pairs[t] = 0;
+  }
   int c = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   int lane = threadIdx.x & 31;
   if (c >= ncell) return;
@@ -472,6 +516,7 @@ struct NbrSmem {
   int gbase[NHOME + 1];   // first row group of each home sub-cell (groups of NBR_G rows)
   int ncs[NBR_THREADS / 32][8];   // per warp: bond-candidate counters of its group's rows
   int next_row;
+  int pairs;                      // half-list entries of this CTA's rows (nonbonded work plan)
 };
 
 // Per-kernel constants of the half-list candidate test.
@@ -684,8 +729,9 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, con
 __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, const int* __restrict__ cell_start,
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
-    int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st) {
+    int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st, int* __restrict__ blk_pairs) {
   pdl_wait();
+  TL_MARK(0, 0);
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NbrSmem S;
   const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
@@ -707,6 +753,7 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
     }
     S.gbase[NHOME] = gb;
     S.next_row = 0;
+    S.pairs = 0;
   }
   __syncthreads();
   if (W > window_cap) {
@@ -747,6 +794,7 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
   }
   if (threadIdx.x < 32) cand[W + threadIdx.x] = make_float4(1e30f, 1e30f, 1e30f, 0.f);  // sentinel
   __syncthreads();
+  TL_MARK(0, 1, W);
   const SlotJK sl{cand_j, cand_k};
   // groups of NBR_G consecutive rows of one home sub-cell; this CTA takes
   // groups split, split + nsplit, ...
@@ -777,8 +825,22 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
       if (l > row_cap) { set_flag(st, ST_ROW_OVF); atomicMax(&st->max_row, l); }
       if (c > cand_cap) { set_flag(st, ST_CAND_OVF); atomicMax(&st->max_cand, c); }
     }
+    if (blk_pairs) {
+      int t = 0;
+#pragma unroll
+      for (int r = 0; r < NBR_G; ++r) t += r < nrow ? min(len[r], row_cap) : 0;
+      if (lane == 0) atomicAdd(&S.pairs, t);
+    }
     __syncwarp();   // ncs is reset by the warp's next group
   }
+  if (blk_pairs) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(blk_pairs + blk, S.pairs);
+  }
+#ifdef REAX_TIMELINE
+  __syncthreads();
+  TL_MARK(0, 2);
+#endif
 }
 
 // =================================================== a4 bond orders (B1-B2)
@@ -1222,6 +1284,86 @@ constexpr int NB_WARPS = NB_THREADS / 32;
 #define NB_MINB 2   // 2 CTAs x 8 warps at <= 128 registers (3 CTAs at 80 registers spills; measured slower)
 #endif
 
+// Work plan of the nonbonded kernel for small grids (a few CTAs per SM slot:
+// there the kernel's length is set by its heaviest home blocks).  Block b,
+// with p_b half-list entries (summed by the list build), becomes n_b =
+// min(NB_UNIT_SPLIT, ceil(p_b / T)) units, T = frac * (sum p) / slots; the
+// n_b CTAs of a block share its rows through a global row counter.  Units
+// are launched by work p_b / n_b, largest first (ties: block index), so the
+// CTA order is longest-processing-time-first.  Which CTA evaluates a row does
+// not change any result (forces are fixed-point sums, energies per-row
+// partials), so the plan only moves time.
+constexpr int PLAN_THREADS = 1024;
+constexpr int NB_PLAN_MAX = PLAN_THREADS;   // home blocks (one per thread)
+constexpr int NB_UNIT_SPLIT = 4;
+__global__ void __launch_bounds__(PLAN_THREADS) k_nb_plan(int nblock, const int* __restrict__ blk_pairs, int slots,
+                                                          float frac, int umax, int* __restrict__ units,
+                                                          int* __restrict__ nunits, int* __restrict__ blkrow) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int wk[PLAN_THREADS];
+  __shared__ int off[PLAN_THREADS];
+  __shared__ long long psum[PLAN_THREADS / 32];
+  __shared__ int wsum[PLAN_THREADS / 32];
+  const int b = threadIdx.x, lane = b & 31, w = b >> 5;
+  int p = 0;
+  if (b < nblock) {
+    p = blk_pairs[b];
+    blkrow[b] = 0;
+  }
+  long long t = p;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) psum[w] = t;
+  __syncthreads();
+  long long tot = 0;
+  for (int q = 0; q < PLAN_THREADS / 32; ++q) tot += psum[q];
+  const long long T = max(1ll, (long long)(frac * (double)tot / slots));
+  int ns = 0;
+  if (b < nblock) ns = (int)min((long long)NB_UNIT_SPLIT, max(1ll, (p + T - 1) / T));
+  const int wu = b < nblock ? p / ns : 0;
+  wk[b] = wu;
+  __syncthreads();
+  int rank = 0;
+  if (b < nblock)
+    for (int q = 0; q < nblock; ++q) {
+      const int x = wk[q];
+      rank += (x > wu) || (x == wu && q < b);
+    }
+  off[b] = 0;
+  __syncthreads();
+  if (b < nblock) off[rank] = ns;
+  __syncthreads();
+  // exclusive scan of the unit counts in rank order
+  const int x = off[b];
+  int y = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int z = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) y += z;
+  }
+  if (lane == 31) wsum[w] = y;
+  __syncthreads();
+  int base = 0, total = 0;
+  for (int q = 0; q < PLAN_THREADS / 32; ++q) {
+    base += q < w ? wsum[q] : 0;
+    total += wsum[q];
+  }
+  __syncthreads();
+  off[b] = base + y - x;
+  __syncthreads();
+  const bool fits = total <= umax;   // else one unit per block (always fits)
+  if (b < nblock) {
+    if (fits) {
+      const int o = off[rank];
+      for (int k = 0; k < ns; ++k) units[o + k] = b | (ns << 24);
+    } else {
+      units[b] = b | (1 << 24);
+    }
+  }
+  if (b == 0) *nunits = fits ? total : nblock;
+}
+
 constexpr int NB_MAX_ROWS = 256;   // rows of one (block, split) work unit that are ranked
 struct NBSmem {
   WinSmem W;
@@ -1248,11 +1390,25 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
     unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
-    double2* __restrict__ erow, int nsplit, Status* st) {
+    double2* __restrict__ erow, int nsplit, Status* st, const int* __restrict__ units, const int* __restrict__ nunits,
+    int* __restrict__ blkrow) {
   pdl_wait();
+  TL_MARK(1, 0);
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ NBSmem S;
-  const int blk = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
+  int blk, split;
+  int* gctr = nullptr;   // global row counter of a block shared by several CTAs
+  if (units) {           // planned units (k_nb_plan): all rows of block blk, shared by ns CTAs
+    if ((int)blockIdx.x >= *nunits) return;
+    const int u = units[blockIdx.x];
+    blk = u & 0xFFFFFF;
+    split = 0;
+    nsplit = 1;
+    if ((u >> 24) > 1) gctr = blkrow + blk;
+  } else {
+    blk = blockIdx.x / nsplit;
+    split = blockIdx.x % nsplit;
+  }
   const int nt = prm->nt;
   double* ET = reinterpret_cast<double*>(dyn);                  // exp table
   double2* LT = reinterpret_cast<double2*>(ET + EXP_TBL);       // log table
@@ -1272,6 +1428,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   kc.invR = prm->invR; kc.phalf = 0.5 * prm->p_vdw; kc.inv_p = prm->inv_p; kc.m140invR = -140.0 * prm->invR;
   const double C = prm->C;
   const int W = build_window(S.W, blk, g, cell_start);
+  TL_MARK(1, 4);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (W > window_cap) {
     if (threadIdx.x == 0) {
@@ -1311,6 +1468,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     S.next_row = 0;
   }
   __syncthreads();
+  TL_MARK(1, 5);
   // phase 2: slot info (flattened over slots: the type loads are independent),
   // row ranking (longest first; ties by home order)
 #pragma unroll 4
@@ -1330,6 +1488,14 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     S.rlen[rank] = my_len;
   }
   __syncthreads();
+#ifdef REAX_TIMELINE
+  {
+    unsigned long long pairs = 0;
+    if (threadIdx.x == 0)
+      for (int t = 0; t < nsorted; ++t) pairs += S.rlen[t];
+    TL_MARK(1, 1, pairs);
+  }
+#endif
   const bool has_shift = S.W.has_shift != 0;
   const double FIXS = c_nb[25], MAGIC = c_nb[26], FLIM = c_nb[27];
   bool bad = false;
@@ -1340,7 +1506,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   // the result independent of which warp runs a row)
   auto row_info = [&](int& si, int& len) -> bool {
     int r = 0;
-    if (lane == 0) r = atomicAdd(&S.next_row, 1);
+    if (lane == 0) r = gctr ? atomicAdd(gctr, 1) : atomicAdd(&S.next_row, 1);
     r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= nrows) return false;
     if (r < nsorted) {
@@ -1434,6 +1600,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     __syncwarp();   // the buffer of this row is refilled two rows later
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  TL_WARP_DONE(1);
   if (__any_sync(0xffffffffu, bad) && lane == 0) S.bad = 1;
   __syncthreads();
   if (threadIdx.x == 0 && S.bad) set_flag(st, ST_RANGE);
@@ -1446,6 +1613,10 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
       if (v != 0) atomicAdd(&gf[c][j], (unsigned long long)v);
     }
   }
+#ifdef REAX_TIMELINE
+  __syncthreads();
+  TL_MARK(1, 2);
+#endif
 }
 
 // a8 finalize, one kernel: un-permute the forces, force[perm[s]] =

@@ -363,6 +363,11 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
                                           ((size_t)nblk(std::max<int64_t>((int64_t)N + 1, (int64_t)g.ncell + 1), LB_TILE) + 1));
   t.lb_ticket = (unsigned*)take(sizeof(unsigned) * 4);
   t.bin_ticket = (unsigned*)take(sizeof(unsigned) * 4);
+  const size_t nplan = g.nblock <= NB_PLAN_MAX ? (size_t)g.nblock : 0;   // planned nonbonded units (small grids)
+  t.blk_pairs = (int*)take(sizeof(int) * nplan);
+  t.blkrow = (int*)take(sizeof(int) * nplan);
+  t.units = (int*)take(sizeof(int) * NB_UNIT_SPLIT * nplan);
+  t.nunits = (int*)take(sizeof(int) * 4);
   t.ilist_tot = (unsigned long long*)take(sizeof(unsigned long long) * 4);   // [2]: H-atom count (k_hb_collect)
   t.prm = (DevParams*)take(sizeof(DevParams));
   t.st = (Status*)take(sizeof(Status));
@@ -417,6 +422,11 @@ struct reax_ctx {
   int launches_cur = 0;
   int nsplit = 1;
   int nsplit_nbr = 1;
+  // planned nonbonded units (k_nb_plan) for grids of at most NB_PLAN_MAX blocks
+  bool nb_plan = false;
+  int nb_slots = 0;     // resident nonbonded CTAs (SMs x NB_MINB)
+  int nb_umax = 0;      // launched CTAs (>= planned units; the rest exit)
+  float nb_frac = 1.0f; // unit target T = frac * pairs / slots
   // fork/join of reax_step (bond chain beside the nonbonded kernel)
   // reax_step_host replays one CUDA graph (copies in, step, copies out) per
   // unchanged (host buffers, box, parameters, workspace, mode)
@@ -655,7 +665,8 @@ void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, const do
     launch_k(c, k_scatter, nblk(N, TPB), TPB, 0, s, N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
     LAUNCH(c);
     launch_k(c, k_cell_gather, nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s, g.ncell, w.cell_start, w.perm, pos, type, g, nt,
-                                                               w.iperm, w.spos, w.sloc, w.stype, q, w.st);
+                                                               w.iperm, w.spos, w.sloc, w.stype, q, w.st,
+             c->nb_plan ? w.blk_pairs : nullptr, g.nblock);
     LAUNCH(c);
   }
 }
@@ -667,7 +678,7 @@ void launch_nbr(reax_ctx* c, cudaStream_t s) {
   Timer t(c, 1, s);
   launch_k(c, k_nbr_build, g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s,
            g, w.cell_start, w.sloc, w.spos, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, w.bc, w.bc_len,
-           c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st);
+           c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st, c->nb_plan ? w.blk_pairs : nullptr);
   LAUNCH(c);
 }
 
@@ -756,9 +767,15 @@ void launch_nb(reax_ctx* c, int nt, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
   Timer t(c, 4, s);
-  launch_k(c, k_nonbonded, g.nblock * c->nsplit, NB_THREADS, nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s,
-           g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy,
-           w.sfz, w.erow, c->nsplit, w.st);
+  if (c->nb_plan) {
+    launch_k(c, k_nb_plan, 1, PLAN_THREADS, 0, s, g.nblock, (const int*)w.blk_pairs, c->nb_slots, c->nb_frac, c->nb_umax,
+             w.units, w.nunits, w.blkrow);
+    LAUNCH(c);
+  }
+  launch_k(c, k_nonbonded, c->nb_plan ? c->nb_umax : g.nblock * c->nsplit, NB_THREADS,
+           nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s, g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len,
+           c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy, w.sfz, w.erow, c->nsplit, w.st,
+           c->nb_plan ? (const int*)w.units : nullptr, c->nb_plan ? (const int*)w.nunits : nullptr, w.blkrow);
   LAUNCH(c);
 }
 
@@ -1008,6 +1025,15 @@ reax_status do_ilist_lists(reax_ctx* c, const reax_ilist_params* p, int64_t* ang
 // ==================================================================== ABI
 extern "C" {
 
+#ifdef REAX_TIMELINE
+// measurement builds only: copy the CTA timeline (see TL_MARK) to host,
+// [2][TL_MAX][4] unsigned 64-bit words; returns TL_MAX
+int reax_timeline_read(void* host) {
+  if (cudaMemcpyFromSymbol(host, g_tl, sizeof(g_tl)) != cudaSuccess) return -1;
+  return TL_MAX;
+}
+#endif
+
 const char* reax_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda); }
 
 
@@ -1125,6 +1151,16 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   ctx->nsplit = choose_split(g.nblock, 2, "REAX_CTAS_PER_SM");
   ctx->nsplit_nbr = choose_split(g.nblock, 4, "REAX_NBR_CTAS_PER_SM");
   if (const char* e = getenv("REAX_NBR_SPLIT")) ctx->nsplit_nbr = std::max(1, std::min(MAX_SPLIT, atoi(e)));
+  {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    ctx->nb_slots = nsm * NB_MINB;
+    const char* pe = getenv("REAX_NB_PLAN");   // "0": static grid (measurement)
+    ctx->nb_plan = g.nblock > 0 && g.nblock <= NB_PLAN_MAX && !(pe && atoi(pe) == 0);
+    if (const char* fe = getenv("REAX_NB_UNIT_FRAC")) ctx->nb_frac = std::max(0.05f, (float)atof(fe));
+    ctx->nb_umax = (int)std::min<long long>((long long)NB_UNIT_SPLIT * g.nblock,
+                                            g.nblock + (long long)std::ceil(2.0 * ctx->nb_slots / ctx->nb_frac));
+  }
   ctx->cut = *cut;
   ctx->prm_valid = false;
   ctx->bep_valid = false;
