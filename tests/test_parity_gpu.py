@@ -270,3 +270,28 @@ def test_gpu_invariances(params):
     assert ctx3.pair_count() == (P, B)
     assert np.all(np.abs(E3 - E) <= 1e-10 * np.abs(E))
     assert np.all(np.abs(F3 - F[perm]) <= 1e-8 * (1 + np.abs(F[perm])))
+
+
+def test_plan_interleaving_bitwise(params):
+    """The nonbonded work plan (heavy home blocks split into units that share
+    a global row counter) never changes a result: steps, separate nonbonded
+    calls and steps again on one context give bitwise the forces and energies
+    of a fresh context, also for a translated system (another plan)."""
+    import paper_1706_07772_b200 as rx
+    s = gen.make_config(1)
+    dev = torch.device("cuda:0")
+    pos, typ, q = (torch.from_numpy(x).to(dev) for x in (s.pos, s.type, s.q))
+    ref = rx.Reax(len(s.pos), s.box, params, CUT, device=dev)
+    F0, E0 = (t.clone() for t in ref.step(pos, typ, q))
+    ctx = rx.Reax(len(s.pos), s.box, params, CUT, device=dev)
+    for k in range(3):
+        F, E = ctx.step(pos, typ, q)
+        assert torch.equal(F, F0) and torch.equal(E, E0), k
+        F, E = ctx.nonbonded(pos, typ, q)
+        Fn, En = ctx.step(pos, typ, q)
+        assert torch.equal(Fn, F0) and torch.equal(En, E0), k
+    pos2 = torch.from_numpy(oracle.wrap(s.pos + np.array([3.3, -1.1, 7.7]), s.box)).to(dev)
+    F1, E1 = (t.clone() for t in ref.step(pos2, typ, q))
+    for k in range(3):
+        F, E = ctx.step(pos2, typ, q)
+        assert torch.equal(F, F1) and torch.equal(E, E1), k

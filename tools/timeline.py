@@ -55,6 +55,15 @@ def analyse(tl, name):
         print(f"  rows    {pc((ph[:, 2] - t1) / 1e3)} (to first warp done)")
         print(f"  warp tail {pc((ph[:, 3] - ph[:, 2]) / 1e3)} (first to last warp done)")
         print(f"  flush   {pc((t2 - ph[:, 3]) / 1e3)}")
+    if ph[:, 3].max() > 0:
+        # slot-time accounting over the span (2 resident CTAs per SM = full)
+        slots = 148 * max(1, int(round(np.percentile([((a <= m) & (e > m)).sum() for m in [span * 0.1, span * 0.2, span * 0.3]], 50) / 148)))
+        rows_t = ((ph[:, 2] - t1) / 1e3).sum() + 0.5 * ((ph[:, 3] - ph[:, 2]) / 1e3).sum()
+        setup_t = (b - a).sum()
+        tail_t = 0.5 * ((ph[:, 3] - ph[:, 2]) / 1e3).sum() + ((t2 - ph[:, 3]) / 1e3).sum()
+        cap = slots * span
+        print(f"  slot-time ({slots} slots x span): rows {rows_t / cap:.3f}, setup {setup_t / cap:.3f}, "
+              f"warp tail + flush {tail_t / cap:.3f}, empty {1 - (rows_t + setup_t + tail_t) / cap:.3f}")
     print(f"  busy SM-time fraction {busy / (148 * span):.3f}")
     edges = np.linspace(0, span, 11)
     mid = 0.5 * (edges[1:] + edges[:-1])
