@@ -1301,7 +1301,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_nb_plan(int nblock, const int*
                                                           int* __restrict__ nunits, int* __restrict__ blkrow) {
   pdl_wait();
   pdl_trigger();
-  __shared__ int wk[PLAN_THREADS];
+  __shared__ __align__(16) int wk[PLAN_THREADS];
   __shared__ int off[PLAN_THREADS];
   __shared__ long long psum[PLAN_THREADS / 32];
   __shared__ int wsum[PLAN_THREADS / 32];
@@ -1321,15 +1321,18 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_nb_plan(int nblock, const int*
   const long long T = max(1ll, (long long)(frac * (double)tot / slots));
   int ns = 0;
   if (b < nblock) ns = (int)min((long long)NB_UNIT_SPLIT, max(1ll, (p + T - 1) / T));
-  const int wu = b < nblock ? p / ns : 0;
-  wk[b] = wu;
+  // unique sort key: unit work, then lower block index first (work < 2^21)
+  const int key = b < nblock ? ((min(p / ns, (1 << 21) - 1) << 10) | (PLAN_THREADS - 1 - b)) : -1;
+  wk[b] = key;
   __syncthreads();
   int rank = 0;
-  if (b < nblock)
-    for (int q = 0; q < nblock; ++q) {
-      const int x = wk[q];
-      rank += (x > wu) || (x == wu && q < b);
+  if (b < nblock) {
+    const int4* k4 = reinterpret_cast<const int4*>(wk);
+    for (int q = 0; q < (nblock + 3) >> 2; ++q) {   // entries >= nblock hold -1
+      const int4 v = k4[q];
+      rank += (v.x > key) + (v.y > key) + (v.z > key) + (v.w > key);
     }
+  }
   off[b] = 0;
   __syncthreads();
   if (b < nblock) off[rank] = ns;
