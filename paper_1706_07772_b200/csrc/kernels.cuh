@@ -50,9 +50,23 @@ __device__ __forceinline__ void tl_warp_done(int kind) {
   }
 }
 #define TL_WARP_DONE(kind) tl_warp_done(kind)
+// first CTA start (before griddepcontrol.wait) / last CTA end of the step's
+// other kernels (id: tools/timeline.py SPANS)
+__device__ unsigned long long g_tl_span[8][2];
+struct TLSpan {
+  int id;
+  __device__ __forceinline__ explicit TLSpan(int i) : id(i) {
+    if (threadIdx.x == 0) atomicMin(&g_tl_span[id][0], tl_now());
+  }
+  __device__ __forceinline__ ~TLSpan() {
+    if (threadIdx.x == 0) atomicMax(&g_tl_span[id][1], tl_now());
+  }
+};
+#define TL_SPAN(id) TLSpan tl_span_(id)
 #else
 #define TL_MARK(kind, slot, ...) ((void)0)
 #define TL_WARP_DONE(kind) ((void)0)
+#define TL_SPAN(id) ((void)0)
 #endif
 
 // a1: x <- x - L floor(x/L), a result equal to L (or below 0 by rounding) -> 0.
@@ -174,6 +188,7 @@ constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_MASK =
 __global__ void __launch_bounds__(LB_THREADS) k_scan_lookback(const int* __restrict__ in, int n, int* __restrict__ out,
                                                               unsigned long long* __restrict__ status,
                                                               unsigned* __restrict__ ticket) {
+  TL_SPAN(1);
   pdl_wait();
   pdl_trigger();
   __shared__ int tile_id;
@@ -870,6 +885,7 @@ __global__ void k_bond_eval(int n, const double4* __restrict__ spos, const int* 
                             const DevParams* __restrict__ prm, int* __restrict__ bc, const int* __restrict__ bc_len,
                             double4* __restrict__ bc_raw, int cand_cap, int* __restrict__ bdeg,
                             unsigned long long* __restrict__ scan_status, int scan_tiles) {
+  TL_SPAN(0);
   pdl_wait();
   pdl_trigger();
   clear_status(scan_status, scan_tiles);
@@ -927,6 +943,7 @@ __global__ void k_bond_fill(int n, const int* __restrict__ bc, const int* __rest
                             const int* __restrict__ perm, int* __restrict__ bdeg, int* __restrict__ ucol,
                             int* __restrict__ ukey, int* __restrict__ uown, double4* __restrict__ uraw,
                             long long bond_cap, Status* st) {
+  TL_SPAN(2);
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x & 31;
@@ -968,6 +985,7 @@ __global__ void k_bond_rank(const int* __restrict__ brow, const int* __restrict_
                             const int* __restrict__ uown, const double4* __restrict__ uraw, int* __restrict__ bcol,
                             int* __restrict__ bkey, int* __restrict__ bown, double* __restrict__ bo, long long bond_cap,
                             const Status* __restrict__ st) {
+  TL_SPAN(3);
   pdl_wait();
   pdl_trigger();
   long long B = st->bonds < bond_cap ? st->bonds : bond_cap;
@@ -991,6 +1009,7 @@ __global__ void k_bond_rank(const int* __restrict__ brow, const int* __restrict_
 __global__ void k_bond_delta(int n, const int* __restrict__ brow, const int* __restrict__ stype,
                              const DevParams* __restrict__ prm, const double* __restrict__ bo,
                              double2* __restrict__ delta, long long bond_cap) {
+  TL_SPAN(4);
   pdl_wait();
   pdl_trigger();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1011,6 +1030,7 @@ __global__ void k_bond_correct(const int* __restrict__ brow, const int* __restri
                                const int* __restrict__ bcol, const int* __restrict__ bkey, const int* __restrict__ bown,
                                int* __restrict__ bmir, double* __restrict__ bo, const double2* __restrict__ delta,
                                long long bond_cap, const Status* __restrict__ st) {
+  TL_SPAN(5);
   pdl_wait();
   pdl_trigger();
   __shared__ BOPair sbo[NTP_MAX];
@@ -1299,6 +1319,7 @@ constexpr int NB_UNIT_SPLIT = 4;
 __global__ void __launch_bounds__(PLAN_THREADS) k_nb_plan(int nblock, const int* __restrict__ blk_pairs, int slots,
                                                           float frac, int umax, int* __restrict__ units,
                                                           int* __restrict__ nunits, int* __restrict__ blkrow) {
+  TL_SPAN(7);
   pdl_wait();
   pdl_trigger();
   __shared__ __align__(16) int wk[PLAN_THREADS];
@@ -1648,6 +1669,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __re
     unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
     double* __restrict__ force, int nparts, const double2* __restrict__ epart, double* __restrict__ part,
     unsigned* __restrict__ ticket, double* __restrict__ energy, int ne, Status* st) {
+  TL_SPAN(6);
   pdl_wait();
   pdl_trigger();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;

@@ -1030,7 +1030,14 @@ extern "C" {
 // [2][TL_MAX][4] unsigned 64-bit words; returns TL_MAX
 int reax_timeline_read(void* host) {
   if (cudaMemcpyFromSymbol(host, g_tl, sizeof(g_tl)) != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol((char*)host + sizeof(g_tl), g_tl_span, sizeof(g_tl_span)) != cudaSuccess) return -1;
   return TL_MAX;
+}
+// reset the span stamps (first start = max, last end = 0)
+int reax_timeline_reset(void) {
+  unsigned long long v[8][2];
+  for (int i = 0; i < 8; ++i) { v[i][0] = ~0ull; v[i][1] = 0ull; }
+  return cudaMemcpyToSymbol(g_tl_span, v, sizeof(v)) == cudaSuccess ? 0 : -1;
 }
 #endif
 

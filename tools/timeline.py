@@ -20,6 +20,10 @@ import gen  # noqa: E402
 import paper_1706_07772_b200 as rx  # noqa: E402
 
 
+SPANS = ("k_bond_eval", "k_scan_lookback", "k_bond_fill", "k_bond_rank", "k_bond_delta", "k_bond_correct",
+         "k_finalize", "k_nb_plan")
+
+
 def analyse(tl, name):
     t0, t1, t2, sm, work = tl[:, 0], tl[:, 1], tl[:, 2], tl[:, 3] & 0xFFFF, tl[:, 3] >> 16
     ok = (t0 > 0) & (t2 >= t0)
@@ -98,9 +102,14 @@ def main():
     for _ in range(5):
         ctx.step(pos, typ, q)
     torch.cuda.synchronize()
-    buf = np.zeros((2, 1 << 16, 8), np.uint64)
+    lib.reax_timeline_reset()
+    ctx.step(pos, typ, q)
+    torch.cuda.synchronize()
+    buf = np.zeros(2 * (1 << 16) * 8 + 16, np.uint64)
     n = lib.reax_timeline_read(ctypes.c_void_p(buf.ctypes.data))
     assert n == 1 << 16
+    spans = buf[2 * (1 << 16) * 8:].reshape(8, 2).astype(np.int64)
+    buf = buf[:2 * (1 << 16) * 8].reshape(2, 1 << 16, 8)
     analyse(buf[0].astype(np.int64), "k_nbr_build")
     analyse(buf[1].astype(np.int64), "k_nonbonded")
     s0 = buf[0][:, 0][buf[0][:, 0] > 0].min()
@@ -108,6 +117,12 @@ def main():
     e0 = buf[0][:, 2].max()
     print("nonbonded first start - list first start %.1f us; list last end - nonbonded first start %.1f us"
           % ((s1 - s0) / 1e3, (int(e0) - int(s1)) / 1e3))
+    e1 = int(buf[1][:, 2].max())
+    print("nonbonded last end: %.1f us after the list start" % ((e1 - int(s0)) / 1e3))
+    for i, name in enumerate(SPANS):
+        a, b = spans[i]
+        if b > 0:
+            print(f"  {name:16s} first start {(a - int(s0)) / 1e3:7.1f}  last end {(b - int(s0)) / 1e3:7.1f} us")
 
 
 if __name__ == "__main__":
