@@ -1392,7 +1392,7 @@ constexpr int NB_MAX_ROWS = 256;   // rows of one (block, split) work unit that 
 struct NBSmem {
   WinSmem W;
   int bad;
-  int rlen0[NB_MAX_ROWS];        // row lengths in home order (ranking input)
+  __align__(16) int rkey[NB_MAX_ROWS];   // ranking keys in home order: length << 8 | (255 - index); -1 past the rows
   int order[NB_MAX_ROWS];        // row window slots, longest row first
   int rlen[NB_MAX_ROWS];         // their lengths
   int next_row;                  // dynamic row counter
@@ -1481,7 +1481,9 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     row_of(S.W, split + threadIdx.x * nsplit, h, my_si);
     const int k = c_win.home_k[h];
     my_len = nbr_len[S.W.start[k] + (my_si - S.W.slot[k])];
-    S.rlen0[threadIdx.x] = my_len;
+    S.rkey[threadIdx.x] = (my_len << 8) | (NB_MAX_ROWS - 1 - (int)threadIdx.x);
+  } else if ((int)threadIdx.x < NB_MAX_ROWS) {
+    S.rkey[threadIdx.x] = -1;
   }
   {
     uint4* z = reinterpret_cast<uint4*>(fa);          // fa and fb are contiguous: 6 window_cap words
@@ -1495,18 +1497,21 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   TL_MARK(1, 5);
   // phase 2: slot info (flattened over slots: the type loads are independent),
   // row ranking (longest first; ties by home order)
-#pragma unroll 4
+#pragma unroll 8
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
     const int k = kmap[t];
     const int j = S.W.start[k] + (t - S.W.slot[k]);
     sinfo[t] = make_int2(j, k | (stype[j] << 8));
   }
   static_assert(NB_MAX_ROWS <= NB_THREADS, "one ranked row per thread");
-  if ((int)threadIdx.x < nsorted) {
+  static_assert(NB_MAX_ROWS <= 256, "ranking keys: 8-bit index");
+  if ((int)threadIdx.x < nsorted) {   // longest first, ties by home order: count the greater keys
+    const int key = (my_len << 8) | (NB_MAX_ROWS - 1 - (int)threadIdx.x);
+    const int4* k4 = reinterpret_cast<const int4*>(S.rkey);
     int rank = 0;
-    for (int t = 0; t < nsorted; ++t) {
-      const int lt = S.rlen0[t];
-      rank += (lt > my_len) || (lt == my_len && t < (int)threadIdx.x);
+    for (int q = 0; q < (nsorted + 3) >> 2; ++q) {
+      const int4 v = k4[q];
+      rank += (v.x > key) + (v.y > key) + (v.z > key) + (v.w > key);
     }
     S.order[rank] = my_si;
     S.rlen[rank] = my_len;
