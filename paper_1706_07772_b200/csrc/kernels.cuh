@@ -6,6 +6,9 @@
 namespace rx {
 
 __constant__ WindowTables c_win;
+// copy of c_win.wu in global memory: read with one index per thread (a
+// divergent constant-bank read would serialise over the warp)
+__device__ int g_win_wu[NWB];
 
 __device__ __forceinline__ void set_flag(Status* st, int f) { atomicOr(&st->flags, f); }
 
@@ -456,14 +459,15 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
     bool need = false;
 #pragma unroll
     for (int h = 0; h < NHOME; ++h) need |= ((hok >> h) & 1u) && ((c_win.mask[h][k >> 5] >> (k & 31)) & 1u);
-    int wb = c_win.wu[k];
+    int wb = __ldg(g_win_wu + k);
     int wv[3] = {wb % WB, (wb / WB) % WB, wb / (WB * WB)};
     int cc[3];
     double sh[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      int u = base[a] + wv[a] - SR;          // unwrapped sub-cell
-      int m = u >= 0 ? u / g.nc[a] : -((-u + g.nc[a] - 1) / g.nc[a]);  // floor(u / nc)
+      int u = base[a] + wv[a] - SR;          // unwrapped sub-cell, in [-SR, nc + HB + SR - 2]
+      // floor(u / nc) in {-1, 0, 1}: nc >= 4 (L > 2 r_nonb, sub-cells >= r_nonb / 2)
+      int m = u < 0 ? -1 : (u >= g.nc[a] ? 1 : 0);
       cc[a] = u - m * g.nc[a];
       sh[a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
       my_shift |= need && (m != 0);

@@ -130,6 +130,7 @@ cudaError_t ensure_tables() {
   if (dev < 64 && g_tab_done[dev]) return cudaSuccess;
   WindowTables T = make_tables();
   e = cudaMemcpyToSymbol(c_win, &T, sizeof(T));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_win_wu, T.wu, sizeof(T.wu));   // per-thread (divergent) reads
   if (e == cudaSuccess && dev < 64) g_tab_done[dev] = true;
   return e;
 }
