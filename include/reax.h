@@ -222,7 +222,7 @@ reax_status reax_check(reax_ctx* ctx, void* stream);
 /* Per-kernel timing with CUDA events on `stream` (off by default).
  * groups: 0 "bin" (wrap + counting sort), 1 "nbr" (k_nbr_build), 2 "bonds"
  * (bond evaluation, scan, fill, row sort + Delta'), 3 "bond_orders"
- * (k_bond_correct), 4 "nonbonded" (k_nonbonded alone), 5 "other" (charge
+ * (k_bond_correct), 4 "nonbonded" (k_nonbonded alone), 5 "other" (work plan, charge
  * gather, force un-permute, energy reduction), 6 "bond_energy" (NEXT-1,
  * reax_bond_energy). */
 #define REAX_NKERNELS 7

@@ -767,12 +767,13 @@ reax_status do_bond_orders(reax_ctx* c, const reax_params* prm, const reax_cutof
 void launch_nb(reax_ctx* c, int nt, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
-  Timer t(c, 4, s);
-  if (c->nb_plan) {
+  if (c->nb_plan) {   // timed with "other", so the nonbonded group times k_nonbonded alone
+    Timer tp(c, 5, s);
     launch_k(c, k_nb_plan, 1, PLAN_THREADS, 0, s, g.nblock, (const int*)w.blk_pairs, c->nb_slots, c->nb_frac, c->nb_umax,
              w.units, w.nunits, w.blkrow);
     LAUNCH(c);
   }
+  Timer t(c, 4, s);
   launch_k(c, k_nonbonded, c->nb_plan ? c->nb_umax : g.nblock * c->nsplit, NB_THREADS,
            nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s, g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len,
            c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy, w.sfz, w.erow, c->nsplit, w.st,
