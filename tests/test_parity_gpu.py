@@ -295,3 +295,12 @@ def test_plan_interleaving_bitwise(params):
     for k in range(3):
         F, E = ctx.step(pos2, typ, q)
         assert torch.equal(F, F1) and torch.equal(E, E1), k
+
+
+def test_plan_near_limit_grid(params):
+    """A 95 A box (19 sub-cells per axis: 10^3 = 1000 home blocks, just under
+    the 1024-block limit of the nonbonded work plan, with partial blocks on
+    three faces): full parity with the oracle through the planned grid."""
+    L = 95.0
+    s = gen.make_system(int(0.0978 * L ** 3), (L, L, L), gen.SEED_BASE + 1234)
+    full_parity(s, params)
