@@ -1167,8 +1167,12 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
     const char* pe = getenv("REAX_NB_PLAN");   // "0": static grid (measurement)
     ctx->nb_plan = g.nblock > 0 && g.nblock <= NB_PLAN_MAX && !(pe && atoi(pe) == 0);
     if (const char* fe = getenv("REAX_NB_UNIT_FRAC")) ctx->nb_frac = std::max(0.05f, (float)atof(fe));
+    // sum_b ceil(p_b / T) <= nblock + (sum p) / T ~ nblock + slots / frac (T = frac (sum p) / slots, rounded
+    // down): a small margin over that keeps the grid's empty CTAs (which delay the dispatch of the
+    // side-stream kernels behind it) few; a plan that does not fit falls back to one unit per block
     ctx->nb_umax = (int)std::min<long long>((long long)NB_UNIT_SPLIT * g.nblock,
-                                            g.nblock + (long long)std::ceil(2.0 * ctx->nb_slots / ctx->nb_frac));
+                                            g.nblock + (long long)std::ceil(ctx->nb_slots / ctx->nb_frac) + 16 +
+                                                g.nblock / 16);
   }
   ctx->cut = *cut;
   ctx->prm_valid = false;
