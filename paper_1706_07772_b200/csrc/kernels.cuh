@@ -1343,9 +1343,21 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_nb_plan(int nblock, const int*
   __syncthreads();
   long long tot = 0;
   for (int q = 0; q < PLAN_THREADS / 32; ++q) tot += psum[q];
-  const long long T = max(1ll, (long long)(frac * (double)tot / slots));
+  long long T = max(1ll, (long long)(frac * (double)tot / slots));
   int ns = 0;
-  if (b < nblock) ns = (int)min((long long)NB_UNIT_SPLIT, max(1ll, (p + T - 1) / T));
+  for (int pass = 0;; ++pass) {   // coarser units (T doubled) until the plan fits the launched grid
+    ns = b < nblock ? (int)min((long long)NB_UNIT_SPLIT, max(1ll, (p + T - 1) / T)) : 0;
+    int c = ns;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) wsum[w] = c;
+    __syncthreads();
+    int cnt = 0;
+    for (int q = 0; q < PLAN_THREADS / 32; ++q) cnt += wsum[q];
+    __syncthreads();
+    if (cnt <= umax || pass >= 8) break;
+    T *= 2;
+  }
   // unique sort key: unit work, then lower block index first (work < 2^21)
   const int key = b < nblock ? ((min(p / ns, (1 << 21) - 1) << 10) | (PLAN_THREADS - 1 - b)) : -1;
   wk[b] = key;

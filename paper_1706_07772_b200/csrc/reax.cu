@@ -428,6 +428,7 @@ struct reax_ctx {
   int nb_slots = 0;     // resident nonbonded CTAs (SMs x NB_MINB)
   int nb_umax = 0;      // launched CTAs (>= planned units; the rest exit)
   float nb_frac = 1.0f; // unit target T = frac * pairs / slots
+  float nb_grid_frac = 0.6f;   // launched units: nblock + grid_frac * slots / frac + 8
   // fork/join of reax_step (bond chain beside the nonbonded kernel)
   // reax_step_host replays one CUDA graph (copies in, step, copies out) per
   // unchanged (host buffers, box, parameters, workspace, mode)
@@ -1167,12 +1168,13 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
     const char* pe = getenv("REAX_NB_PLAN");   // "0": static grid (measurement)
     ctx->nb_plan = g.nblock > 0 && g.nblock <= NB_PLAN_MAX && !(pe && atoi(pe) == 0);
     if (const char* fe = getenv("REAX_NB_UNIT_FRAC")) ctx->nb_frac = std::max(0.05f, (float)atof(fe));
-    // sum_b ceil(p_b / T) <= nblock + (sum p) / T ~ nblock + slots / frac (T = frac (sum p) / slots, rounded
-    // down): a small margin over that keeps the grid's empty CTAs (which delay the dispatch of the
-    // side-stream kernels behind it) few; a plan that does not fit falls back to one unit per block
+    if (const char* ge = getenv("REAX_NB_GRID_FRAC")) ctx->nb_grid_frac = std::max(0.0f, (float)atof(ge));
+    // sum_b ceil(p_b / T) <= nblock + (sum p) / T ~ nblock + slots / frac (T = frac (sum p) / slots);
+    // blocks below T stay whole, so plans need much less (c1: 515 of 343 + 296). The grid is kept
+    // near that (its empty CTAs delay the dispatch of the side-stream kernels behind it); a plan that
+    // does not fit is made coarser (k_nb_plan doubles T)
     ctx->nb_umax = (int)std::min<long long>((long long)NB_UNIT_SPLIT * g.nblock,
-                                            g.nblock + (long long)std::ceil(ctx->nb_slots / ctx->nb_frac) + 16 +
-                                                g.nblock / 16);
+                                            g.nblock + (long long)std::ceil(ctx->nb_grid_frac * ctx->nb_slots / ctx->nb_frac) + 8);
   }
   ctx->cut = *cut;
   ctx->prm_valid = false;
