@@ -428,7 +428,7 @@ struct reax_ctx {
   int nb_slots = 0;     // resident nonbonded CTAs (SMs x NB_MINB)
   int nb_umax = 0;      // launched CTAs (>= planned units; the rest exit)
   float nb_frac = 1.2f; // unit target T = frac * pairs / slots (1.2: measured best at c1 of 0.8-1.5)
-  float nb_grid_frac = 0.6f;   // launched units: nblock + grid_frac * slots / frac + 8
+  float nb_grid_frac = 0.2f;   // launched units: nblock + grid_frac * slots / frac + 8 (c1 swept 0.12-0.6)
   // fork/join of reax_step (bond chain beside the nonbonded kernel)
   // reax_step_host replays one CUDA graph (copies in, step, copies out) per
   // unchanged (host buffers, box, parameters, workspace, mode)
