@@ -17,13 +17,21 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _HDR = os.path.join(_HERE, "oracle.h")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CFLAGS = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
+CFLAGS = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11", "-pthread"]
+
+# Row-parallel oracle (oracle.c header): results are bitwise independent of
+# the thread count; ORACLE_THREADS overrides the default of all host cores.
+THREADS = int(os.environ.get("ORACLE_THREADS", "0")) or (os.cpu_count() or 1)
+
+
+def _t(threads):
+    return int(threads) if threads else THREADS
 
 
 def build(force: bool = False) -> str:
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
-        subprocess.check_call(CFLAGS + ["-o", _LIB, _SRC, "-lm"])
+        subprocess.check_call(CFLAGS + ["-o", _LIB, _SRC, "-lm", "-lpthread"])
     return _LIB
 
 
@@ -95,11 +103,12 @@ def _get():
             "orc_wrap": (None, [I64, V, V, V]),
             "orc_min_image": (DBL, [DBL, DBL]),
             "orc_half_list_brute": (I64, [I64, V, V, DBL, V, V, I64]),
-            "orc_half_list_cells": (I64, [I64, V, V, DBL, V, V, I64]),
+            "orc_half_list_cells": (I64, [I64, V, V, DBL, V, V, I64, INT]),
+            "orc_digest_cells": (None, [I64, V, V, DBL, V, V, INT]),
             "orc_digest": (None, [I64, V, V, V, V]),
             "orc_mix64_pub": (U64, [U64, U64]),
             "orc_bo_raw": (None, [DBL, INT, INT, V, V]),
-            "orc_bonds": (I64, [I64, V, V, V, V, DBL, DBL, V, V, V, V, V, V, I64]),
+            "orc_bonds": (I64, [I64, V, V, V, V, DBL, DBL, V, V, V, V, V, V, I64, INT]),
             "orc_delta": (None, [I64, V, V, V, V, V]),
             "orc_bo_corr_pair": (None, [V, DBL, DBL, DBL, DBL, INT, INT, V, V, V]),
             "orc_bo_correct": (None, [I64, V, V, V, V, V, V, V, V]),
@@ -108,11 +117,12 @@ def _get():
             "orc_coulomb_kernel": (None, [DBL, INT, INT, V, V, V]),
             "orc_pair": (None, [DBL, INT, INT, DBL, DBL, V, DBL, V, V]),
             "orc_nonbonded": (None, [I64, V, V, V, V, V, DBL, V, V, V, V]),
+            "orc_nonbonded_rows": (None, [I64, V, V, V, V, V, DBL, V, V, INT]),
             "orc_atom_neighbors": (I64, [I64, I64, V, V, DBL, V, I64]),
             "orc_atom_force": (None, [I64, I64, V, V, V, V, V, DBL, V, V]),
             "orc_atom_bonds": (I64, [I64, I64, V, V, V, V, DBL, DBL, V, V, V, I64]),
             "orc_bond_energy_pair": (None, [DBL, V, DBL, DBL, DBL, DBL, INT, INT, V, V, V]),
-            "orc_bond_energy": (None, [I64, V, V, V, V, V, V, V, V, V, V, V]),
+            "orc_bond_energy": (None, [I64, V, V, V, V, V, V, V, V, V, V, V, INT]),
             "orc_angles": (I64, [I64, V, V, V, DBL, DBL, V, V, I64]),
             "orc_hbonds": (I64, [I64, V, V, V, V, DBL, ctypes.c_int32, ctypes.c_uint32, V, V, I64]),
             "orc_atom_hbonds": (I64, [I64, I64, V, V, V, INT, DBL, ctypes.c_int32, ctypes.c_uint32, V, I64]),
@@ -144,11 +154,15 @@ def min_image(d, L):
     return _get().orc_min_image(float(d), float(L))
 
 
-def half_list(pos, box, R, mode="cells"):
+def half_list(pos, box, R, mode="cells", threads=None):
     """Canonical half list (rowoff int64[n+1], col int32[P]): rows i asc, j>i asc."""
     pos, box = _a(pos, np.float64), _a(box, np.float64)
     n = len(pos)
-    fn = _get().orc_half_list_cells if mode == "cells" else _get().orc_half_list_brute
+    if mode == "cells":
+        T = _t(threads)
+        fn = lambda *a: _get().orc_half_list_cells(*a, T)   # noqa: E731
+    else:
+        fn = _get().orc_half_list_brute
     rowoff = np.empty(n + 1, np.int64)
     cap = max(1, int(n * 260))
     while True:
@@ -163,6 +177,17 @@ def digest(n, rowoff, col):
     cnt = np.empty(n, np.int64)
     dig = np.empty(n, np.uint64)
     _get().orc_digest(n, _ptr(_a(rowoff, np.int64)), _ptr(_a(col, np.int32)), _ptr(cnt), _ptr(dig))
+    return cnt, dig
+
+
+def digest_cells(pos, box, R, threads=None):
+    """Per-atom (full neighbour count, sum of mix64(min, max) mod 2^64) straight
+    from the cell grid: no stored list (c3/c4)."""
+    pos, box = _a(pos, np.float64), _a(box, np.float64)
+    n = len(pos)
+    cnt = np.empty(n, np.int64)
+    dig = np.empty(n, np.uint64)
+    _get().orc_digest_cells(n, _ptr(pos), _ptr(box), float(R), _ptr(cnt), _ptr(dig), _t(threads))
     return cnt, dig
 
 
@@ -186,12 +211,16 @@ def bo_corr_pair(raw, di, dboci, dj, dbocj, ti, tj, params):
     return out, f
 
 
-def bonds(pos, type_, box, params, r_bond, bo_cut, hrow, hcol):
+def bonds(pos, type_, box, params, r_bond, bo_cut, hrow, hcol, threads=None):
     """Full bond CSR: brow int64[n+1], bcol int32[B] (rows sorted by j), mirror int32[B]
-    (absolute entry index of the reverse bond), raw float64[B,4] (BO'sigma, BO'pi, BO'pipi, BO')."""
+    (absolute entry index of the reverse bond), raw float64[B,4] (BO'sigma, BO'pi, BO'pipi, BO').
+    hrow = hcol = None: candidates from the cell grid at r_bond (no stored half list)."""
     P = _P(params)
     pos, box, type_ = _a(pos, np.float64), _a(box, np.float64), _a(type_, np.int32)
-    hrow, hcol = _a(hrow, np.int64), _a(hcol, np.int32)
+    if hrow is not None:
+        hrow, hcol = _a(hrow, np.int64), _a(hcol, np.int32)
+    hp = _ptr(hrow) if hrow is not None else None
+    hc = _ptr(hcol) if hcol is not None else None
     n = len(pos)
     brow = np.empty(n + 1, np.int64)
     cap = max(16, 8 * n)
@@ -200,7 +229,7 @@ def bonds(pos, type_, box, params, r_bond, bo_cut, hrow, hcol):
         mir = np.empty(cap, np.int32)
         raw = np.empty((cap, 4))
         B = _get().orc_bonds(n, _ptr(pos), _ptr(type_), _ptr(box), P.ref, float(r_bond), float(bo_cut),
-                             _ptr(hrow), _ptr(hcol), _ptr(brow), _ptr(bcol), _ptr(mir), _ptr(raw), cap)
+                             hp, hc, _ptr(brow), _ptr(bcol), _ptr(mir), _ptr(raw), cap, _t(threads))
         if B <= cap:
             return brow, bcol[:B].copy(), mir[:B].copy(), raw[:B].copy()
         cap = int(B)
@@ -267,6 +296,18 @@ def nonbonded(pos, type_, q, box, params, R, hrow, hcol):
     return E, F
 
 
+def nonbonded_rows(pos, type_, q, box, params, R, threads=None):
+    """O6 row-parallel (gather over full rows from the cell grid): E = [E_vdW, E_Coul], F (n,3)."""
+    P = _P(params)
+    pos, type_, q, box = _a(pos, np.float64), _a(type_, np.int32), _a(q, np.float64), _a(box, np.float64)
+    n = len(pos)
+    E = np.empty(2)
+    F = np.empty((n, 3))
+    _get().orc_nonbonded_rows(n, _ptr(pos), _ptr(type_), _ptr(q), _ptr(box), P.ref, float(R), _ptr(E), _ptr(F),
+                              _t(threads))
+    return E, F
+
+
 def atom_neighbors(i, pos, box, R):
     pos, box = _a(pos, np.float64), _a(box, np.float64)
     out = np.empty(2048, np.int32)
@@ -296,16 +337,32 @@ def atom_bonds(i, pos, type_, box, params, r_bond, bo_cut):
     return part[:m].copy(), raw[:m].copy(), dl
 
 
-def evaluate(system, params, cut, mode="cells"):
+def evaluate(system, params, cut, mode="cells", threads=None):
     """Whole path in order: wrap -> list -> bonds -> Delta' -> corrected BO -> nonbonded."""
     pos = wrap(system.pos, system.box)
-    hrow, hcol = half_list(pos, system.box, cut["r_nonb"], mode)
-    brow, bcol, mir, raw = bonds(pos, system.type, system.box, params, cut["r_bond"], cut["bo_cut"], hrow, hcol)
+    hrow, hcol = half_list(pos, system.box, cut["r_nonb"], mode, threads)
+    brow, bcol, mir, raw = bonds(pos, system.type, system.box, params, cut["r_bond"], cut["bo_cut"], hrow, hcol,
+                                 threads)
     dlt = delta(system.type, params, brow, raw)
     corr = bo_correct(system.type, params, brow, bcol, mir, raw, dlt)
-    E, F = nonbonded(pos, system.type, system.q, system.box, params, cut["r_nonb"], hrow, hcol)
+    E, F = nonbonded_rows(pos, system.type, system.q, system.box, params, cut["r_nonb"], threads)
     return dict(pos=pos, hrow=hrow, hcol=hcol, brow=brow, bcol=bcol, mirror=mir, raw=raw, delta=dlt,
                 corr=corr, E=E, F=F)
+
+
+def evaluate_stream(system, params, cut, threads=None):
+    """The whole path without a stored half list (c3/c4: 3.4e9 pairs at c4):
+    per-atom digests of the list, the full bond list with BO', Delta' and
+    corrected BO, energies and forces — each row straight from the cell grid."""
+    pos = wrap(system.pos, system.box)
+    cnt, dig = digest_cells(pos, system.box, cut["r_nonb"], threads)
+    brow, bcol, mir, raw = bonds(pos, system.type, system.box, params, cut["r_bond"], cut["bo_cut"], None, None,
+                                 threads)
+    dlt = delta(system.type, params, brow, raw)
+    corr = bo_correct(system.type, params, brow, bcol, mir, raw, dlt)
+    E, F = nonbonded_rows(pos, system.type, system.q, system.box, params, cut["r_nonb"], threads)
+    return dict(pos=pos, cnt=cnt, dig=dig, brow=brow, bcol=bcol, mirror=mir, raw=raw, delta=dlt, corr=corr,
+                E=E, F=F)
 
 
 def bond_energy_pair(r, raw, di, dboci, dj, dbocj, ti, tj, params, bparams):
@@ -318,7 +375,7 @@ def bond_energy_pair(r, raw, di, dboci, dj, dbocj, ti, tj, params, bparams):
     return out
 
 
-def bond_energy(pos, type_, box, params, bparams, brow, bcol, raw, dlt):
+def bond_energy(pos, type_, box, params, bparams, brow, bcol, raw, dlt, threads=None):
     """O8 (NEXT-1): E_bond and its forces F (n,3) at a fixed bond set."""
     P, Q = _P(params), _Q(params, bparams)
     pos, type_, box = _a(pos, np.float64), _a(type_, np.int32), _a(box, np.float64)
@@ -327,7 +384,7 @@ def bond_energy(pos, type_, box, params, bparams, brow, bcol, raw, dlt):
     E = ctypes.c_double()
     _get().orc_bond_energy(n, _ptr(pos), _ptr(type_), _ptr(box), P.ref, Q.ref, _ptr(_a(brow, np.int64)),
                            _ptr(_a(bcol, np.int32)), _ptr(_a(raw, np.float64)), _ptr(_a(dlt, np.float64)),
-                           _ptr(F), ctypes.addressof(E))
+                           _ptr(F), ctypes.addressof(E), _t(threads))
     return E.value, F
 
 

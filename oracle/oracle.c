@@ -9,7 +9,12 @@
  *
  * Plain, slow, obviously correct: scalar IEEE fp64, compiled with
  * -O2 -ffp-contract=off (no FMA contraction, no fast-math), glibc libm,
- * single thread, every loop in the order the definition states.
+ * every loop in the order the definition states.  Row-parallel with POSIX
+ * threads (SURVEY.md §8(c) "std::thread over atom rows"):
+ * every atom row is computed on its own, in a fixed order, and writes only
+ * its own outputs; per-row Neumaier partials are combined in row order after
+ * the parallel pass.  Results are therefore bitwise independent of the
+ * thread count T (tests/test_oracle_threads.py pins 1 vs T).
  *
  * What it computes (the reading adopted in DESIGN.md):
  *   O1 minimum image, half-open [-L/2, L/2)
@@ -33,6 +38,7 @@
  * reading taken.
  * ==========================================================================*/
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -65,6 +71,140 @@ static double orc_dist2(const double* pos, int64_t i, int64_t j, const double bo
   return (d[0] * d[0] + d[1] * d[1]) + d[2] * d[2];
 }
 
+static int cmp_i32(const void* a, const void* b) {
+  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x > y) - (x < y);
+}
+
+/* ------------------------------------------------------ row-parallel driver */
+
+/* Rows [0, n) are dealt to T threads in chunks of ORC_CHUNK through an atomic
+ * counter.  fn(i, ctx, scratch) writes only row i's outputs, so the result is
+ * the same for every T and every dealing. */
+#define ORC_CHUNK 64
+typedef void (*orc_row_fn)(int64_t i, void* ctx, void* scratch);
+typedef struct {
+  int64_t n, next;
+  orc_row_fn fn;
+  void* ctx;
+  size_t scratch;
+} orc_job;
+
+static void* orc_worker(void* arg) {
+  orc_job* J = (orc_job*)arg;
+  void* scr = J->scratch ? malloc(J->scratch) : NULL;
+  for (;;) {
+    int64_t a = __atomic_fetch_add(&J->next, (int64_t)ORC_CHUNK, __ATOMIC_RELAXED);
+    if (a >= J->n) break;
+    int64_t b = a + ORC_CHUNK < J->n ? a + ORC_CHUNK : J->n;
+    for (int64_t i = a; i < b; ++i) J->fn(i, J->ctx, scr);
+  }
+  free(scr);
+  return NULL;
+}
+
+static void orc_par_rows(int64_t n, int T, orc_row_fn fn, void* ctx, size_t scratch) {
+  orc_job J = {n, 0, fn, ctx, scratch};
+  pthread_t th[256];
+  int started = 0;
+  if (T > 256) T = 256;
+  for (int t = 1; t < T && n > ORC_CHUNK; ++t)
+    if (pthread_create(&th[started], NULL, orc_worker, &J) == 0) ++started;
+  orc_worker(&J);
+  for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+}
+
+/* Cell grid for O2: cells of side L/floor(L/(Rc(1+1e-9))) per axis, strictly
+ * wider than Rc, so rounding in floor(x/side) never puts two atoms within Rc
+ * more than one cell apart; the atoms of each cell in ascending index
+ * (counting sort).  maxcand bounds the candidates of any row. */
+typedef struct {
+  int nc[3];
+  int64_t ncell, maxcand;
+  int64_t* start; /* ncell + 1 */
+  int64_t* atom;  /* n, cell-major */
+  int32_t* cell;  /* 3n */
+} orc_grid;
+
+/* the deduplicated neighbour cells of cell cc (c0 has 2 cells per axis, so
+ * -1 and +1 name the same cell) */
+static int orc_grid_nbcells(const orc_grid* G, const int32_t* cc, int64_t nb[27]) {
+  int nnb = 0;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        int cx = ((cc[0] + dx) % G->nc[0] + G->nc[0]) % G->nc[0];
+        int cy = ((cc[1] + dy) % G->nc[1] + G->nc[1]) % G->nc[1];
+        int cz = ((cc[2] + dz) % G->nc[2] + G->nc[2]) % G->nc[2];
+        int64_t c = ((int64_t)cz * G->nc[1] + cy) * G->nc[0] + cx;
+        int dup = 0;
+        for (int m = 0; m < nnb; ++m) dup |= (nb[m] == c);
+        if (!dup) nb[nnb++] = c;
+      }
+  return nnb;
+}
+
+static void orc_grid_build(orc_grid* G, int64_t n, const double* pos, const double box[3], double Rc) {
+  for (int k = 0; k < 3; ++k) {
+    G->nc[k] = (int)floor(box[k] / (Rc * (1.0 + 1e-9)));
+    if (G->nc[k] < 1) G->nc[k] = 1;
+  }
+  G->ncell = (int64_t)G->nc[0] * G->nc[1] * G->nc[2];
+  G->start = (int64_t*)calloc((size_t)G->ncell + 1, sizeof(int64_t));
+  G->atom = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  G->cell = (int32_t*)malloc(sizeof(int32_t) * 3 * (size_t)(n > 0 ? n : 1));
+  int64_t* cid = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t c = 0;
+    for (int k = 2; k >= 0; --k) {
+      int ck = (int)floor(pos[3 * i + k] / (box[k] / G->nc[k]));
+      if (ck >= G->nc[k]) ck = G->nc[k] - 1;
+      if (ck < 0) ck = 0;
+      G->cell[3 * i + k] = ck;
+      c = c * G->nc[k] + ck;
+    }
+    cid[i] = c;
+    G->start[c + 1]++;
+  }
+  for (int64_t c = 0; c < G->ncell; ++c) G->start[c + 1] += G->start[c];
+  int64_t* fill = (int64_t*)calloc((size_t)G->ncell, sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) G->atom[G->start[cid[i]] + fill[cid[i]]++] = i;
+  G->maxcand = 1;
+  for (int64_t c = 0; c < G->ncell; ++c) {
+    int32_t cc[3] = {(int32_t)(c % G->nc[0]), (int32_t)((c / G->nc[0]) % G->nc[1]),
+                     (int32_t)(c / ((int64_t)G->nc[0] * G->nc[1]))};
+    int64_t nb[27], s = 0;
+    int nnb = orc_grid_nbcells(G, cc, nb);
+    for (int m = 0; m < nnb; ++m) s += G->start[nb[m] + 1] - G->start[nb[m]];
+    if (s > G->maxcand) G->maxcand = s;
+  }
+  free(cid);
+  free(fill);
+}
+
+static void orc_grid_free(orc_grid* G) {
+  free(G->start);
+  free(G->atom);
+  free(G->cell);
+}
+
+/* Row i of the list at radius^2 R2 from the grid: every j != i (with half,
+ * only j > i) in the neighbour cells with min-image r^2 <= R2, ascending. */
+static int64_t orc_grid_row(const orc_grid* G, int64_t i, const double* pos, const double box[3], double R2,
+                            int half, int32_t* out) {
+  int64_t nb[27], len = 0;
+  double d[3];
+  int nnb = orc_grid_nbcells(G, &G->cell[3 * i], nb);
+  for (int m = 0; m < nnb; ++m)
+    for (int64_t a = G->start[nb[m]]; a < G->start[nb[m] + 1]; ++a) {
+      int64_t j = G->atom[a];
+      if (j == i || (half && j < i)) continue;
+      if (orc_dist2(pos, i, j, box, d) <= R2) out[len++] = (int32_t)j;
+    }
+  qsort(out, (size_t)len, sizeof(int32_t), cmp_i32);
+  return len;
+}
+
 /* ---------------------------------------------------------------- O2 list */
 
 /* Brute force: every unordered pair i<j with min-image r^2 <= R^2, emitted as
@@ -87,72 +227,86 @@ int64_t orc_half_list_brute(int64_t n, const double* pos, const double box[3], d
   return p;
 }
 
-static int cmp_i32(const void* a, const void* b) {
-  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
-  return (x > y) - (x < y);
+/* Cell-list version of the same set (O2), row-parallel: a counting pass
+ * gives every row's length, a serial prefix sum the offsets, a fill pass the
+ * rows (each j > i with r^2 <= R^2 in the deduplicated neighbour cells of the
+ * grid above, ascending).  SPEC.md:155: "each thread writing disjoint row
+ * ranges after a counting pass".  rowoff is written always, col only if the
+ * total fits cap.  Returns the pair count. */
+typedef struct {
+  const orc_grid* G;
+  const double* pos;
+  const double* box;
+  double R2;
+  int64_t* len;
+  const int64_t* rowoff;
+  int32_t* col;
+} orc_hl_ctx;
+
+static void orc_hl_count(int64_t i, void* c, void* scr) {
+  orc_hl_ctx* H = (orc_hl_ctx*)c;
+  H->len[i] = orc_grid_row(H->G, i, H->pos, H->box, H->R2, 1, (int32_t*)scr);
 }
 
-/* Cell-list version of the same set (O2): cells of side L/floor(L/(R(1+1e-9)))
- * per axis (strictly wider than R, so rounding in floor(x/side) can never put
- * two atoms within R more than one cell apart),
- * the set of neighbour cells deduplicated (c0 has 2 cells per axis, so -1 and
- * +1 name the same cell), candidate j > i kept iff r^2 <= R^2. */
+static void orc_hl_fill(int64_t i, void* c, void* scr) {
+  orc_hl_ctx* H = (orc_hl_ctx*)c;
+  int64_t m = orc_grid_row(H->G, i, H->pos, H->box, H->R2, 1, (int32_t*)scr);
+  memcpy(H->col + H->rowoff[i], scr, sizeof(int32_t) * (size_t)m);
+}
+
 int64_t orc_half_list_cells(int64_t n, const double* pos, const double box[3], double R,
-                            int64_t* rowoff, int32_t* col, int64_t cap) {
-  int nc[3];
-  for (int k = 0; k < 3; ++k) {
-    nc[k] = (int)floor(box[k] / (R * (1.0 + 1e-9)));
-    if (nc[k] < 1) nc[k] = 1;
-  }
-  int64_t ncell = (int64_t)nc[0] * nc[1] * nc[2];
-  int64_t* head = (int64_t*)malloc(sizeof(int64_t) * ncell);
-  int64_t* next = (int64_t*)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
-  int32_t* cell = (int32_t*)malloc(sizeof(int32_t) * 3 * (n > 0 ? n : 1));
-  int32_t* row = (int32_t*)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
-  for (int64_t c = 0; c < ncell; ++c) head[c] = -1;
-  for (int64_t i = n - 1; i >= 0; --i) {
-    int64_t c = 0;
-    for (int k = 2; k >= 0; --k) {
-      int ck = (int)floor(pos[3 * i + k] / (box[k] / nc[k]));
-      if (ck >= nc[k]) ck = nc[k] - 1;
-      if (ck < 0) ck = 0;
-      cell[3 * i + k] = ck;
-      c = c * nc[k] + ck;
-    }
-    next[i] = head[c];
-    head[c] = i;
-  }
-  double R2 = R * R, d[3];
+                            int64_t* rowoff, int32_t* col, int64_t cap, int T) {
+  orc_grid G;
+  orc_grid_build(&G, n, pos, box, R);
+  int64_t* len = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  orc_hl_ctx H = {&G, pos, box, R * R, len, rowoff, col};
+  size_t scr = sizeof(int32_t) * (size_t)G.maxcand;
+  orc_par_rows(n, T, orc_hl_count, &H, scr);
   int64_t p = 0;
   for (int64_t i = 0; i < n; ++i) {
     rowoff[i] = p;
-    /* deduplicated neighbour cells */
-    int64_t nb[27];
-    int nnb = 0;
-    for (int dz = -1; dz <= 1; ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          int cx = ((cell[3 * i] + dx) % nc[0] + nc[0]) % nc[0];
-          int cy = ((cell[3 * i + 1] + dy) % nc[1] + nc[1]) % nc[1];
-          int cz = ((cell[3 * i + 2] + dz) % nc[2] + nc[2]) % nc[2];
-          int64_t c = ((int64_t)cz * nc[1] + cy) * nc[0] + cx;
-          int dup = 0;
-          for (int m = 0; m < nnb; ++m) dup |= (nb[m] == c);
-          if (!dup) nb[nnb++] = c;
-        }
-    int64_t len = 0;
-    for (int m = 0; m < nnb; ++m)
-      for (int64_t j = head[nb[m]]; j >= 0; j = next[j])
-        if (j > i && orc_dist2(pos, i, j, box, d) <= R2) row[len++] = (int32_t)j;
-    qsort(row, (size_t)len, sizeof(int32_t), cmp_i32);
-    for (int64_t m = 0; m < len; ++m) {
-      if (p < cap) col[p] = row[m];
-      ++p;
-    }
+    p += len[i];
   }
   rowoff[n] = p;
-  free(head); free(next); free(cell); free(row);
+  if (p <= cap) orc_par_rows(n, T, orc_hl_fill, &H, scr);
+  free(len);
+  orc_grid_free(&G);
   return p;
+}
+
+/* Per-atom digest straight from the grid (c3/c4, no stored list): for each
+ * atom, the number of pairs it belongs to (its full neighbour count) and the
+ * sum of mix64(min, max) over them mod 2^64. */
+static uint64_t orc_mix64(uint64_t a, uint64_t b);
+typedef struct {
+  const orc_grid* G;
+  const double* pos;
+  const double* box;
+  double R2;
+  int64_t* cnt;
+  uint64_t* dig;
+} orc_dg_ctx;
+
+static void orc_dg_row(int64_t i, void* c, void* scr) {
+  orc_dg_ctx* D = (orc_dg_ctx*)c;
+  int32_t* row = (int32_t*)scr;
+  int64_t m = orc_grid_row(D->G, i, D->pos, D->box, D->R2, 0, row);
+  uint64_t h = 0;
+  for (int64_t a = 0; a < m; ++a) {
+    uint64_t j = (uint64_t)row[a], ii = (uint64_t)i;
+    h += orc_mix64(ii < j ? ii : j, ii < j ? j : ii);
+  }
+  D->cnt[i] = m;
+  D->dig[i] = h;
+}
+
+void orc_digest_cells(int64_t n, const double* pos, const double box[3], double R, int64_t* cnt, uint64_t* dig,
+                      int T) {
+  orc_grid G;
+  orc_grid_build(&G, n, pos, box, R);
+  orc_dg_ctx D = {&G, pos, box, R * R, cnt, dig};
+  orc_par_rows(n, T, orc_dg_row, &D, sizeof(int32_t) * (size_t)G.maxcand);
+  orc_grid_free(&G);
 }
 
 /* Per-atom digest for large configs: for each atom, the
@@ -194,49 +348,104 @@ void orc_bo_raw(double r, int ti, int tj, const orc_params* P, double out[4]) {
   out[3] = (bs + bp) + bpp; /* B2, summed in this order */
 }
 
-/* O3: for every canonical pair of the half list with r <= r_bond (r^2 <=
- * r_bond^2), BO' from B1-B2; a bond iff BO' >= bo_cut (reading 2A).  Emits the
- * FULL list (both i->j and j->i, "requires the bond list to be a
+/* O3: for every canonical pair (i < j) with r <= r_bond (r^2 <= r_bond^2),
+ * BO' from B1-B2; a bond iff BO' >= bo_cut (reading 2A).  Emits the FULL
+ * list (both i->j and j->i, "requires the bond list to be a
  * full list with both i-j and j-i bonds available") as CSR with rows sorted by
  * j, plus the mirror index.  bo: [B][4].  Returns B (entries);
- * writes nothing past cap. */
+ * writes nothing past cap.
+ * The canonical candidates of row i are its half-list row (hrow/hcol) or,
+ * with hrow == NULL, the j > i of the cell grid at r_bond (large systems, no
+ * stored half list).  Two row-parallel passes evaluate B1-B2 (count, then
+ * fill per-row kept lists); the full list is then assembled serially in
+ * canonical (i asc, j asc) order: row i receives partners j < i (from
+ * earlier rows, ascending i) before its own partners j > i (ascending), so
+ * every row ends sorted by j. */
+typedef struct {
+  const double* pos;
+  const int32_t* type;
+  const double* box;
+  const orc_params* P;
+  double rb2, bo_cut;
+  const int64_t* hrow;
+  const int32_t* hcol;
+  const orc_grid* G;
+  int64_t* kcnt;      /* kept canonical bonds of row i */
+  const int64_t* koff;
+  int32_t* kj;
+  double* kv;         /* [K][4] */
+} orc_bd_ctx;
+
+static void orc_bd_row(int64_t i, orc_bd_ctx* C, int32_t* cand, int fill) {
+  double d[3], v[4];
+  int64_t m, k = 0;
+  const int32_t* row;
+  if (C->hrow) {
+    row = C->hcol + C->hrow[i];
+    m = C->hrow[i + 1] - C->hrow[i];
+  } else {
+    m = orc_grid_row(C->G, i, C->pos, C->box, C->rb2, 1, cand);
+    row = cand;
+  }
+  for (int64_t a = 0; a < m; ++a) {
+    int64_t j = row[a];
+    double r2 = orc_dist2(C->pos, i, j, C->box, d);
+    if (r2 > C->rb2) continue;
+    orc_bo_raw(sqrt(r2), C->type[i], C->type[j], C->P, v);
+    if (v[3] < C->bo_cut) continue;
+    if (fill) {
+      int64_t e = C->koff[i] + k;
+      C->kj[e] = (int32_t)j;
+      for (int t = 0; t < 4; ++t) C->kv[4 * e + t] = v[t];
+    }
+    ++k;
+  }
+  if (!fill) C->kcnt[i] = k;
+}
+static void orc_bd_count(int64_t i, void* c, void* scr) { orc_bd_row(i, (orc_bd_ctx*)c, (int32_t*)scr, 0); }
+static void orc_bd_fill(int64_t i, void* c, void* scr) { orc_bd_row(i, (orc_bd_ctx*)c, (int32_t*)scr, 1); }
+
 int64_t orc_bonds(int64_t n, const double* pos, const int32_t* type, const double box[3],
                   const orc_params* P, double r_bond, double bo_cut, const int64_t* hrow,
                   const int32_t* hcol, int64_t* brow, int32_t* bcol, int32_t* bmirror,
-                  double* bo, int64_t cap) {
-  double rb2 = r_bond * r_bond, d[3], v[4];
-  int64_t* deg = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
-  /* pass 1: count kept bonds per atom */
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t p = hrow[i]; p < hrow[i + 1]; ++p) {
-      int64_t j = hcol[p];
-      double r2 = orc_dist2(pos, i, j, box, d);
-      if (r2 > rb2) continue;
-      orc_bo_raw(sqrt(r2), type[i], type[j], P, v);
-      if (v[3] >= bo_cut) { deg[i]++; deg[j]++; }
-    }
+                  double* bo, int64_t cap, int T) {
+  size_t n1 = (size_t)(n > 0 ? n : 1);
+  orc_grid G = {{0, 0, 0}, 0, 1, NULL, NULL, NULL};
+  if (!hrow) orc_grid_build(&G, n, pos, box, r_bond);
+  int64_t* kcnt = (int64_t*)calloc(n1, sizeof(int64_t));
+  int64_t* koff = (int64_t*)calloc(n1 + 1, sizeof(int64_t));
+  orc_bd_ctx C = {pos, type, box, P, r_bond * r_bond, bo_cut, hrow, hcol, &G, kcnt, koff, NULL, NULL};
+  size_t scr = hrow ? 0 : sizeof(int32_t) * (size_t)G.maxcand;
+  orc_par_rows(n, T, orc_bd_count, &C, scr);
+  for (int64_t i = 0; i < n; ++i) koff[i + 1] = koff[i] + kcnt[i];
+  int64_t K = koff[n];
+  /* full degrees: own canonical bonds + appearances as the partner */
+  int64_t* deg = (int64_t*)calloc(n1, sizeof(int64_t));
+  C.kj = (int32_t*)malloc(sizeof(int32_t) * (size_t)(K > 0 ? K : 1));
+  C.kv = (double*)malloc(sizeof(double) * 4 * (size_t)(K > 0 ? K : 1));
+  orc_par_rows(n, T, orc_bd_fill, &C, scr);
+  for (int64_t i = 0; i < n; ++i) {
+    deg[i] += kcnt[i];
+    for (int64_t e = koff[i]; e < koff[i + 1]; ++e) deg[C.kj[e]]++;
+  }
   brow[0] = 0;
   for (int64_t i = 0; i < n; ++i) brow[i + 1] = brow[i] + deg[i];
   int64_t B = brow[n];
-  if (B > cap) { free(deg); return B; }
-  /* pass 2: fill.  Canonical pairs are visited in (i asc, j asc) order, so row
-   * i receives partners j < i (from earlier rows, ascending i) before its own
-   * partners j > i (ascending): every row ends sorted by j. */
-  int64_t* fill = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t p = hrow[i]; p < hrow[i + 1]; ++p) {
-      int64_t j = hcol[p];
-      double r2 = orc_dist2(pos, i, j, box, d);
-      if (r2 > rb2) continue;
-      orc_bo_raw(sqrt(r2), type[i], type[j], P, v);
-      if (v[3] < bo_cut) continue;
-      int64_t ei = brow[i] + fill[i]++, ej = brow[j] + fill[j]++;
-      bcol[ei] = (int32_t)j; bcol[ej] = (int32_t)i;
-      bmirror[ei] = (int32_t)ej; /* mirror = absolute entry index of j->i */
-      bmirror[ej] = (int32_t)ei;
-      for (int k = 0; k < 4; ++k) { bo[4 * ei + k] = v[k]; bo[4 * ej + k] = v[k]; }
-    }
-  free(deg); free(fill);
+  if (B <= cap) {
+    int64_t* fill = (int64_t*)calloc(n1, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = koff[i]; k < koff[i + 1]; ++k) {
+        int64_t j = C.kj[k];
+        int64_t ei = brow[i] + fill[i]++, ej = brow[j] + fill[j]++;
+        bcol[ei] = (int32_t)j; bcol[ej] = (int32_t)i;
+        bmirror[ei] = (int32_t)ej; /* mirror = absolute entry index of j->i */
+        bmirror[ej] = (int32_t)ei;
+        for (int t = 0; t < 4; ++t) { bo[4 * ei + t] = C.kv[4 * k + t]; bo[4 * ej + t] = C.kv[4 * k + t]; }
+      }
+    free(fill);
+  }
+  free(deg); free(kcnt); free(koff); free(C.kj); free(C.kv);
+  if (!hrow) orc_grid_free(&G);
   return B;
 }
 
@@ -385,6 +594,64 @@ void orc_nonbonded(int64_t n, const double* pos, const int32_t* type, const doub
     }
   E[0] = ev.s + ev.c;
   E[1] = ec.s + ec.c;
+}
+
+/* O6, row-parallel (the form every evaluation uses; orc_nonbonded above is
+ * Alg. 2's scatter loop literally, kept as its cross-check).  Each atom row a
+ * visits its FULL neighbour set from the cell grid in ascending b and gathers
+ * F_a = sum_b g_ab d_ab with d_ab = minimum-image(x_b - x_a), g_ab =
+ * (dE/dr)/r — the same F = -grad E as the scatter F_i += f, F_k -= f, each
+ * pair seen from both of its atoms; the energy of row a is the Neumaier sum
+ * of e(a, b) over b > a (each pair once).  The row energies are combined in
+ * row order with a Neumaier sum (reading 22: any order within tolerance). */
+typedef struct {
+  const orc_grid* G;
+  const double *pos, *box, *q;
+  const int32_t* type;
+  const orc_params* P;
+  double R;
+  double* F;
+  double* Erow; /* [n][2] */
+} orc_nb_ctx;
+
+static void orc_nb_row(int64_t a, void* c, void* scr) {
+  orc_nb_ctx* C = (orc_nb_ctx*)c;
+  int32_t* row = (int32_t*)scr;
+  int64_t m = orc_grid_row(C->G, a, C->pos, C->box, C->R * C->R, 0, row);
+  orc_ksum ev = {0, 0}, ec = {0, 0};
+  double f[3] = {0.0, 0.0, 0.0}, d[3], e[2], dEdr;
+  for (int64_t t = 0; t < m; ++t) {
+    int64_t b = row[t];
+    double r = sqrt(orc_dist2(C->pos, a, b, C->box, d));
+    orc_pair(r, C->type[a], C->type[b], C->q[a], C->q[b], C->P, C->R, e, &dEdr);
+    double g = dEdr / r;
+    for (int k = 0; k < 3; ++k) f[k] += g * d[k];
+    if (b > a) {
+      ks_add(&ev, e[0]);
+      ks_add(&ec, e[1]);
+    }
+  }
+  for (int k = 0; k < 3; ++k) C->F[3 * a + k] = f[k];
+  C->Erow[2 * a] = ev.s + ev.c;
+  C->Erow[2 * a + 1] = ec.s + ec.c;
+}
+
+void orc_nonbonded_rows(int64_t n, const double* pos, const int32_t* type, const double* q,
+                        const double box[3], const orc_params* P, double R, double E[2], double* F, int T) {
+  orc_grid G;
+  orc_grid_build(&G, n, pos, box, R);
+  double* Erow = (double*)malloc(sizeof(double) * 2 * (size_t)(n > 0 ? n : 1));
+  orc_nb_ctx C = {&G, pos, box, q, type, P, R, F, Erow};
+  orc_par_rows(n, T, orc_nb_row, &C, sizeof(int32_t) * (size_t)G.maxcand);
+  orc_ksum ev = {0, 0}, ec = {0, 0};
+  for (int64_t a = 0; a < n; ++a) {
+    ks_add(&ev, Erow[2 * a]);
+    ks_add(&ec, Erow[2 * a + 1]);
+  }
+  E[0] = ev.s + ev.c;
+  E[1] = ec.s + ec.c;
+  free(Erow);
+  orc_grid_free(&G);
 }
 
 /* ------------------------------------------ per-atom brute force (large N) */
@@ -548,44 +815,74 @@ void orc_bond_energy_pair(double r, const double raw[4], double di, double dboci
   out[4] = (dr[0] + dr[1]) + dr[2];   /* dBO'/dr */
 }
 
-/* O8: E1 over the bonds of O3 (canonical i < j, ascending), Neumaier-summed;
- * forces [n][3] (overwritten) by the two passes stated above: D_i summed over
- * the canonical bonds in order, then g per bond.  raw: [B][4] BO' terms of
- * O3; delta: [n][2] of O4. */
+/* O8: E1 over the bonds of O3, row-parallel.  Pass 1 (per atom row a, bonds
+ * in row order): D_a = sum over a's bonds of de_b/dS_a, each bond evaluated
+ * in canonical orientation (i, j) = (min, max) so that de/dS_i is out[2] and
+ * de/dS_j out[3]; the row's energy is the Neumaier sum of e over its
+ * partners b > a (each bond once), rows combined in row order.  Pass 2: F_a
+ * = sum_b g d_ab, g = (de/dr + (D_i + D_j) dBO'/dr)/r, d_ab =
+ * minimum-image(x_b - x_a) — the scatter F_i += g d_ij, F_j -= g d_ij seen
+ * from each atom.  raw: [B][4] BO' terms of O3; delta: [n][2] of O4;
+ * forces [n][3] overwritten. */
+typedef struct {
+  const double *pos, *box, *raw, *delta;
+  const int32_t *type, *bcol;
+  const int64_t* brow;
+  const orc_params* P;
+  const orc_bond_params* Q;
+  double *D, *Erow, *F;
+} orc_be_ctx;
+
+static void orc_be_eval(const orc_be_ctx* C, int64_t a, int64_t e, double d[3], double* r, double out[5]) {
+  int64_t b = C->bcol[e], i = a < b ? a : b, j = a < b ? b : a;
+  *r = sqrt(orc_dist2(C->pos, a, b, C->box, d));
+  orc_bond_energy_pair(*r, &C->raw[4 * e], C->delta[2 * i], C->delta[2 * i + 1], C->delta[2 * j],
+                       C->delta[2 * j + 1], C->type[i], C->type[j], C->P, C->Q, out);
+}
+
+static void orc_be_row1(int64_t a, void* c, void* scr) {
+  orc_be_ctx* C = (orc_be_ctx*)c;
+  double d[3], r, out[5], D = 0.0;
+  orc_ksum E = {0.0, 0.0};
+  (void)scr;
+  for (int64_t e = C->brow[a]; e < C->brow[a + 1]; ++e) {
+    int64_t b = C->bcol[e];
+    orc_be_eval(C, a, e, d, &r, out);
+    D += a < b ? out[2] : out[3];
+    if (b > a) ks_add(&E, out[0]);
+  }
+  C->D[a] = D;
+  C->Erow[a] = E.s + E.c;
+}
+
+static void orc_be_row2(int64_t a, void* c, void* scr) {
+  orc_be_ctx* C = (orc_be_ctx*)c;
+  double d[3], r, out[5], f[3] = {0.0, 0.0, 0.0};
+  (void)scr;
+  for (int64_t e = C->brow[a]; e < C->brow[a + 1]; ++e) {
+    int64_t b = C->bcol[e], i = a < b ? a : b, j = a < b ? b : a;
+    orc_be_eval(C, a, e, d, &r, out);
+    double g = (out[1] + (C->D[i] + C->D[j]) * out[4]) / r;
+    for (int k = 0; k < 3; ++k) f[k] += g * d[k];
+  }
+  for (int k = 0; k < 3; ++k) C->F[3 * a + k] = f[k];
+}
+
 void orc_bond_energy(int64_t n, const double* pos, const int32_t* type, const double box[3],
                      const orc_params* P, const orc_bond_params* Q, const int64_t* brow,
                      const int32_t* bcol, const double* raw, const double* delta, double* force,
-                     double* energy) {
-  double* D = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+                     double* energy, int T) {
+  size_t n1 = (size_t)(n > 0 ? n : 1);
+  double* D = (double*)calloc(n1, sizeof(double));
+  double* Erow = (double*)calloc(n1, sizeof(double));
+  orc_be_ctx C = {pos, box, raw, delta, type, bcol, brow, P, Q, D, Erow, force};
+  orc_par_rows(n, T, orc_be_row1, &C, 0);
+  orc_par_rows(n, T, orc_be_row2, &C, 0);
   orc_ksum E = {0.0, 0.0};
-  double d[3], out[5];
-  for (int64_t k = 0; k < 3 * n; ++k) force[k] = 0.0;
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t e = brow[i]; e < brow[i + 1]; ++e) {
-      int64_t j = bcol[e];
-      if (j < i) continue;
-      double r = sqrt(orc_dist2(pos, i, j, box, d));
-      orc_bond_energy_pair(r, &raw[4 * e], delta[2 * i], delta[2 * i + 1], delta[2 * j], delta[2 * j + 1],
-                           type[i], type[j], P, Q, out);
-      ks_add(&E, out[0]);
-      D[i] += out[2];
-      D[j] += out[3];
-    }
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t e = brow[i]; e < brow[i + 1]; ++e) {
-      int64_t j = bcol[e];
-      if (j < i) continue;
-      double r = sqrt(orc_dist2(pos, i, j, box, d));
-      orc_bond_energy_pair(r, &raw[4 * e], delta[2 * i], delta[2 * i + 1], delta[2 * j], delta[2 * j + 1],
-                           type[i], type[j], P, Q, out);
-      double g = (out[1] + (D[i] + D[j]) * out[4]) / r;
-      for (int k = 0; k < 3; ++k) {
-        force[3 * i + k] += g * d[k];
-        force[3 * j + k] -= g * d[k];
-      }
-    }
+  for (int64_t a = 0; a < n; ++a) ks_add(&E, Erow[a]);
   *energy = E.s + E.c;
   free(D);
+  free(Erow);
 }
 
 /* ------------------------------------------------ O9 interaction lists (NEXT-3)

@@ -169,3 +169,29 @@ def test_zero_bond_energies_give_zero(small, params, bparams):
     bp.De_pipi[:] = 0.0
     E, F, _ = _energy(small, p, bp)
     assert E == 0.0 and np.all(F == 0.0)
+
+
+@pytest.mark.parametrize("m", [2.0, 3.0, 0.5])
+def test_e1_closed_form_sign_of_p_be1(params, bparams, m):
+    """E1 at BOs = m^(1/p_be2): BOs^p_be2 = m, so e = -De_s BOs exp(p_be1 (1 - m))
+    - De_p BOpi - De_pp BOpipi.  Delta' = 0 gives f1 = 1 exactly and
+    Delta'boc = -1000 gives f4 = f5 = 1 exactly (exp(< -700) = 0), so the
+    corrected orders are the raw terms: BOs = raw sigma, BOpi, BOpipi.  At
+    m = 2 the factor is exp(-p_be1): a flipped sign of p_be1 (exp(+p_be1)) or a
+    misplaced p_be2 fails."""
+    for ti, tj in [(0, 0), (0, 2), (1, 3)]:
+        b1, b2 = bparams.p_be1[ti, tj], bparams.p_be2[ti, tj]
+        assert abs(b1) > 1e-3
+        bs = m ** (1.0 / b2)
+        bpi, bpp = 0.25, 0.125
+        raw = np.array([bs, bpi, bpp, (bs + bpi) + bpp])
+        out = oracle.bond_energy_pair(1.3, raw, 0.0, -1000.0, 0.0, -1000.0, ti, tj, params, bparams)
+        # BOs = BO - BOpi - BOpipi reconstructs raw sigma to rounding
+        want = -params.De[ti, tj] * bs * np.exp(b1 * (1.0 - m)) - bparams.De_pi[ti, tj] * bpi \
+            - bparams.De_pipi[ti, tj] * bpp
+        assert abs(out[0] - want) <= 1e-13 * abs(want), (ti, tj, out[0], want)
+        # and the sigma factor alone at m = 2 is exp(-p_be1), not exp(+p_be1)
+        if m == 2.0:
+            sig = (out[0] + bparams.De_pi[ti, tj] * bpi + bparams.De_pipi[ti, tj] * bpp) / (-params.De[ti, tj] * bs)
+            assert abs(sig - np.exp(-b1)) <= 1e-12 * np.exp(-b1)
+            assert abs(sig - np.exp(b1)) > 1e-6

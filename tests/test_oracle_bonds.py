@@ -182,3 +182,23 @@ def test_atom_bonds_matches_list(c0, params, c0_oracle):
         assert part.tolist() == o["bcol"][seg].tolist()
         assert np.array_equal(raw, o["raw"][seg])
         assert np.array_equal(dl, o["delta"][i])
+
+
+@pytest.mark.parametrize("m", [2.0, 3.0, 0.5])
+def test_bo_raw_exponents_closed_form(params, m):
+    """B1 at r = r0 * m^(1/p): (r/r0)^p = m, so BO'_k = exp(m * pa_k) for
+    each term with its own exponent (sigma: p_bo1, p_bo2; pi: p_bo3, p_bo4;
+    pipi: p_bo5, p_bo6).  The three exponents of a pair differ, so a swapped
+    or misplaced exponent (or prefactor) fails at m != 1."""
+    p = params
+    for ti, tj in [(0, 0), (0, 3), (1, 2), (3, 3)]:
+        terms = [(p.r_sigma, p.p_bo1, p.p_bo2, 0), (p.r_pi, p.p_bo3, p.p_bo4, 1), (p.r_pipi, p.p_bo5, p.p_bo6, 2)]
+        pw = [p.p_bo2[ti, tj], p.p_bo4[ti, tj], p.p_bo6[ti, tj]]
+        assert len(set(np.round(pw, 12))) == 3   # distinct exponents: the pin can see a swap
+        for r0v, pa, pb, k in terms:
+            r0 = 0.5 * (r0v[ti] + r0v[tj])
+            r = r0 * m ** (1.0 / pb[ti, tj])
+            want = np.exp(m * pa[ti, tj])
+            got = oracle.bo_raw(r, ti, tj, p)[k]
+            # (r/r0)^p = m to a few ulp; d exp(pa x)/dx relative = |pa| <= 1
+            assert abs(got - want) <= 1e-14 * want * max(1.0, m), (ti, tj, k, got, want)
