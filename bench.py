@@ -5,7 +5,8 @@ Contract:
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 One rank per GPU (torchrun for N > 1).  A step = one reax_step (lists rebuilt,
 bond orders, nonbonded energies and forces) on the synthetic PETN-shaped
-config C (default BASELINE.json configs[1], 32,480 atoms).  N > 1 runs
+config C (default BASELINE.json configs[4], 16,588,000 atoms: the largest
+single-GPU config; c1 is reported beside it under "c1").  N > 1 runs
 independent replicas ("replicas only": north_star keeps the path on one GPU).
 Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (the
 reference arm of this tier) on the host cores.
@@ -26,10 +27,56 @@ sys.path.insert(0, ROOT)
 METRIC = "atom-steps/s (list build+bond orders+nonbonded forces); % FP64/HBM roofline"
 # Algorithmic work per unit:
 W_NB_DP_PER_PAIR = 200.0    # FP64-pipe thread instructions per half pair (N1-N6, formula-minimal)
-NBR_BYTES_PER_ATOM_FIXED = 16 + 4 + 4   # read fp32 local coords; write row length; bond-candidate count
+NBR_BYTES_PER_ATOM_ALG = 900.0         # algorithmic bytes per atom of the half-list build
+NBR_BYTES_PER_ATOM_FIXED = 16 + 4 + 4   # as stored here: fp32 local coords in; row length, bond-candidate count out
 NBR_BYTES_PER_PAIR = 2                  # one uint16 window slot per half-list entry
 NBR_BYTES_PER_BONDCAND = 4
 FLUSH_BYTES = 512 << 20                 # > 126 MB L2
+DEFAULT_CONFIG = 4                      # the largest single-GPU config of BASELINE.json (c4, 16.6M atoms)
+ORACLE_BUDGET_S = 20.0                  # CPU seconds of the bounded oracle sample (cpu_baseline)
+
+
+def config_dict(k):
+    """The workload description both arms print (identical dicts)."""
+    import gen
+    c = gen.CONFIGS[k]
+    return {"workload": workload_name(k, c), "n_atoms": c["n"], "box_A": list(c["box"]),
+            "cutoffs": dict(gen.CUTOFFS), "lists": "rebuilt every step",
+            "l2": "GPU arm: 512 MB written between timed steps (L2 flush)"}
+
+
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_sample(k, budget_s, threads):
+    """A bounded sample of config k for the CPU oracle: a smaller periodic
+    system from the same recipe (generator, density 0.0978/A^3, PETN types,
+    parameters, cutoffs), sized from a calibration run so that one oracle
+    evaluation takes about budget_s on `threads` threads.  c0-c2 are small
+    enough to be their own sample when they fit."""
+    import gen
+    import oracle
+    params = gen.make_params()
+    c = gen.CONFIGS[k]
+    cal = gen.make_system(29 * 1120, (69.3, 69.3, 69.3), gen.SEED_BASE + 1)   # c1-sized calibration
+    t0 = time.perf_counter()
+    oracle.evaluate_stream(cal, params, gen.CUTOFFS, threads=threads)
+    per_atom = (time.perf_counter() - t0) / len(cal.pos)
+    if c["n"] * per_atom <= budget_s:
+        return gen.make_config(k), f"one full oracle evaluation of c{k} ({c['n']:,} atoms)"
+    n = max(2088, int(round(budget_s / per_atom / 29)) * 29)
+    L = (n / 0.0978) ** (1 / 3)
+    s = gen.make_system(n, (L, L, L), gen.SEED_BASE + 100 + k)
+    return s, (f"one full oracle evaluation (lists, bond orders, energies, forces) of a {n:,}-atom periodic "
+               f"cube of {L:.2f} A from the same recipe as c{k} (generator, density 0.0978/A^3, PETN types, "
+               f"parameters, 10/5 A cutoffs): a bounded sample of c{k}'s {c['n']:,} atoms")
 
 
 def workload_name(k, c):
@@ -100,17 +147,17 @@ def replica_throughput(n_atoms, steps, world, max_ms):
     return n_atoms * steps * world / (max_ms * 1e-3)
 
 
-def run_cpu_oracle(k, evals):
+def run_cpu_oracle(k, evals, threads):
     import gen
     import oracle
     params = gen.make_params()
-    s = gen.make_config(k)
     oracle.build()
+    s, sample = oracle_sample(k, ORACLE_BUDGET_S / max(1, evals), threads)
     t0 = time.perf_counter()
     for _ in range(evals):
-        oracle.evaluate(s, params, gen.CUTOFFS)
+        oracle.evaluate_stream(s, params, gen.CUTOFFS, threads=threads)
     dt = time.perf_counter() - t0
-    return len(s.pos) * evals / dt, dt, len(s.pos)
+    return len(s.pos) * evals / dt, dt, sample
 
 
 def reference_arm(args, rank, world):
@@ -119,32 +166,19 @@ def reference_arm(args, rank, world):
     import oracle
     if rank != 0:
         return
-    c = gen.CONFIGS[args.config]
     params = gen.make_params()
     oracle.build()
-    # one full oracle evaluation of the config per step if that fits ~150 s
-    # for W + K steps, else a smaller system from the same recipe (density,
-    # generator, parameters, cutoffs): a bounded sample of the workload
-    full = gen.make_config(args.config)
-    t0 = time.perf_counter()
-    oracle.evaluate(full, params, gen.CUTOFFS)
-    t_full = time.perf_counter() - t0
+    threads = oracle.THREADS
+    # each step one oracle evaluation of a bounded sample of the config, sized
+    # so that the W + K steps take about 150 s on the host cores
     budget = 150.0 / max(1, args.steps + args.warmup)
-    if t_full <= budget:
-        s, sample = full, f"one full oracle evaluation of {workload_name(args.config, c)} per step"
-    else:
-        frac = max(budget / t_full, 0.02)
-        n = max(2088, int(round(c["n"] * frac / 29)) * 29)
-        L = (n / 0.0978) ** (1 / 3)
-        s = gen.make_system(n, (L, L, L), gen.SEED_BASE + 100 + args.config)
-        sample = (f"per step one full oracle evaluation of a {n:,}-atom system from the same recipe "
-                  f"(cube {L:.2f} A, density 0.0978/A^3, same generator/params/cutoffs): bounded sample of c{args.config}")
+    s, sample = oracle_sample(args.config, budget, threads)
     for _ in range(args.warmup):
-        oracle.evaluate(s, params, gen.CUTOFFS)
+        oracle.evaluate_stream(s, params, gen.CUTOFFS, threads=threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.evaluate(s, params, gen.CUTOFFS)
+        oracle.evaluate_stream(s, params, gen.CUTOFFS, threads=threads)
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = len(s.pos) * args.steps / tot
@@ -152,12 +186,56 @@ def reference_arm(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "atom-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, c), "n_atoms": c["n"], "impl_detail": "C oracle (oracle/oracle.c), gcc -O2 -ffp-contract=off, 1 thread"},
-        "cpu_baseline": {"value": value, "unit": "atom-steps/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "config": config_dict(args.config),
+        "impl_detail": f"C oracle (oracle/oracle.c), gcc -O2 -ffp-contract=off, row-parallel on {threads} threads "
+                       "(oracle.evaluate_stream)",
+        "cpu_baseline": {"value": value, "unit": "atom-steps/s", "cores": threads, "cpu": cpu_model(),
+                         "kind": "oracle", "sample": sample + " per step"},
         "e2e": {"value": value, "unit": "atom-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
+
+
+def measure_c1(rx, gen, params, dev, flush, world, steps=50):
+    """Supplementary: the same step on c1 (32,480 atoms; launch- and
+    tail-bound), graph-replayed, L2 flushed between steps."""
+    import torch
+    s = gen.make_config(1)
+    n = len(s.pos)
+    ctx = rx.Reax(n, s.box, params, gen.CUTOFFS, device=dev)
+    pos, typ, q = (torch.from_numpy(x).to(dev) for x in (s.pos, s.type, s.q))
+    F = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    E = torch.empty(2, dtype=torch.float64, device=dev)
+    ctx.step(pos, typ, q, F, E)
+    torch.cuda.synchronize()
+    ctx.set_async(True)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            ctx.step(pos, typ, q, F, E)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ctx.step(pos, typ, q, F, E)
+    for _ in range(3):
+        g.replay()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for k in range(steps):
+        flush.fill_(float(k))
+        ev[k][0].record()
+        g.replay()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    ctx.check()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    ms = max_over_ranks([ms], world, dev)[0]
+    return {"workload": workload_name(1, gen.CONFIGS[1]), "value": replica_throughput(n, steps, world, ms),
+            "unit": "atom-steps/s", "ms_per_step": ms / steps, "steps": steps,
+            "note": "supplementary (BASELINE configs[1]); the headline is the config above"}
 
 
 def main():
@@ -165,7 +243,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
+    ap.add_argument("--no-c1", action="store_true", help="skip the supplementary c1 measurement")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -394,34 +473,42 @@ def main():
     lctx.check()
     nb_iso_s = lctx.kernel_ms(reset=True)["nonbonded"][0] / 10 * 1e-3
     del lctx
-    nbr_bytes = n * NBR_BYTES_PER_ATOM_FIXED + P * NBR_BYTES_PER_PAIR + 2.9 * n * NBR_BYTES_PER_BONDCAND
-    hbm_peak = None
+    nbr_bytes = n * NBR_BYTES_PER_ATOM_ALG
+    nbr_bytes_stored = n * NBR_BYTES_PER_ATOM_FIXED + P * NBR_BYTES_PER_PAIR + 2.9 * n * NBR_BYTES_PER_BONDCAND
+    hbm_peak, hbm_src = None, "MEASURED_PEAKS.json hbm_gbs"
     try:
         hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     except Exception:
-        hbm_peak = 6650.0   # B200_PROFILING.md fallback
+        hbm_peak, hbm_src = 6650.0, "B200_PROFILING.md fallback"
     traffic = nbr_traffic = dp_exec = None
-    try:   # from the committed ncu capture of this workload (profiles/ncu_summary.json)
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get(f"c{args.config}", {})
+    prof_src = None
+    try:   # from the committed ncu --set full capture of this workload (profiles/ncu_summary.json)
+        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        prof = summ.get(f"c{args.config}", {})
         traffic = prof.get("k_nonbonded", {}).get("dram_bytes_per_launch")
         nbr_traffic = prof.get("k_nbr_build", {}).get("dram_bytes_per_launch")
         dp_exec = prof.get("k_nonbonded", {}).get("dp_thread_inst_per_pair")
+        prof_src = prof.get("_source") or summ.get("_source")
     except Exception:
         pass
+    c1 = None
+    if not args.no_c1 and args.config != 1:
+        c1 = measure_c1(rx, gen, params, dev, flush, world)
     step_total_ms = sum(v[0] for v in kms.values())
     line = {
         "metric": METRIC, "value": value, "unit": "atom-steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, c), "n_atoms": n, "half_pairs": P, "bond_entries": B,
-                   "evals_timed": args.steps, "lists": "rebuilt every step", "l2": "flushed (512 MB write) between timed steps",
+        "config": config_dict(args.config),
+        "counts": {"half_pairs": P, "bond_entries": B, "evals_timed": args.steps,
                    "parallelism": "replicas" if world > 1 else "single GPU",
                    "launch": "direct launches" if args.no_graph else "CUDA graph replay of reax_step (async mode)"},
         "ns_per_atom_step": 1e9 / value * world if value else None,
         "roofline": {"bound": "alu", "kernel": "k_nonbonded (a7)",
                      "achieved": achieved / 1e12, "peak": peak_dfma / 1e12,
                      "unit": "T FP64-pipe thread-instructions/s", "frac": achieved / peak_dfma,
-                     "traffic": traffic, "work": f"{W_NB_DP_PER_PAIR:.0f} DP inst/pair x {P} pairs per launch",
+                     "traffic": traffic, "traffic_source": prof_src,
+                     "work": f"{W_NB_DP_PER_PAIR:.0f} DP inst/pair x {P} pairs per launch",
                      "peak_source": "DFMA probe measured in this run (tools/peak.cu); MEASURED_PEAKS.json has no FP64 entry",
                      "avg_launch_ms": nb_avg_s * 1e3,
                      "executed_dp_per_pair": dp_exec,
@@ -432,7 +519,9 @@ def main():
         "roofline_kernels": [
             {"kernel": "k_nbr_build (a3-a4; reax_build_lists path, timed separately)", "bound": "hbm", "achieved": nbr_bytes / nbr_avg_s / 1e9, "peak": hbm_peak,
              "unit": "GB/s", "frac": nbr_bytes / nbr_avg_s / 1e9 / hbm_peak, "avg_launch_ms": nbr_avg_s * 1e3,
-             "bytes_per_launch": nbr_bytes, "traffic": nbr_traffic},
+             "bytes_per_launch": nbr_bytes, "bytes_rule": "SURVEY.md 8(d) a3: 900 B/atom (algorithmic)",
+             "bytes_stored_per_launch": nbr_bytes_stored, "peak_source": hbm_src,
+             "traffic": nbr_traffic, "traffic_source": prof_src},
             {"kernel": "k_nonbonded (a7) on its own (reax_nonbonded path, no concurrent bond chain)", "bound": "alu",
              "achieved": W_NB_DP_PER_PAIR * P / nb_iso_s / 1e12, "peak": peak_dfma / 1e12,
              "unit": "T FP64-pipe thread-instructions/s", "frac": W_NB_DP_PER_PAIR * P / nb_iso_s / peak_dfma,
@@ -447,11 +536,14 @@ def main():
         "next_rows": {"bond_energy": bond_energy, "interaction_lists": ilists},
         "clocks": clocks,
     }
+    if c1 is not None:
+        line["c1"] = c1
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        evals = 3 if args.config <= 1 else 1
-        v, dt, nn = run_cpu_oracle(args.config if args.config <= 2 else 1, evals)
-        line["cpu_baseline"] = {"value": v, "unit": "atom-steps/s", "cores": 1, "kind": "oracle",
-                                "sample": f"{evals} full oracle evaluation(s) of c{args.config if args.config <= 2 else 1} ({nn:,} atoms), {dt:.1f} s, 1 thread"}
+        import oracle
+        threads = oracle.THREADS
+        v, dt, sample = run_cpu_oracle(args.config, 1, threads)
+        line["cpu_baseline"] = {"value": v, "unit": "atom-steps/s", "cores": threads, "cpu": cpu_model(),
+                                "kind": "oracle", "sample": f"{sample}; {dt:.1f} s on {threads} threads"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

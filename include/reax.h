@@ -58,8 +58,10 @@ typedef enum {
   REAX_ERR_NONFINITE = 6, /* NaN/Inf in positions, charges or computed energies */
   REAX_ERR_CUDA = 7,      /* a CUDA runtime error */
   REAX_ERR_STATE = 8,     /* call order / binding violated (no workspace, stale lists) */
-  REAX_ERR_RANGE = 9      /* a pair force |dE/dr| or a row force component >= 65536 kcal/mol/A:
-                             outside the fixed-point force accumulator (2^-35 resolution) */
+  REAX_ERR_RANGE = 9      /* a pair force |dE/dr| or a row force component >= 65536 kcal/mol/A, or
+                             one CTA's accumulated partial force on a window atom beyond 32768
+                             kcal/mol/A: outside the fixed-point force accumulator (2^-35
+                             resolution); results are then undefined */
 } reax_status;
 
 #define REAX_MAX_TYPES 16

@@ -125,6 +125,8 @@ def _get():
             "orc_bond_energy": (None, [I64, V, V, V, V, V, V, V, V, V, V, V, INT]),
             "orc_angles": (I64, [I64, V, V, V, DBL, DBL, V, V, I64]),
             "orc_hbonds": (I64, [I64, V, V, V, V, DBL, ctypes.c_int32, ctypes.c_uint32, V, V, I64]),
+            "orc_hbonds_cells": (I64, [I64, V, V, V, V, DBL, ctypes.c_int32, ctypes.c_uint32, V, V, I64, INT]),
+            "orc_species": (I64, [I64, V, INT, V, V, V, V, V, V, V, I64, V]),
             "orc_atom_hbonds": (I64, [I64, I64, V, V, V, INT, DBL, ctypes.c_int32, ctypes.c_uint32, V, I64]),
         }
         for name, (res, args) in sig.items():
@@ -416,16 +418,21 @@ def angles(brow, bcol, corr, thb_cut, thb_cutsq):
         cap = int(t)
 
 
-def hbonds(pos, type_, box, brow, r_hb, h_type, acc_mask):
-    """O9 H-bond list: (hb_off int64[n+1], hb_z int32[H]) by brute force."""
+def hbonds(pos, type_, box, brow, r_hb, h_type, acc_mask, mode="brute", threads=None):
+    """O9 H-bond list: (hb_off int64[n+1], hb_z int32[H]) by brute force (the
+    definition) or, mode="cells", from the cell grid at r_hb (row-parallel)."""
     pos, type_, box, brow = _a(pos, np.float64), _a(type_, np.int32), _a(box, np.float64), _a(brow, np.int64)
     n = len(pos)
     off = np.empty(n + 1, np.int64)
     cap = max(1, 64 * n)
     while True:
         z = np.empty(cap, np.int32)
-        t = _get().orc_hbonds(n, _ptr(pos), _ptr(type_), _ptr(box), _ptr(brow), float(r_hb), int(h_type),
-                              int(acc_mask), _ptr(off), _ptr(z), cap)
+        if mode == "cells":
+            t = _get().orc_hbonds_cells(n, _ptr(pos), _ptr(type_), _ptr(box), _ptr(brow), float(r_hb), int(h_type),
+                                        int(acc_mask), _ptr(off), _ptr(z), cap, _t(threads))
+        else:
+            t = _get().orc_hbonds(n, _ptr(pos), _ptr(type_), _ptr(box), _ptr(brow), float(r_hb), int(h_type),
+                                  int(acc_mask), _ptr(off), _ptr(z), cap)
         if t <= cap:
             return off, z[:t].copy()
         cap = int(t)
@@ -449,3 +456,27 @@ def atom_hbonds(i, pos, type_, box, has_bond, r_hb, h_type, acc_mask):
                                int(h_type), int(acc_mask), _ptr(out), 4096)
     assert m <= 4096
     return out[:m].copy()
+
+
+# NEXT-4: default bond-order threshold of the species analysis
+SPECIES_BO_THRESH = 0.3
+
+
+def species(type_, ntypes, brow, bcol, corr, thresh=SPECIES_BO_THRESH):
+    """O10 species analysis: (mol_id int32[n] in 1..M, M, species_comp int32[S, ntypes]
+    sorted ascending, species_count int64[S])."""
+    type_, brow, bcol, corr = _a(type_, np.int32), _a(brow, np.int64), _a(bcol, np.int32), _a(corr, np.float64)
+    th = np.broadcast_to(np.asarray(thresh, np.float64), (ntypes, ntypes))
+    th = np.ascontiguousarray(th)
+    n = len(type_)
+    mol = np.empty(n, np.int32)
+    cap = 1024
+    while True:
+        comp = np.empty((cap, ntypes), np.int32)
+        cnt = np.empty(cap, np.int64)
+        S = ctypes.c_int64()
+        M = _get().orc_species(n, _ptr(type_), int(ntypes), _ptr(brow), _ptr(bcol), _ptr(corr), _ptr(th), _ptr(mol),
+                               _ptr(comp), _ptr(cnt), cap, ctypes.addressof(S))
+        if S.value <= cap:
+            return mol, int(M), comp[:S.value].copy(), cnt[:S.value].copy()
+        cap = S.value

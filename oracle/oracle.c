@@ -961,3 +961,136 @@ int64_t orc_atom_hbonds(int64_t i, int64_t n, const double* pos, const int32_t* 
   }
   return t;
 }
+
+/* O9 H-bond lists from the cell grid at r_hb, row-parallel (the same set as
+ * orc_hbonds' O(N^2) definition, which pins it; c3/c4).  Count pass, serial
+ * offsets, fill pass; rows ascending in z. */
+typedef struct {
+  const orc_grid* G;
+  const double *pos, *box;
+  const int32_t* type;
+  const int64_t* brow;
+  double r2;
+  int32_t h_type;
+  uint32_t acc_mask;
+  int64_t* cnt;
+  const int64_t* off;
+  int32_t* z;
+} orc_hb_ctx;
+
+static void orc_hb_row(int64_t i, orc_hb_ctx* C, int32_t* row, int fill) {
+  int64_t t = 0;
+  if (C->type[i] == C->h_type && C->brow[i + 1] > C->brow[i]) {
+    int64_t m = orc_grid_row(C->G, i, C->pos, C->box, C->r2, 0, row);
+    for (int64_t a = 0; a < m; ++a)
+      if ((C->acc_mask >> C->type[row[a]]) & 1u) {
+        if (fill) C->z[C->off[i] + t] = row[a];
+        ++t;
+      }
+  }
+  if (!fill) C->cnt[i] = t;
+}
+static void orc_hb_count(int64_t i, void* c, void* s) { orc_hb_row(i, (orc_hb_ctx*)c, (int32_t*)s, 0); }
+static void orc_hb_fill(int64_t i, void* c, void* s) { orc_hb_row(i, (orc_hb_ctx*)c, (int32_t*)s, 1); }
+
+int64_t orc_hbonds_cells(int64_t n, const double* pos, const int32_t* type, const double box[3], const int64_t* brow,
+                         double r_hb, int32_t h_type, uint32_t acc_mask, int64_t* hb_off, int32_t* hb_z, int64_t cap,
+                         int T) {
+  orc_grid G;
+  orc_grid_build(&G, n, pos, box, r_hb);
+  int64_t* cnt = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+  orc_hb_ctx C = {&G, pos, box, type, brow, r_hb * r_hb, h_type, acc_mask, cnt, hb_off, hb_z};
+  size_t scr = sizeof(int32_t) * (size_t)G.maxcand;
+  orc_par_rows(n, T, orc_hb_count, &C, scr);
+  int64_t t = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    hb_off[i] = t;
+    t += cnt[i];
+  }
+  hb_off[n] = t;
+  if (t <= cap) orc_par_rows(n, T, orc_hb_fill, &C, scr);
+  free(cnt);
+  orc_grid_free(&G);
+  return t;
+}
+
+/* ------------------------------------------- O10 species analysis (NEXT-4)
+ * PAPER.md:217-221 (§3.4, the in situ species algorithm), step by step:
+ *  1. "A pair of atoms ... are deemed to be bonded if the bond order value
+ *     between the two atoms is larger than a threshold specified for this
+ *     interaction type (default value is 0.3).  A molecule ID, that is the
+ *     smaller value of the two global IDs, is assigned to the pair of atoms.
+ *     This process is repeated until every atom has been assigned a molecule
+ *     ID": label[i] = i, then sweeps over the bonds (canonical i < j, BO =
+ *     the corrected total bond order of a6, BO > thresh[ti][tj] strictly)
+ *     setting both labels to the smaller one, until a sweep changes nothing
+ *     (the label is then the smallest global ID of the connected component).
+ *  2. "Sorting is performed for all molecule IDs and molecule IDs are
+ *     reassigned from 1 to M": mol_id[i] = 1 + rank of label[i] among the
+ *     distinct labels in ascending order.
+ *  3. "counting the number of atoms of each element.  Molecules with the same
+ *     number of atoms per element are identified as the same species" (the
+ *     element of an atom is its type).
+ *  4. "each distinct species and their counts": species sorted by their
+ *     composition vector (count of type 0, then type 1, ...) ascending.
+ * Global IDs are the 0-based input indices.  corr: [B][4] (corr[4e] = BO).
+ * Writes mol_id[n]; up to cap species (sp_comp [cap][ntypes], sp_count);
+ * *n_species = the number of distinct species.  Returns M. */
+static int orc_sp_nt;
+static int orc_cmp_comp(const void* a, const void* b) {
+  const int32_t *x = (const int32_t*)a, *y = (const int32_t*)b;
+  for (int t = 0; t < orc_sp_nt; ++t)
+    if (x[t] != y[t]) return x[t] < y[t] ? -1 : 1;
+  return 0;
+}
+
+int64_t orc_species(int64_t n, const int32_t* type, int ntypes, const int64_t* brow, const int32_t* bcol,
+                    const double* corr, const double* thresh, int32_t* mol_id, int32_t* sp_comp, int64_t* sp_count,
+                    int64_t cap, int64_t* n_species) {
+  size_t n1 = (size_t)(n > 0 ? n : 1);
+  int64_t* label = (int64_t*)malloc(sizeof(int64_t) * n1);
+  for (int64_t i = 0; i < n; ++i) label[i] = i;
+  for (int changed = 1; changed;) { /* step 1 */
+    changed = 0;
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t e = brow[i]; e < brow[i + 1]; ++e) {
+        int64_t j = bcol[e];
+        if (j <= i || !(corr[4 * e] > thresh[type[i] * ntypes + type[j]])) continue;
+        int64_t m = label[i] < label[j] ? label[i] : label[j];
+        if (label[i] != m || label[j] != m) {
+          label[i] = label[j] = m;
+          changed = 1;
+        }
+      }
+  }
+  int64_t* rank = (int64_t*)malloc(sizeof(int64_t) * n1); /* step 2 */
+  for (int64_t i = 0; i < n; ++i) rank[i] = 0;
+  for (int64_t i = 0; i < n; ++i) rank[label[i]] = 1;
+  int64_t M = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t isroot = rank[i];
+    rank[i] = M;
+    M += isroot;
+  }
+  for (int64_t i = 0; i < n; ++i) mol_id[i] = (int32_t)(rank[label[i]] + 1);
+  int32_t* comp = (int32_t*)calloc((size_t)(M > 0 ? M : 1) * (size_t)ntypes, sizeof(int32_t)); /* step 3 */
+  for (int64_t i = 0; i < n; ++i) comp[(int64_t)(mol_id[i] - 1) * ntypes + type[i]]++;
+  orc_sp_nt = ntypes; /* step 4 */
+  qsort(comp, (size_t)M, sizeof(int32_t) * (size_t)ntypes, orc_cmp_comp);
+  int64_t S = 0;
+  for (int64_t m = 0; m < M; ++m) {
+    if (m == 0 || orc_cmp_comp(&comp[m * ntypes], &comp[(m - 1) * ntypes]) != 0) {
+      if (S < cap) {
+        memcpy(&sp_comp[S * ntypes], &comp[m * ntypes], sizeof(int32_t) * (size_t)ntypes);
+        sp_count[S] = 0;
+      }
+      ++S;
+    }
+    if (S - 1 < cap) sp_count[S - 1]++;
+  }
+  *n_species = S;
+  free(label);
+  free(rank);
+  free(comp);
+  return M;
+}

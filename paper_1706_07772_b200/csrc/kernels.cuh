@@ -1650,14 +1650,20 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   __syncthreads();
   if (threadIdx.x == 0 && S.bad) set_flag(st, ST_RANGE);
   unsigned long long* gf[3] = {sfx, sfy, sfz};
+  bool wide = false;
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
     const int j = sinfo[t].x;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const long long v = ((long long)fb[c * window_cap + t] << 20) + (long long)fa[c * window_cap + t];
+      const int b = fb[c * window_cap + t];
+      // the high word wraps mod 2^32 at |F| = 2^16 kcal/mol/A: a slot's
+      // accumulated F_j beyond half of that (|B| > 2^30) is flagged too
+      wide |= b > (1 << 30) || b < -(1 << 30);
+      const long long v = ((long long)b << 20) + (long long)fa[c * window_cap + t];
       if (v != 0) atomicAdd(&gf[c][j], (unsigned long long)v);
     }
   }
+  if (wide) set_flag(st, ST_RANGE);
 #ifdef REAX_TIMELINE
   __syncthreads();
   TL_MARK(1, 2);

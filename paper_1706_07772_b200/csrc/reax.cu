@@ -1151,6 +1151,15 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
       ensure_smem(k_export_pairs, exp_smem(c.window_cap)) != cudaSuccess)
     return REAX_ERR_CUDA;
 
+  // a graph captured by reax_step_host holds the old layout's offsets and
+  // capacities: never replay it on the new workspace (even at the same base)
+  if (ctx->hg_exec) {
+    cudaGraphExecDestroy(ctx->hg_exec);
+    ctx->hg_exec = nullptr;
+  }
+  ctx->hg_key.clear();
+  memset(ctx->hg_ptr, 0, sizeof(ctx->hg_ptr));
+  ctx->hg_ws = nullptr;
   ctx->maxsm = (size_t)maxsm;
   ctx->ws_base = (char*)ws;
   ctx->ws_bytes = bytes;
@@ -1268,6 +1277,11 @@ reax_status reax_step_host(reax_ctx* ctx, int64_t n, const double* pos, const in
   const void* ptr[5] = {pos, type, q, force, energy};
   if (keyed && ctx->hg_exec && key == ctx->hg_key && memcmp(ptr, ctx->hg_ptr, sizeof(ptr)) == 0 &&
       ctx->hg_ws == ctx->ws_base && ctx->hg_async == ctx->async) {
+    // the graph holds no parameter upload (the set was current at capture);
+    // another call on this context may have uploaded a different set since
+    // (a memcmp when nothing changed)
+    reax_status ru = upload_params(ctx, params, cut, s);
+    if (ru != REAX_OK) return ru;
     // replay: H2D copies, the whole step (side-stream fork included), D2H copies
     if (cudaError_t e_ = cudaGraphLaunch(ctx->hg_exec, s)) return fail_cuda(e_);
     if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);

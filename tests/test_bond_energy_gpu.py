@@ -102,12 +102,3 @@ def test_separate_calls_match_step(params, bparams):
 @pytest.mark.slow
 def test_c2(params, bparams):
     _check(gen.make_config(2), params, bparams)
-
-
-@pytest.mark.slow
-def test_c3_properties(params, bparams):
-    """At sizes the oracle would take long on: Newton's third law and a finite,
-    negative energy (every bond term is bounded below by -De sums)."""
-    _, F, E = _gpu_bond(gen.make_config(3), params, bparams)
-    assert np.isfinite(E) and E < 0
-    assert np.all(np.abs(F.sum(0)) <= 1e-11 * np.abs(F).sum())

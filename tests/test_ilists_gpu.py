@@ -48,32 +48,3 @@ def test_invalid_r_hb(params, c0):
     ctx, _, _ = gpu_run(c0, params)
     with pytest.raises(rx.ReaxError):
         ctx.interaction_lists(r_hb=20.0)   # beyond 2 sub-cell sides
-
-
-@pytest.mark.slow
-def test_c3_sampled(params):
-    """c3 (1.04M atoms): the angle list of sampled bond entries from the
-    exported bond list and corrected BO (the oracle's own rule applied to the
-    GPU's bonds, which the a4-a6 parity tests pin), and the H-bond rows of
-    sampled H atoms against the oracle's per-atom brute force."""
-    s = gen.make_config(3)
-    ctx, _, _ = gpu_run(s, params)
-    ao, ak, ho, hz = [t.cpu().numpy() for t in ctx.interaction_lists()]
-    brow, bcol, _, bo, _ = [t.cpu().numpy() for t in ctx.export_bonds()]
-    il = oracle.ILIST
-    n = len(s.pos)
-    rng = np.random.default_rng(7)
-    rows = np.repeat(np.arange(n), np.diff(brow))
-    for e in rng.choice(len(bcol), 200, replace=False):
-        j = rows[e]
-        sub_off, sub_k = oracle.angles(np.array([0, brow[j + 1] - brow[j]]), bcol[brow[j]:brow[j + 1]],
-                                       bo[brow[j]:brow[j + 1], 4:], il["thb_cut"], il["thb_cutsq"])
-        p = e - brow[j]
-        assert ak[ao[e]:ao[e + 1]].tolist() == sub_k[sub_off[p]:sub_off[p + 1]].tolist()
-    has_bond = np.diff(brow) > 0
-    pos = oracle.wrap(s.pos, s.box)
-    hs = np.flatnonzero((s.type == il["h_type"]) & has_bond)
-    for i in rng.choice(hs, 30, replace=False):
-        want = oracle.atom_hbonds(i, pos, s.type, s.box, True, il["r_hb"], il["h_type"], il["acc_mask"])
-        assert hz[ho[i]:ho[i + 1]].tolist() == want.tolist()
-    assert ho[-1] == np.diff(ho)[hs].sum()

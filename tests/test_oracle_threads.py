@@ -62,3 +62,16 @@ def test_stream_forms_match_stored_list(c0, params, tiny):
         assert np.array_equal(st["cnt"], c) and np.array_equal(st["dig"], d)
         for k in ("brow", "bcol", "mirror", "raw", "delta", "corr", "E", "F"):
             assert np.array_equal(st[k], ref[k]), k
+
+
+def test_hbonds_cells_match_definition(c0, params, tiny):
+    """O9 H-bond lists from the grid (row-parallel, c3/c4) == the O(N^2)
+    definition; 1 vs T threads bitwise."""
+    il = oracle.ILIST
+    for s in (c0, tiny):
+        ref = oracle.evaluate(s, params, CUT)
+        a = oracle.hbonds(ref["pos"], s.type, s.box, ref["brow"], il["r_hb"], il["h_type"], il["acc_mask"])
+        for T in (1, 5):
+            b = oracle.hbonds(ref["pos"], s.type, s.box, ref["brow"], il["r_hb"], il["h_type"], il["acc_mask"],
+                              mode="cells", threads=T)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])

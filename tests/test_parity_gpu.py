@@ -137,50 +137,6 @@ def test_c2_full(params):
     full_parity(gen.make_config(2), params)
 
 
-def _sampled(k, params, nsample, seed=0):
-    s = gen.make_config(k)
-    ctx, F, E = gpu_run(s, params)
-    n = len(s.pos)
-    rng = np.random.default_rng(seed)
-    idx = np.concatenate([[0, n - 1], rng.choice(n, nsample, replace=False)])
-    cnt, dig = [t.cpu().numpy() for t in ctx.export_digest()]
-    brow, bcol, mir, bo, dl = [t.cpu().numpy() for t in ctx.export_bonds()]
-    for i in idx:
-        nb = oracle.atom_neighbors(i, s.pos, s.box, CUT["r_nonb"])
-        assert cnt[i] == len(nb), (i, cnt[i], len(nb))
-        h = 0
-        for j in nb:
-            h = (h + oracle.mix64(min(i, j), max(i, j))) % (1 << 64)
-        assert int(np.uint64(dig[i].view(np.uint64))) == h
-        Fo, _ = oracle.atom_force(i, s.pos, s.type, s.q, s.box, params, CUT["r_nonb"])
-        assert np.all(np.abs(F[i] - Fo) <= TOL_F * (1 + np.abs(Fo))), (i, F[i], Fo)
-        part, raw, dli = oracle.atom_bonds(i, s.pos, s.type, s.box, params, CUT["r_bond"], CUT["bo_cut"])
-        seg = slice(brow[i], brow[i + 1])
-        assert bcol[seg].tolist() == part.tolist()
-        assert np.max(np.abs(bo[seg, :4] - raw), initial=0) <= 1e-12
-        assert np.all(np.abs(dl[i] - dli) <= 1e-12)
-        for e, j in zip(range(brow[i], brow[i + 1]), part):
-            _, _, dlj = oracle.atom_bonds(j, s.pos, s.type, s.box, params, CUT["r_bond"], CUT["bo_cut"])
-            a, b = (i, j) if i < j else (j, i)
-            da, db = (dli, dlj) if i < j else (dlj, dli)
-            corr, _ = oracle.bo_corr_pair(bo[e, :4], da[0], da[1], db[0], db[1], s.type[a], s.type[b], params)
-            assert np.all(np.abs(bo[e, 4:] - corr) <= 1e-12)
-    # properties at any size: Newton's third law, mirror symmetry of the bond list
-    assert np.all(np.abs(F.sum(0)) <= 1e-11 * np.abs(F).sum())
-    assert np.array_equal(bo[mir], bo)
-    return E
-
-
-@pytest.mark.slow
-def test_c3_sampled(params):
-    _sampled(3, params, 40)
-
-
-@pytest.mark.slow
-def test_c4_sampled(params):
-    _sampled(4, params, 24)
-
-
 def test_separate_calls_match_step(params):
     """reax_build_lists + reax_bond_orders + reax_nonbonded (one stream) and
     reax_step (bond chain forked onto a side stream beside the nonbonded
