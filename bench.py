@@ -441,6 +441,55 @@ def main():
                   "angle_entries": sizes[0], "hbond_entries": sizes[1]}
     except Exception as ex:   # reported, never silently dropped
         ilists = {"error": str(ex)}
+    # NEXT-4 (outside `value`): reax_species on the step's bond orders
+    species = None
+    try:
+        one_step()
+        torch.cuda.synchronize()
+        ctx.species()
+        sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+        for k in range(3):
+            flush.fill_(float(k))
+            sev[k][0].record()
+            _, M, comp, cnt = ctx.species()
+            sev[k][1].record()
+        torch.cuda.synchronize()
+        species = {"row": "NEXT-4 species analysis (reax_species: union-find, renumbering, census; synchronous)",
+                   "ms_per_call": sum(a.elapsed_time(b) for a, b in sev) / 3, "molecules": M, "species": len(comp),
+                   "bo_threshold": 0.3}
+    except Exception as ex:   # reported, never silently dropped
+        species = {"error": str(ex)}
+    # NEXT-2 (outside `value`): QEq on the step's half list (H build, then the
+    # dual Jacobi-PCG at the paper's tolerance 1e-6 from zero guesses), if the
+    # doubly stored H fits beside the workspace
+    qeq = None
+    try:
+        qp = gen.make_qeq_params()
+        free, _ = torch.cuda.mem_get_info(dev)
+        need = 2 * P * 12 + n * 120
+        if need > free - (4 << 30):
+            qeq = {"skipped": f"H needs {need / 2**30:.1f} GiB, {free / 2**30:.1f} GiB free"}
+        else:
+            qeq_ms = []
+            for k in range(2):
+                flush.fill_(float(k))
+                a, b, c_ = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                a.record()
+                ctx.qeq_build()
+                b.record()
+                qq, ss, tt, it = ctx.qeq_solve(qp.chi, qp.eta, tol=1e-6)
+                c_.record()
+                torch.cuda.synchronize()
+                qeq_ms.append((a.elapsed_time(b), b.elapsed_time(c_), it))
+            bms, sms, it = qeq_ms[-1]
+            qeq = {"row": "NEXT-2 QEq (reax_qeq_build + reax_qeq_solve, tol 1e-6, zero guesses)", "build_ms": bms,
+                   "solve_ms": sms, "iterations": it, "spmv_bytes_per_iter": 2 * P * 12 + n * 32,
+                   "ms_per_iteration": sms / max(1, max(it)),
+                   "achieved_gbs_per_iteration": (2 * P * 12 + n * 32) / (sms / max(1, max(it)) * 1e-3) / 1e9}
+            ctx._qeq_scratch = None
+            torch.cuda.empty_cache()
+    except Exception as ex:
+        qeq = {"error": str(ex)}
     nb_ms, _ = kms["nonbonded"]
     nb_avg_s = nb_ms / args.steps * 1e-3
     achieved = W_NB_DP_PER_PAIR * P / nb_avg_s
@@ -533,7 +582,7 @@ def main():
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,
         "e2e": e2e,
-        "next_rows": {"bond_energy": bond_energy, "interaction_lists": ilists},
+        "next_rows": {"bond_energy": bond_energy, "interaction_lists": ilists, "species": species, "qeq": qeq},
         "clocks": clocks,
     }
     if c1 is not None:

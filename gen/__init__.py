@@ -165,3 +165,24 @@ def make_bond_params(seed: int = BOND_SEED, ntypes: int = NTYPES) -> BondParams:
     pp = np.empty((ntypes, ntypes, 4), np.float64)
     _get().gen_bond_params(seed, ntypes, pp.ctypes.data)
     return BondParams(*(np.ascontiguousarray(pp[:, :, k]) for k in range(4)))
+
+
+QEQ_SEED = SEED_BASE + 8000
+
+
+@dataclass
+class QEqParams:
+    """QEq parameters per type (NEXT-2; reading 33): electronegativity
+    chi (kcal/mol/e) and hardness eta = H_ii (kcal/mol/e^2)."""
+    chi: np.ndarray
+    eta: np.ndarray
+
+    def copy(self) -> "QEqParams":
+        return QEqParams(self.chi.copy(), self.eta.copy())
+
+
+def make_qeq_params(seed: int = QEQ_SEED, ntypes: int = NTYPES) -> QEqParams:
+    """chi ~ U[80, 200] kcal/mol/e (3.5-8.7 eV), eta ~ U[350, 500] kcal/mol/e^2
+    (ReaxFF's 2 eta of 7.6-10.8 eV): per type, chi then eta, from SplitMix64."""
+    u = uniforms(seed, 2 * ntypes)
+    return QEqParams(80.0 + 120.0 * u[:ntypes], 350.0 + 150.0 * u[ntypes:])

@@ -61,7 +61,9 @@ typedef enum {
   REAX_ERR_RANGE = 9      /* a pair force |dE/dr| or a row force component >= 65536 kcal/mol/A, or
                              one CTA's accumulated partial force on a window atom beyond 32768
                              kcal/mol/A: outside the fixed-point force accumulator (2^-35
-                             resolution); results are then undefined */
+                             resolution); results are then undefined */,
+  REAX_ERR_CONVERGENCE = 10 /* QEq: a system not converged to tol within maxiter (results are the
+                               last iterates) */
 } reax_status;
 
 #define REAX_MAX_TYPES 16
@@ -195,6 +197,62 @@ reax_status reax_interaction_counts(reax_ctx* ctx, const reax_ilist_params* para
 reax_status reax_interaction_lists(reax_ctx* ctx, const reax_ilist_params* params, int64_t* ang_off, int32_t* ang_k,
                                    int64_t* hb_off, int32_t* hb_z, void* stream);
 
+/* NEXT-2: QEq charge equilibration, PAPER.md:204-208 (§3.3
+ * "QEq"; reading 33).  The charges minimise
+ *   E(q) = sum_i (chi_i q_i + 1/2 eta_i q_i^2) + sum_{i<j} H_ij q_i q_j,  sum_i q_i = 0,
+ * i.e. H s = -chi, H t = -1 ("two linear systems ... with a common kernel H"),
+ * q = s - (sum s / sum t) t, with H_ii = eta_i and H_ij = C Tap(r_ij)
+ * (r_ij^3 + gamma_ij^-3)^(-1/3) for the pairs of the current half list (the
+ * shielded Coulomb kernel of the nonbonded term without charges; positions
+ * and parameters of the last reax_build_lists / reax_step).
+ *  - reax_qeq_bytes: scratch bytes for the current list ([dev] caller-owned,
+ *    256-byte aligned); synchronises `stream`.
+ *  - reax_qeq_build: computes every unique H_ij once from the half list and
+ *    stores it in scratch (both row segments, sorted: deterministic).  The
+ *    scratch then belongs to this list: a new build of the lists (or another
+ *    scratch pointer) makes the solves return REAX_ERR_STATE.
+ *  - reax_qeq_matvec: y = H x for two vectors ([dev] n fp64 each, input
+ *    order); eta [host] ntypes.
+ *  - reax_qeq_solve: Jacobi-preconditioned CG on both systems at once (one
+ *    pass over H per iteration serves both right-hand sides), each to
+ *    ||b - H x|| <= tol ||b|| (the paper's runs: tol = 1e-6) or
+ *    maxiter iterations.  chi, eta [host] ntypes (eta > 0); s, t [dev] n fp64
+ *    in/out: initial guesses in (zeros, or an extrapolation of earlier
+ *    solutions), solutions out; q [dev] n fp64 out; iters [host]
+ *    2 (iterations of the s and t systems).  REAX_ERR_CONVERGENCE if either
+ *    system is not converged after maxiter.  Synchronous on `stream`;
+ *    deterministic (fixed summation order everywhere). */
+reax_status reax_qeq_bytes(reax_ctx* ctx, size_t* bytes, void* stream);
+reax_status reax_qeq_build(reax_ctx* ctx, void* scratch, size_t scratch_bytes, void* stream);
+reax_status reax_qeq_matvec(reax_ctx* ctx, const double* eta, void* scratch, size_t scratch_bytes, const double* x_s,
+                            const double* x_t, double* y_s, double* y_t, void* stream);
+reax_status reax_qeq_solve(reax_ctx* ctx, const double* chi, const double* eta, double tol, int32_t maxiter,
+                           void* scratch, size_t scratch_bytes, double* s, double* t, double* q, int32_t* iters,
+                           void* stream);
+
+/* NEXT-4: in situ molecular species analysis of the
+ * corrected bond orders of the last reax_bond_orders / reax_step
+ * (§3.4 "A Tool for Molecular Species Analysis"):
+ *   - atoms i, j are bonded iff BO_ij > bo_threshold[t_i * nt + t_j] (strict;
+ *     bo_threshold [host] nt*nt symmetric, or NULL for the paper's default 0.3);
+ *   - the molecule ID of an atom is the smallest global ID (0-based input
+ *     index) of its connected component ("the smaller value of the two global
+ *     IDs ... repeated until every atom has been assigned a molecule ID");
+ *   - molecule IDs are sorted and renumbered 1..M: mol_id [dev] n int32, input
+ *     order; *n_molecules = M;
+ *   - species = molecules with the same number of atoms per element (type):
+ *     species_comp [host] species_cap*nt int32 (atoms of each type),
+ *     species_count [host] species_cap int64 (molecules), sorted by the
+ *     composition vector ascending; *n_species = the number of species
+ *     (REAX_ERR_CAPACITY, with *n_species set, if it exceeds species_cap).
+ * scratch [dev] is caller-owned, >= reax_species_bytes(n, nt), 256-byte
+ * aligned (REAX_ERR_CAPACITY if smaller).  Synchronous on `stream`.
+ * REAX_ERR_STATE without a current bond list. */
+reax_status reax_species_bytes(int64_t n, int32_t ntypes, size_t* bytes);
+reax_status reax_species(reax_ctx* ctx, const double* bo_threshold, void* scratch, size_t scratch_bytes,
+                         int32_t* mol_id, int64_t* n_molecules, int32_t* species_comp, int64_t* species_count,
+                         int64_t species_cap, int64_t* n_species, void* stream);
+
 /* a7-a8: Alg. 2 over the half list: tapered shielded vdW + Coulomb (N1-N6)
  * at the given charges.  q [dev] n fp64; force [dev] n*3 fp64 (overwritten,
  * input order, F = -dE/dx); energy [dev] 2 fp64 {E_vdW, E_Coul}
@@ -226,8 +284,9 @@ reax_status reax_check(reax_ctx* ctx, void* stream);
  * (bond evaluation, scan, fill, row sort + Delta'), 3 "bond_orders"
  * (k_bond_correct), 4 "nonbonded" (k_nonbonded alone), 5 "other" (work plan, charge
  * gather, force un-permute, energy reduction), 6 "bond_energy" (NEXT-1,
- * reax_bond_energy). */
-#define REAX_NKERNELS 7
+ * reax_bond_energy), 7 "species" (NEXT-4, reax_species), 8 "qeq" (NEXT-2,
+ * reax_qeq). */
+#define REAX_NKERNELS 9
 reax_status reax_set_timing(reax_ctx* ctx, int enable);
 /* Accumulated milliseconds and launch counts per kernel group since the last
  * reset (synchronises the last recorded events).  reset = 0: accumulate and

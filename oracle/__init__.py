@@ -127,6 +127,9 @@ def _get():
             "orc_hbonds": (I64, [I64, V, V, V, V, DBL, ctypes.c_int32, ctypes.c_uint32, V, V, I64]),
             "orc_hbonds_cells": (I64, [I64, V, V, V, V, DBL, ctypes.c_int32, ctypes.c_uint32, V, V, I64, INT]),
             "orc_species": (I64, [I64, V, INT, V, V, V, V, V, V, V, I64, V]),
+            "orc_qeq_H": (None, [I64, V, V, V, V, DBL, V, V, V]),
+            "orc_qeq_spmv": (None, [I64, V, V, V, V, V, V]),
+            "orc_qeq": (None, [I64, V, V, V, V, DBL, V, V, V, V, DBL, INT, V, V, V, V]),
             "orc_atom_hbonds": (I64, [I64, I64, V, V, V, INT, DBL, ctypes.c_int32, ctypes.c_uint32, V, I64]),
         }
         for name, (res, args) in sig.items():
@@ -480,3 +483,41 @@ def species(type_, ntypes, brow, bcol, corr, thresh=SPECIES_BO_THRESH):
         if S.value <= cap:
             return mol, int(M), comp[:S.value].copy(), cnt[:S.value].copy()
         cap = S.value
+
+
+# NEXT-2: QEq convergence tolerance of the paper's runs
+QEQ_TOL = 1e-6
+
+
+def qeq_H(pos, type_, box, params, R, hrow, hcol):
+    """O11: H_ij of every canonical half-list pair (aligned with hcol)."""
+    P = _P(params)
+    pos, type_, box = _a(pos, np.float64), _a(type_, np.int32), _a(box, np.float64)
+    hrow, hcol = _a(hrow, np.int64), _a(hcol, np.int32)
+    hval = np.empty(len(hcol))
+    _get().orc_qeq_H(len(pos), _ptr(pos), _ptr(type_), _ptr(box), P.ref, float(R), _ptr(hrow), _ptr(hcol), _ptr(hval))
+    return hval
+
+
+def qeq_spmv(eta_atom, hrow, hcol, hval, x):
+    eta_atom, hrow, hcol, hval, x = (_a(eta_atom, np.float64), _a(hrow, np.int64), _a(hcol, np.int32),
+                                     _a(hval, np.float64), _a(x, np.float64))
+    y = np.empty_like(x)
+    _get().orc_qeq_spmv(len(x), _ptr(eta_atom), _ptr(hrow), _ptr(hcol), _ptr(hval), _ptr(x), _ptr(y))
+    return y
+
+
+def qeq(pos, type_, box, params, R, hrow, hcol, chi, eta, tol=QEQ_TOL, maxiter=1000, s0=None, t0=None):
+    """O11 QEq: (q, s, t, iters[2]) with H s = -chi, H t = -1, q = s - (sum s/sum t) t."""
+    P = _P(params)
+    pos, type_, box = _a(pos, np.float64), _a(type_, np.int32), _a(box, np.float64)
+    hrow, hcol = _a(hrow, np.int64), _a(hcol, np.int32)
+    n = len(pos)
+    s = np.zeros(n) if s0 is None else np.array(s0, np.float64)
+    t = np.zeros(n) if t0 is None else np.array(t0, np.float64)
+    q = np.empty(n)
+    it = np.zeros(2, np.int32)
+    _get().orc_qeq(n, _ptr(pos), _ptr(type_), _ptr(box), P.ref, float(R), _ptr(hrow), _ptr(hcol),
+                   _ptr(_a(chi, np.float64)), _ptr(_a(eta, np.float64)), float(tol), int(maxiter), _ptr(s), _ptr(t),
+                   _ptr(q), _ptr(it))
+    return q, s, t, it

@@ -1094,3 +1094,107 @@ int64_t orc_species(int64_t n, const int32_t* type, int ntypes, const int64_t* b
   free(comp);
   return M;
 }
+
+/* ------------------------------------------------------- O11 QEq (NEXT-2)
+ * PAPER.md:204-208 (§3.3 "QEq"): charges minimise
+ *   E(q) = sum_i (chi_i q_i + 1/2 eta_i q_i^2) + sum_{i<j} H_ij q_i q_j
+ * subject to sum_i q_i = 0 (reading 33).  With Lagrange multipliers
+ * this gives "two linear systems of equations ... with a common kernel H, an
+ * N x N sparse matrix": H s = -chi, H t = -1, and q = s - (sum s / sum t) t.
+ * H_ii = eta_i; H_ij = C Tap(r_ij) (r_ij^3 + gamma_ij^-3)^(-1/3) for the pairs
+ * of the half list ("a truncated electrostatics interaction"; the shielded
+ * Coulomb kernel of N5 without the charges, orc_taper x orc_coulomb_kernel),
+ * stored once per unordered pair ("only unique, non-zero elements of the
+ * sparse matrix are computed and stored").  Solved by "a diagonally
+ * preconditioned ... CG solver" (Jacobi-PCG, preconditioner 1/eta_i), each
+ * system from its initial guess to ||b - H x|| <= tol ||b|| (PAPER.md:243:
+ * QEq tolerance 1e-6). */
+
+/* H_ij of every canonical pair (hval[P], aligned with hcol). */
+void orc_qeq_H(int64_t n, const double* pos, const int32_t* type, const double box[3], const orc_params* P,
+               double R, const int64_t* hrow, const int32_t* hcol, double* hval) {
+  double d[3], tap, dtap, k, dk;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = hrow[i]; p < hrow[i + 1]; ++p) {
+      int64_t j = hcol[p];
+      double r = sqrt(orc_dist2(pos, i, j, box, d));
+      orc_taper(r, R, &tap, &dtap);
+      orc_coulomb_kernel(r, type[i], type[j], P, &k, &dk);
+      hval[p] = P->coulomb_c * tap * k;
+    }
+}
+
+/* y = H x over the half-stored H: y_i = eta_i x_i + sum_{j in row i} H_ij x_j,
+ * and y_j += H_ij x_i for each stored (i, j). */
+void orc_qeq_spmv(int64_t n, const double* eta_atom, const int64_t* hrow, const int32_t* hcol, const double* hval,
+                  const double* x, double* y) {
+  for (int64_t i = 0; i < n; ++i) y[i] = eta_atom[i] * x[i];
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = hrow[i]; p < hrow[i + 1]; ++p) {
+      int64_t j = hcol[p];
+      y[i] += hval[p] * x[j];
+      y[j] += hval[p] * x[i];
+    }
+}
+
+static double orc_dot(int64_t n, const double* a, const double* b) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+
+/* Jacobi-PCG on H x = b from the initial x (in/out); returns the iterations. */
+int orc_qeq_pcg(int64_t n, const double* eta_atom, const int64_t* hrow, const int32_t* hcol, const double* hval,
+                const double* b, double* x, double tol, int maxiter) {
+  size_t n1 = (size_t)(n > 0 ? n : 1);
+  double *r = (double*)malloc(sizeof(double) * n1), *z = (double*)malloc(sizeof(double) * n1);
+  double *p = (double*)malloc(sizeof(double) * n1), *Ap = (double*)malloc(sizeof(double) * n1);
+  orc_qeq_spmv(n, eta_atom, hrow, hcol, hval, x, Ap);
+  for (int64_t i = 0; i < n; ++i) {
+    r[i] = b[i] - Ap[i];
+    z[i] = r[i] / eta_atom[i];
+    p[i] = z[i];
+  }
+  double bn = sqrt(orc_dot(n, b, b)), rz = orc_dot(n, r, z);
+  int it = 0;
+  while (it < maxiter && sqrt(orc_dot(n, r, r)) > tol * bn) {
+    orc_qeq_spmv(n, eta_atom, hrow, hcol, hval, p, Ap);
+    double alpha = rz / orc_dot(n, p, Ap);
+    for (int64_t i = 0; i < n; ++i) {
+      x[i] += alpha * p[i];
+      r[i] -= alpha * Ap[i];
+      z[i] = r[i] / eta_atom[i];
+    }
+    double rz1 = orc_dot(n, r, z), beta = rz1 / rz;
+    rz = rz1;
+    for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    ++it;
+  }
+  free(r); free(z); free(p); free(Ap);
+  return it;
+}
+
+/* The whole QEq: H, then s (H s = -chi), t (H t = -1) from the guesses in
+ * s, t (in/out), q = s - (sum s / sum t) t.  chi, eta per type.  iters[2]. */
+void orc_qeq(int64_t n, const double* pos, const int32_t* type, const double box[3], const orc_params* P,
+             double R, const int64_t* hrow, const int32_t* hcol, const double* chi, const double* eta, double tol,
+             int maxiter, double* s, double* t, double* q, int* iters) {
+  size_t n1 = (size_t)(n > 0 ? n : 1);
+  int64_t np = hrow[n];
+  double* hval = (double*)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1));
+  double *ea = (double*)malloc(sizeof(double) * n1), *bs = (double*)malloc(sizeof(double) * n1),
+         *bt = (double*)malloc(sizeof(double) * n1);
+  orc_qeq_H(n, pos, type, box, P, R, hrow, hcol, hval);
+  for (int64_t i = 0; i < n; ++i) {
+    ea[i] = eta[type[i]];
+    bs[i] = -chi[type[i]];
+    bt[i] = -1.0;
+  }
+  iters[0] = orc_qeq_pcg(n, ea, hrow, hcol, hval, bs, s, tol, maxiter);
+  iters[1] = orc_qeq_pcg(n, ea, hrow, hcol, hval, bt, t, tol, maxiter);
+  double ss = 0.0, st = 0.0;
+  for (int64_t i = 0; i < n; ++i) { ss += s[i]; st += t[i]; }
+  double mu = ss / st;
+  for (int64_t i = 0; i < n; ++i) q[i] = s[i] - mu * t[i];
+  free(hval); free(ea); free(bs); free(bt);
+}

@@ -19,14 +19,16 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("REAX_LIBRARY", os.path.join(_HERE, "libreax.so"))
 
-OK, ERR_ARG, ERR_BOX, ERR_CUTOFF, ERR_PARAM, ERR_CAPACITY, ERR_NONFINITE, ERR_CUDA, ERR_STATE, ERR_RANGE = range(10)
-KERNEL_GROUPS = ("bin", "nbr", "bonds", "bond_orders", "nonbonded", "other", "bond_energy")
+(OK, ERR_ARG, ERR_BOX, ERR_CUTOFF, ERR_PARAM, ERR_CAPACITY, ERR_NONFINITE, ERR_CUDA, ERR_STATE, ERR_RANGE,
+ ERR_CONVERGENCE) = range(11)
+KERNEL_GROUPS = ("bin", "nbr", "bonds", "bond_orders", "nonbonded", "other", "bond_energy", "species", "qeq")
 EXPORTED = ("reax_status_str", "reax_create", "reax_destroy", "reax_workspace_bytes", "reax_bind_workspace",
             "reax_required", "reax_build_lists", "reax_bond_orders", "reax_nonbonded", "reax_step",
             "reax_step_host", "reax_set_async", "reax_check", "reax_set_timing", "reax_kernel_ms",
             "reax_launches_per_step", "reax_pair_count", "reax_export_pairs", "reax_export_nbr_digest",
             "reax_export_bonds", "reax_selftest_math", "reax_last_cuda_error", "reax_bond_energy",
-            "reax_interaction_counts", "reax_interaction_lists")
+            "reax_interaction_counts", "reax_interaction_lists", "reax_qeq_bytes", "reax_qeq_build",
+            "reax_qeq_matvec", "reax_qeq_solve", "reax_species_bytes", "reax_species")
 
 
 class ReaxError(RuntimeError):
@@ -112,6 +114,13 @@ def load_library(path: str = LIB_PATH):
         "reax_export_nbr_digest": (ctypes.c_int, [V, P, P, P]),
         "reax_export_bonds": (ctypes.c_int, [V, P, P, P, P, P, P]),
         "reax_selftest_math": (ctypes.c_int, [V, I64, P, P, P, P, P]),
+        "reax_qeq_bytes": (ctypes.c_int, [V, ctypes.POINTER(ctypes.c_size_t), P]),
+        "reax_qeq_build": (ctypes.c_int, [V, P, ctypes.c_size_t, P]),
+        "reax_qeq_matvec": (ctypes.c_int, [V, P, P, ctypes.c_size_t, P, P, P, P, P]),
+        "reax_qeq_solve": (ctypes.c_int, [V, P, P, ctypes.c_double, I32, P, ctypes.c_size_t, P, P, P, P, P]),
+        "reax_species_bytes": (ctypes.c_int, [I64, I32, ctypes.POINTER(ctypes.c_size_t)]),
+        "reax_species": (ctypes.c_int, [V, P, P, ctypes.c_size_t, P, ctypes.POINTER(I64), P, P, I64,
+                                        ctypes.POINTER(I64), P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -288,6 +297,86 @@ class Reax:
         _check(self.lib.reax_interaction_lists(self.ctx, ctypes.byref(ip), ptr(ao), ptr(ak), ptr(ho), ptr(hz),
                                                _stream_ptr(stream)), "reax_interaction_lists")
         return ao, ak[:na.value], ho, hz[:nh.value]
+
+    # ------------------------------------------------------------ NEXT-2 QEq
+    def qeq_build(self, stream=None):
+        """reax_qeq_build: H of the current half list into a scratch buffer owned
+        by this object (regrown when the list needs more)."""
+        need = ctypes.c_size_t()
+        _check(self.lib.reax_qeq_bytes(self.ctx, ctypes.byref(need), _stream_ptr(stream)), "reax_qeq_bytes")
+        if getattr(self, "_qeq_scratch", None) is None or self._qeq_scratch.numel() < need.value:
+            self._qeq_scratch = None
+            self._qeq_scratch = torch.empty(int(need.value), dtype=torch.uint8, device=self.device)
+        _check(self.lib.reax_qeq_build(self.ctx, ctypes.c_void_p(self._qeq_scratch.data_ptr()),
+                                       self._qeq_scratch.numel(), _stream_ptr(stream)), "reax_qeq_build")
+
+    def _qeq_args(self):
+        return ctypes.c_void_p(self._qeq_scratch.data_ptr()), self._qeq_scratch.numel()
+
+    def qeq_matvec(self, eta, x_s, x_t, stream=None):
+        """reax_qeq_matvec: (H x_s, H x_t) with the built H (input order)."""
+        import numpy as np
+        e = np.ascontiguousarray(eta, np.float64)
+        ys = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        yt = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        sp, nb = self._qeq_args()
+        d = lambda t, nm: _dptr(t, torch.float64, (self.n,), nm)
+        _check(self.lib.reax_qeq_matvec(self.ctx, e.ctypes.data, sp, nb, d(x_s, "x_s"), d(x_t, "x_t"), d(ys, "y_s"),
+                                        d(yt, "y_t"), _stream_ptr(stream)), "reax_qeq_matvec")
+        return ys, yt
+
+    def qeq_solve(self, chi, eta, tol=1e-6, maxiter=1000, s=None, t=None, q=None, stream=None):
+        """reax_qeq_solve: dual Jacobi-PCG from the guesses in s, t (zeros if
+        None; updated in place).  Returns (q, s, t, iters[2])."""
+        import numpy as np
+        c = np.ascontiguousarray(chi, np.float64)
+        e = np.ascontiguousarray(eta, np.float64)
+        s = s if s is not None else torch.zeros(self.n, dtype=torch.float64, device=self.device)
+        t = t if t is not None else torch.zeros(self.n, dtype=torch.float64, device=self.device)
+        q = q if q is not None else torch.empty(self.n, dtype=torch.float64, device=self.device)
+        it = (ctypes.c_int32 * 2)()
+        sp, nb = self._qeq_args()
+        d = lambda x, nm: _dptr(x, torch.float64, (self.n,), nm)
+        _check(self.lib.reax_qeq_solve(self.ctx, c.ctypes.data, e.ctypes.data, float(tol), int(maxiter), sp, nb,
+                                       d(s, "s"), d(t, "t"), d(q, "q"), it, _stream_ptr(stream)), "reax_qeq_solve")
+        return q, s, t, [it[0], it[1]]
+
+    def qeq(self, qeq_params, tol=1e-6, maxiter=1000, s=None, t=None, q=None, stream=None):
+        """H of the current lists, then the solve (NEXT-2)."""
+        self.qeq_build(stream)
+        return self.qeq_solve(qeq_params.chi, qeq_params.eta, tol, maxiter, s, t, q, stream)
+
+    def species(self, bo_threshold=None, mol_id=None, stream=None):
+        """reax_species (NEXT-4): molecules of the current corrected bond orders
+        (bonds with BO > threshold, default 0.3) and the species census.
+        Returns (mol_id int32[n] on the device, 1..M, M, comp int32[S, nt]
+        (numpy, sorted), count int64[S] (numpy))."""
+        import numpy as np
+        nt = int(self.params.s.ntypes)
+        need = ctypes.c_size_t()
+        _check(self.lib.reax_species_bytes(self.n, nt, ctypes.byref(need)), "reax_species_bytes")
+        if getattr(self, "_sp_scratch", None) is None or self._sp_scratch.numel() < need.value:
+            self._sp_scratch = torch.empty(int(need.value), dtype=torch.uint8, device=self.device)
+        mol_id = mol_id if mol_id is not None else torch.empty(self.n, dtype=torch.int32, device=self.device)
+        th = None
+        if bo_threshold is not None:
+            th = np.ascontiguousarray(np.broadcast_to(np.asarray(bo_threshold, np.float64), (nt, nt)))
+        M, S = ctypes.c_int64(), ctypes.c_int64()
+        cap = getattr(self, "_sp_cap", 4096)
+        while True:
+            comp = np.empty((cap, nt), np.int32)
+            cnt = np.empty(cap, np.int64)
+            code = self.lib.reax_species(self.ctx, th.ctypes.data if th is not None else None,
+                                         ctypes.c_void_p(self._sp_scratch.data_ptr()), self._sp_scratch.numel(),
+                                         _dptr(mol_id, torch.int32, (self.n,), "mol_id"), ctypes.byref(M),
+                                         comp.ctypes.data, cnt.ctypes.data, cap, ctypes.byref(S),
+                                         _stream_ptr(stream))
+            if code == ERR_CAPACITY and S.value > cap:
+                cap = int(S.value)
+                self._sp_cap = cap
+                continue
+            _check(code, "reax_species")
+            return mol_id, int(M.value), comp[:S.value].copy(), cnt[:S.value].copy()
 
     def step(self, pos, type_, q, force=None, energy=None, stream=None):
         force = force if force is not None else torch.empty((self.n, 3), dtype=torch.float64, device=self.device)

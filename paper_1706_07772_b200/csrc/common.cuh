@@ -95,6 +95,7 @@ enum : int {
   ST_NONFINITE_OUT = 64,
   ST_RANGE = 128,           // a force contribution outside the fixed-point range
   ST_HB_OVF = 512,          // an H atom's H-bond list beyond HB_CAP entries
+  ST_QEQ_UNSORTED = 1024,   // a QEq lower segment too long to sort (results stay correct, not reproducible)
 };
 
 struct Status {

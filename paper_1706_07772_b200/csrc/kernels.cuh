@@ -2204,4 +2204,465 @@ __global__ void k_export_bonds(int n, const int* __restrict__ iperm, const int* 
   }
 }
 
+// ====================================================== NEXT-4 species analysis
+// PAPER.md:217-221 (§3.4): bonds with BO > threshold (per type pair, default
+// 0.3) join atoms into molecules labelled by their smallest global (input)
+// index, renumbered 1..M in label order; species = molecules with the same
+// atom count per element (type).  GPU form: a lock-free union-find over the
+// bond list in input-index space (a root is only ever hooked under a smaller
+// root, so every tree's root is its smallest index and the final labels do
+// not depend on the order of the unions), a scan of the roots for the
+// renumbering, per-root composition counters, and an open-addressing hash
+// table keyed by the composition vector for the census (the host sorts the
+// few distinct species).
+struct SpThr {
+  double t[NT_MAX * NT_MAX];
+};
+
+__device__ __forceinline__ int sp_find(int* P, int x) {
+  for (;;) {   // path halving; P[x] <= x always, so every shortcut is an ancestor
+    const int p = __ldcg(P + x);
+    if (p == x) return x;
+    const int g = __ldcg(P + p);
+    if (g != p) P[x] = g;
+    x = g;
+  }
+}
+
+__global__ void k_sp_init(int n, int* __restrict__ parent) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) parent[i] = i;
+}
+
+// one canonical entry (original i < j) per bond: unite(i, j) if BO > thr
+__global__ void k_sp_union(const int* __restrict__ brow, int n, const int* __restrict__ bown,
+                           const int* __restrict__ bcol, const int* __restrict__ bkey, const int* __restrict__ perm,
+                           const int* __restrict__ stype, const double* __restrict__ bo, int nt, SpThr thr,
+                           int* parent) {
+  const int B = brow[n];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < B; e += gridDim.x * blockDim.x) {
+    const int so = bown[e];
+    int a = perm[so], b = bkey[e];
+    if (a >= b) continue;
+    if (!(bo[8 * (int64_t)e + 4] > thr.t[stype[so] * nt + stype[bcol[e]]])) continue;
+    for (;;) {
+      a = sp_find(parent, a);
+      b = sp_find(parent, b);
+      if (a == b) break;
+      if (a > b) { const int t = a; a = b; b = t; }
+      const int old = atomicCAS(parent + b, b, a);   // hook the larger root under the smaller
+      if (old == b) break;
+      b = old;
+    }
+  }
+}
+
+// after all unions: parent[i] = root (the component's smallest index);
+// isroot for the renumbering scan; per-root composition counts
+__global__ void k_sp_count(int n, const int* __restrict__ perm, const int* __restrict__ stype, int nt, int* parent,
+                           int* __restrict__ isroot, int* __restrict__ comp) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const int i = perm[s];
+    const int r = sp_find(parent, i);
+    isroot[i] = r == i;
+    atomicAdd(comp + (int64_t)r * nt + stype[s], 1);
+  }
+}
+
+__device__ __forceinline__ uint64_t sp_hash(const int* __restrict__ c, int nt) {
+  uint64_t h = 0x9E3779B97F4A7C15ull;
+  for (int t = 0; t < nt; ++t) {
+    h ^= (uint64_t)(unsigned)c[t] + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
+  }
+  return h;
+}
+
+// mol_id[i] = 1 + rank of root(i) (exclusive scan of isroot); roots insert
+// their composition into the species table (rep = a root holding that
+// composition, cnt = molecules)
+__global__ void k_sp_label(int n, const int* __restrict__ parent, const long long* __restrict__ rank,
+                           int* __restrict__ mol_id, const int* __restrict__ comp, int nt, int2* table,
+                           unsigned mask) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    // read-only walk to the root (no kernel writes parent any more; a root
+    // written by one thread of k_sp_count may have been overwritten there by
+    // another thread's path halving with an ancestor, so parent[i] itself
+    // need not be the root)
+    int r = i;
+    for (int p = parent[r]; p != r; p = parent[r]) r = p;
+    mol_id[i] = (int)rank[r] + 1;
+    if (r != i) continue;
+    const int* ci = comp + (int64_t)i * nt;
+    unsigned h = (unsigned)sp_hash(ci, nt) & mask;
+    for (;;) {
+      const int old = atomicCAS(&table[h].x, -1, i);
+      bool same = old == -1;
+      if (!same) {
+        const int* co = comp + (int64_t)old * nt;
+        same = true;
+        for (int t = 0; t < nt; ++t) same &= co[t] == ci[t];
+      }
+      if (same) {
+        atomicAdd(&table[h].y, 1);
+        break;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+__global__ void k_sp_collect(unsigned size, const int2* __restrict__ table, const int* __restrict__ comp, int nt,
+                             int* __restrict__ out_comp, long long* __restrict__ out_cnt, unsigned* nsp) {
+  for (unsigned h = blockIdx.x * blockDim.x + threadIdx.x; h < size; h += gridDim.x * blockDim.x) {
+    const int2 v = table[h];
+    if (v.x < 0) continue;
+    const unsigned k = atomicAdd(nsp, 1u);
+    for (int t = 0; t < nt; ++t) out_comp[(int64_t)k * nt + t] = comp[(int64_t)v.x * nt + t];
+    out_cnt[k] = v.y;
+  }
+}
+
+// ================================================================ NEXT-2 QEq
+// PAPER.md:204-208 (§3.3 "QEq"): H_ii = eta_i, H_ij = C Tap(r) (r^3 +
+// gamma_ij^-3)^(-1/3) over the half list ("only unique, non-zero elements ...
+// computed", from the neighbour list, rows placed by an atom-based prefix
+// sum), then "a diagonally preconditioned parallel CG solver" run on the two
+// systems H s = -chi and H t = -1 concurrently ("combines the sparse matrix
+// multiplication and orthogonalization computations for the two linear
+// systems"): one pass over H per iteration serves both right-hand sides.
+//
+// GPU layout (sorted atom order): every unique H_ij is computed once, from
+// the half list, and stored twice — in row i's upper segment (the half-list
+// row, in its order) and in row j's lower segment — so that the SpMV is a
+// pure gather (warp per row, no atomics, fixed summation order).  The lower
+// segments are filled through per-row atomic cursors and then sorted by
+// column, which makes every SpMV, and so the whole solve, deterministic.
+// Vectors of the two systems are interleaved (double2: s-system, t-system).
+constexpr int QEQ_THREADS = 256;
+constexpr int QEQ_GRID = 148 * 4;     // fixed grid: the reduction shape never changes
+constexpr int QEQ_SORT_CAP = 768;     // lower segment entries sorted in shared memory per warp
+constexpr int QEQ_SORT_THREADS = 128;
+
+struct QEqState {
+  double rz[2][2];      // [parity][system]
+  double bb[2];         // ||b||^2
+  double rr[2];         // ||r||^2 after the last update
+  int active[2][2];     // [parity][system]
+  int iters[2];
+};
+
+__device__ __forceinline__ double qeq_H(double r, double g3, double C, double invR) {
+  const double x = r * invR;
+  const double x2 = x * x;
+  const double tap = fma(x2 * x2, fma(x, fma(x, fma(x, 20.0, -70.0), 84.0), -35.0), 1.0);
+  return C * tap * rcbrt(fma(r * r, r, g3));
+}
+
+// mode 0: lower-segment counts lcnt[j] (+1 per half entry with partner j);
+// mode 1: H values into the upper (row s, position off[s] + e) and lower
+// (row j, off[j] + len[j] + cursor) segments
+__global__ void __launch_bounds__(NBR_THREADS) k_qeq_hbuild(Grid g, const int* __restrict__ cell_start,
+    const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
+    const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap, int mode,
+    int* __restrict__ lcnt, const long long* __restrict__ off, int* __restrict__ cur, int* __restrict__ hcol,
+    double* __restrict__ hval) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ WinSmem W;
+  int* slot_j = reinterpret_cast<int*>(dyn);
+  unsigned char* slot_k = reinterpret_cast<unsigned char*>(slot_j + window_cap);
+  const int nW = build_window(W, blockIdx.x, g, cell_start);
+  if (nW > window_cap) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int k = warp; k < c_win.nwu; k += nwarp)
+    for (int a = lane; a < W.cnt[k]; a += 32) {
+      slot_j[W.slot[k] + a] = W.start[k] + a;
+      slot_k[W.slot[k] + a] = (unsigned char)k;
+    }
+  __syncthreads();
+  const double C = prm->C, invR = prm->invR;
+  const int nt = prm->nt;
+  for (int r = warp;; r += nwarp) {
+    int h, si;
+    if (!row_of(W, r, h, si)) break;
+    const int s = slot_j[si];
+    const int len = nbr_len[s];
+    const double4 xi = spos[s];
+    const int ti = stype[s];
+    for (int e = lane; e < len; e += 32) {
+      const int t = nbr[(int64_t)s * row_cap + e];
+      const int j = slot_j[t];
+      if (mode == 0) {
+        atomicAdd(lcnt + j, 1);
+        continue;
+      }
+      const double4 xj = spos[j];
+      const double4 sh = W.shift[slot_k[t]];
+      const double dx = xj.x + sh.x - xi.x, dy = xj.y + sh.y - xi.y, dz = xj.z + sh.z - xi.z;
+      const double rr = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
+      const double v = qeq_H(rr, prm->nb[ti * nt + stype[j]].g3, C, invR);
+      const long long u = off[s] + e;
+      hcol[u] = j;
+      hval[u] = v;
+      const long long l = off[j] + nbr_len[j] + atomicAdd(cur + j, 1);
+      hcol[l] = s;
+      hval[l] = v;
+    }
+  }
+}
+
+__global__ void k_qeq_rowlen(int n, const int* __restrict__ len, int* __restrict__ deg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) deg[i] += len[i];
+}
+
+// sort every lower segment by column (warp per row, rank sort in shared memory)
+__global__ void __launch_bounds__(QEQ_SORT_THREADS) k_qeq_sortlow(int n, const long long* __restrict__ off,
+                                                            const int* __restrict__ nbr_len, int* __restrict__ hcol,
+                                                            double* __restrict__ hval, Status* st) {
+  __shared__ int sc[QEQ_SORT_THREADS / 32][QEQ_SORT_CAP];
+  __shared__ double sv[QEQ_SORT_THREADS / 32][QEQ_SORT_CAP];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nw = gridDim.x * (QEQ_SORT_THREADS / 32);
+  for (int row = blockIdx.x * (QEQ_SORT_THREADS / 32) + w; row < n; row += nw) {
+    const long long a = off[row] + nbr_len[row], b = off[row + 1];
+    const int m = (int)(b - a);
+    if (m <= 1) continue;
+    if (m > QEQ_SORT_CAP) {   // left in fill order: correct, not reproducible
+      if (lane == 0) set_flag(st, ST_QEQ_UNSORTED);
+      continue;
+    }
+    for (int k = lane; k < m; k += 32) {
+      sc[w][k] = hcol[a + k];
+      sv[w][k] = hval[a + k];
+    }
+    __syncwarp();
+    for (int k = lane; k < m; k += 32) {
+      const int key = sc[w][k];
+      int rank = 0;
+      for (int q = 0; q < m; ++q) rank += sc[w][q] < key;   // columns of a row are distinct
+      hcol[a + rank] = key;
+      hval[a + rank] = sv[w][k];
+    }
+    __syncwarp();
+  }
+}
+
+// fixed-shape block sum of K doubles per thread -> part[blockIdx.x * K + k]
+template <int K>
+__device__ __forceinline__ void qeq_block_sum(double (&v)[K], double* __restrict__ part) {
+  __shared__ double red[K][QEQ_THREADS / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    if (lane == 0) red[k][w] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double t = 0.0;
+    for (int q = 0; q < QEQ_THREADS / 32; ++q) t += red[threadIdx.x][q];
+    part[blockIdx.x * K + threadIdx.x] = t;
+  }
+}
+
+// every block reduces the QEQ_GRID partials of K values in the same fixed
+// order (so all blocks see identical scalars): out[k] = sum_b part[b*K + k]
+template <int K>
+__device__ __forceinline__ void qeq_total(const double* __restrict__ part, double (&out)[K]) {
+  __shared__ double red[K][QEQ_THREADS / 32];
+  __shared__ double tot[K];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < QEQ_GRID; b += QEQ_THREADS) v += part[b * K + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[k][w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double t = 0.0;
+    for (int q = 0; q < QEQ_THREADS / 32; ++q) t += red[threadIdx.x][q];
+    tot[threadIdx.x] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = tot[k];
+  __syncthreads();
+}
+
+struct QEqType {
+  double eta[NT_MAX], chi[NT_MAX];
+};
+
+// y = H x for both systems (warp per row, fixed order); with part, also the
+// partial dots x . y of both systems
+__global__ void __launch_bounds__(QEQ_THREADS) k_qeq_spmv(int n, const long long* __restrict__ off,
+    const int* __restrict__ hcol, const double* __restrict__ hval, const int* __restrict__ stype, QEqType ty,
+    const double2* __restrict__ x, double2* __restrict__ y, double* __restrict__ part) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nw = gridDim.x * (QEQ_THREADS / 32);
+  double d[2] = {0.0, 0.0};
+  for (int row = blockIdx.x * (QEQ_THREADS / 32) + w; row < n; row += nw) {
+    const long long a = off[row], b = off[row + 1];
+    double a0 = 0.0, a1 = 0.0;
+    for (long long e = a + lane; e < b; e += 32) {
+      const double v = hval[e];
+      const double2 xc = x[hcol[e]];
+      a0 = fma(v, xc.x, a0);
+      a1 = fma(v, xc.y, a1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if (lane == 0) {
+      const double2 xr = x[row];
+      const double et = ty.eta[stype[row]];
+      const double2 yr = make_double2(fma(et, xr.x, a0), fma(et, xr.y, a1));
+      y[row] = yr;
+      d[0] = fma(xr.x, yr.x, d[0]);
+      d[1] = fma(xr.y, yr.y, d[1]);
+    }
+  }
+  if (part) qeq_block_sum<2>(d, part);
+}
+
+// start: x from the guesses (input order -> sorted), done by k_qeq_gather;
+// r = b - Ax, z = r / eta, p = z; partials {r.z (2), r.r (2), b.b (2)}
+__global__ void __launch_bounds__(QEQ_THREADS) k_qeq_gather(int n, const int* __restrict__ perm,
+    const double* __restrict__ s0, const double* __restrict__ t0, double2* __restrict__ x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int o = perm[i];
+    x[i] = make_double2(s0[o], t0[o]);
+  }
+}
+
+__global__ void __launch_bounds__(QEQ_THREADS) k_qeq_start(int n, const int* __restrict__ stype, QEqType ty,
+    const double2* __restrict__ Ax, double2* __restrict__ r, double2* __restrict__ z, double2* __restrict__ p,
+    double* __restrict__ part) {
+  double v[6] = {0, 0, 0, 0, 0, 0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int t = stype[i];
+    const double b0 = -ty.chi[t], b1 = -1.0, ie = 1.0 / ty.eta[t];
+    const double2 ax = Ax[i];
+    const double2 rr = make_double2(b0 - ax.x, b1 - ax.y);
+    const double2 zz = make_double2(rr.x * ie, rr.y * ie);
+    r[i] = rr;
+    z[i] = zz;
+    p[i] = zz;
+    v[0] = fma(rr.x, zz.x, v[0]);
+    v[1] = fma(rr.y, zz.y, v[1]);
+    v[2] = fma(rr.x, rr.x, v[2]);
+    v[3] = fma(rr.y, rr.y, v[3]);
+    v[4] = fma(b0, b0, v[4]);
+    v[5] = fma(b1, b1, v[5]);
+  }
+  qeq_block_sum<6>(v, part);
+}
+
+// one block: the start scalars
+__global__ void __launch_bounds__(QEQ_THREADS) k_qeq_start_state(const double* __restrict__ part, double tol,
+                                                                 int maxiter, QEqState* stt) {
+  double t[6];
+  qeq_total<6>(part, t);
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < 2; ++c) {
+      stt->rz[0][c] = t[c];
+      stt->rr[c] = t[2 + c];
+      stt->bb[c] = t[4 + c];
+      stt->active[0][c] = maxiter > 0 && t[2 + c] > tol * tol * t[4 + c];
+      stt->iters[c] = 0;
+    }
+  }
+}
+
+// alpha = r.z / p.Ap (from the spmv partials) for the active systems;
+// x += alpha p, r -= alpha Ap, z = r / eta; partials {r.z (2), r.r (2)}
+__global__ void __launch_bounds__(QEQ_THREADS) k_qeq_update(int n, const int* __restrict__ stype, QEqType ty,
+    const double* __restrict__ part_pap, const QEqState* __restrict__ stt, int par, double2* __restrict__ x,
+    double2* __restrict__ r, double2* __restrict__ z, const double2* __restrict__ p, const double2* __restrict__ Ap,
+    double* __restrict__ part) {
+  double pap[2];
+  qeq_total<2>(part_pap, pap);
+  const double al0 = stt->active[par][0] ? stt->rz[par][0] / pap[0] : 0.0;
+  const double al1 = stt->active[par][1] ? stt->rz[par][1] / pap[1] : 0.0;
+  double v[4] = {0, 0, 0, 0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double ie = 1.0 / ty.eta[stype[i]];
+    const double2 pi = p[i], api = Ap[i];
+    double2 xi = x[i], ri = r[i];
+    xi.x = fma(al0, pi.x, xi.x);
+    xi.y = fma(al1, pi.y, xi.y);
+    ri.x = fma(-al0, api.x, ri.x);
+    ri.y = fma(-al1, api.y, ri.y);
+    const double2 zi = make_double2(ri.x * ie, ri.y * ie);
+    x[i] = xi;
+    r[i] = ri;
+    z[i] = zi;
+    v[0] = fma(ri.x, zi.x, v[0]);
+    v[1] = fma(ri.y, zi.y, v[1]);
+    v[2] = fma(ri.x, ri.x, v[2]);
+    v[3] = fma(ri.y, ri.y, v[3]);
+  }
+  qeq_block_sum<4>(v, part);
+}
+
+// beta = r.z (new) / r.z (old); p = z + beta p; block 0 advances the state
+// (iteration counts, convergence ||r|| <= tol ||b||, the next r.z)
+__global__ void __launch_bounds__(QEQ_THREADS) k_qeq_direction(int n, const double* __restrict__ part_rz,
+    QEqState* stt, int par, double tol, int maxiter, const double2* __restrict__ z, double2* __restrict__ p) {
+  double t[4];
+  qeq_total<4>(part_rz, t);
+  const int a0 = stt->active[par][0], a1 = stt->active[par][1];
+  const double be0 = a0 ? t[0] / stt->rz[par][0] : 0.0;
+  const double be1 = a1 ? t[1] / stt->rz[par][1] : 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double2 zi = z[i];
+    double2 pi = p[i];
+    pi.x = fma(be0, pi.x, zi.x);
+    pi.y = fma(be1, pi.y, zi.y);
+    p[i] = pi;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int act[2] = {a0, a1};
+    for (int c = 0; c < 2; ++c) {   // (parity par^1 is read only by the next iteration's kernels)
+      stt->active[par ^ 1][c] = 0;
+      if (!act[c]) continue;
+      stt->rz[par ^ 1][c] = t[c];
+      stt->rr[c] = t[2 + c];
+      stt->iters[c] += 1;
+      stt->active[par ^ 1][c] = stt->iters[c] < maxiter && t[2 + c] > tol * tol * stt->bb[c];
+    }
+  }
+}
+
+// s, t back to input order; partials {sum s, sum t}
+__global__ void __launch_bounds__(QEQ_THREADS) k_qeq_scatter(int n, const int* __restrict__ perm,
+    const double2* __restrict__ x, double* __restrict__ s, double* __restrict__ t, double* __restrict__ part) {
+  double v[2] = {0.0, 0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double2 xi = x[i];
+    const int o = perm[i];
+    s[o] = xi.x;
+    t[o] = xi.y;
+    v[0] += xi.x;
+    v[1] += xi.y;
+  }
+  qeq_block_sum<2>(v, part);
+}
+
+// q = s - (sum s / sum t) t (input order)
+__global__ void __launch_bounds__(QEQ_THREADS) k_qeq_charges(int n, const double* __restrict__ part,
+    const double* __restrict__ s, const double* __restrict__ t, double* __restrict__ q) {
+  double tot[2];
+  qeq_total<2>(part, tot);
+  const double mu = tot[0] / tot[1];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) q[i] = fma(-mu, t[i], s[i]);
+}
+
 }  // namespace rx

@@ -407,6 +407,11 @@ struct reax_ctx {
   std::vector<double> prm_key;  // raw reax_params + cutoffs of the last successful build
   // state
   bool lists_ok = false;
+  uint64_t list_gen = 0;      // reax_build_lists / reax_step calls (QEq H belongs to one list)
+  const void* qeq_scratch = nullptr;
+  uint64_t qeq_gen = 0;
+  int64_t qeq_P = -1;
+  bool qeq_unsorted = false;
   bool bonds_ok = false;
   const double* last_pos = nullptr;
   const int* last_type = nullptr;
@@ -558,8 +563,12 @@ reax_status read_status(reax_ctx* c, cudaStream_t s, bool sync) {
 // the status block read back into h_st (stream synchronised): OK, or the
 // error it latched (the device copy is cleared for the next call)
 reax_status interpret_status(reax_ctx* c, cudaStream_t s) {
-  int f = c->h_st->flags;
-  if (f == 0) return REAX_OK;
+  int f = c->h_st->flags & ~ST_QEQ_UNSORTED;   // informational: a QEq row left in fill order
+  if (c->h_st->flags & ST_QEQ_UNSORTED) c->qeq_unsorted = true;
+  if (f == 0) {
+    if (c->h_st->flags) cudaMemsetAsync(c->w.st, 0, sizeof(Status), s);
+    return REAX_OK;
+  }
   if (f & (ST_ROW_OVF | ST_CAND_OVF | ST_BOND_OVF | ST_WIN_OVF)) {
     c->need = c->cap;
     if (f & ST_ROW_OVF) c->need.row_cap = std::max(c->cap.row_cap, (c->h_st->max_row + 32) / 32 * 32);
@@ -726,6 +735,7 @@ reax_status prep_build(reax_ctx* c, int64_t n, const double* pos, const int* typ
   if (r != REAX_OK) return r;
   c->cut = *cut;
   c->lists_ok = c->bonds_ok = false;
+  ++c->list_gen;
   return REAX_OK;
 }
 
@@ -1023,6 +1033,304 @@ reax_status do_ilist_lists(reax_ctx* c, const reax_ilist_params* p, int64_t* ang
   return read_status(c, s, true);
 }
 
+// NEXT-4: species analysis of the current corrected bond orders
+// (reading 32).  Scratch layout (caller-owned):
+struct SpLayout {
+  size_t parent, isroot, comp, out_comp, rank, out_cnt, table, nsp, total;
+  unsigned tsize;
+};
+SpLayout sp_layout(int64_t n, int nt) {
+  SpLayout L;
+  const size_t N = (size_t)std::max<int64_t>(n, 1);
+  unsigned t = 1024;
+  while ((size_t)t < 2 * N) t <<= 1;
+  L.tsize = t;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { const size_t at = o; o = (o + bytes + 255) & ~(size_t)255; return at; };
+  L.parent = take(4 * N);
+  L.isroot = take(4 * N);
+  L.comp = take(4 * N * nt);
+  L.out_comp = take(4 * N * nt);
+  L.rank = take(8 * (N + 1));
+  L.out_cnt = take(8 * N);
+  L.table = take(8 * (size_t)t);
+  L.nsp = take(16);
+  L.total = o;
+  return L;
+}
+
+reax_status do_species(reax_ctx* c, const double* thresh, void* scratch, size_t scratch_bytes, int32_t* mol_id,
+                       int64_t* n_molecules, int32_t* sp_comp, int64_t* sp_count, int64_t sp_cap, int64_t* n_species,
+                       cudaStream_t s) {
+  if (!c || !n_molecules || !n_species) return REAX_ERR_ARG;
+  if (!c->bound || !c->lists_ok || !c->bonds_ok || !c->prm_valid) return REAX_ERR_STATE;
+  const int nt = c->h_prm->nt;
+  const int N = (int)c->n;
+  if (sp_cap < 0 || (sp_cap > 0 && (!sp_comp || !sp_count)) || (N > 0 && !mol_id)) return REAX_ERR_ARG;
+  SpThr thr;
+  for (int t = 0; t < nt * nt; ++t) {
+    const double v = thresh ? thresh[t] : 0.3;
+    if (!std::isfinite(v) || (thresh && v != thresh[(t % nt) * nt + t / nt])) return REAX_ERR_PARAM;
+    thr.t[t] = v;
+  }
+  *n_molecules = 0;
+  *n_species = 0;
+  if (N == 0) return REAX_OK;
+  const SpLayout L = sp_layout(N, nt);
+  if (!scratch || scratch_bytes < L.total) return REAX_ERR_CAPACITY;
+  if (((uintptr_t)scratch) % 256 != 0) return REAX_ERR_ARG;
+  char* b = (char*)scratch;
+  int* parent = (int*)(b + L.parent);
+  int* isroot = (int*)(b + L.isroot);
+  int* comp = (int*)(b + L.comp);
+  int* out_comp = (int*)(b + L.out_comp);
+  long long* rank = (long long*)(b + L.rank);
+  long long* out_cnt = (long long*)(b + L.out_cnt);
+  int2* table = (int2*)(b + L.table);
+  unsigned* nsp = (unsigned*)(b + L.nsp);
+  WS& w = c->w;
+  {
+    Timer t(c, 7, s);
+    if (cudaMemsetAsync(comp, 0, 4 * (size_t)N * nt, s) != cudaSuccess ||
+        cudaMemsetAsync(table, 0xff, 8 * (size_t)L.tsize, s) != cudaSuccess ||   // rep = -1 (and count -1, reset below)
+        cudaMemsetAsync(nsp, 0, 16, s) != cudaSuccess)
+      return fail_cuda(cudaGetLastError());
+    k_sp_init<<<nblk(N, TPB), TPB, 0, s>>>(N, parent);
+    LAUNCH(c);
+    k_sp_union<<<148 * 8, TPB, 0, s>>>(w.brow, N, w.bown, w.bcol, w.bkey, w.perm, w.stype, w.bo, nt, thr, parent);
+    LAUNCH(c);
+    k_sp_count<<<nblk(N, TPB), TPB, 0, s>>>(N, w.perm, w.stype, nt, parent, isroot, comp);
+    LAUNCH(c);
+    if (scan<int, long long>(c, isroot, N, rank, s) != cudaSuccess) return fail_cuda(cudaGetLastError());
+    k_sp_label<<<nblk(N, TPB), TPB, 0, s>>>(N, parent, rank, mol_id, comp, nt, table, L.tsize - 1);
+    LAUNCH(c);
+    k_sp_collect<<<nblk(L.tsize, TPB), TPB, 0, s>>>(L.tsize, table, comp, nt, out_comp, out_cnt, nsp);
+    LAUNCH(c);
+  }
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  long long M = 0;
+  unsigned S = 0;
+  if (cudaMemcpyAsync(&M, rank + N, sizeof(long long), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(&S, nsp, sizeof(unsigned), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return fail_cuda(cudaGetLastError());
+  std::vector<int> hc((size_t)S * nt);
+  std::vector<long long> hn(S);
+  if (S > 0 && (cudaMemcpyAsync(hc.data(), out_comp, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaMemcpyAsync(hn.data(), out_cnt, sizeof(long long) * S, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess))
+    return fail_cuda(cudaGetLastError());
+  // the table's slot order is arbitrary: species sorted by composition
+  std::vector<unsigned> ord(S);
+  for (unsigned k = 0; k < S; ++k) ord[k] = k;
+  std::sort(ord.begin(), ord.end(), [&](unsigned x, unsigned y) {
+    return std::lexicographical_compare(hc.begin() + (size_t)x * nt, hc.begin() + (size_t)(x + 1) * nt,
+                                        hc.begin() + (size_t)y * nt, hc.begin() + (size_t)(y + 1) * nt);
+  });
+  for (unsigned k = 0; k < S && (int64_t)k < sp_cap; ++k) {
+    for (int t = 0; t < nt; ++t) sp_comp[(size_t)k * nt + t] = hc[(size_t)ord[k] * nt + t];
+    sp_count[k] = hn[ord[k]] + 1;   // the count word started at -1 (0xffffffff)
+  }
+  *n_molecules = M;
+  *n_species = S;
+  if ((int64_t)S > sp_cap) return REAX_ERR_CAPACITY;
+  return read_status(c, s, true);
+}
+
+// NEXT-2: QEq (reading 33).  Caller-owned
+// scratch (sorted order): row offsets, lower-segment counts and cursors, the
+// doubly stored H (column, value), the interleaved CG vectors, partials.
+struct QLayout {
+  size_t off, lcnt, cur, hcol, hval, x, r, z, p, Ap, part, part2, stt, total;
+};
+QLayout qeq_layout(int64_t n, int64_t P) {
+  QLayout L;
+  const size_t N = (size_t)std::max<int64_t>(n, 1), E = (size_t)std::max<int64_t>(2 * P, 1);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { const size_t at = o; o = (o + bytes + 255) & ~(size_t)255; return at; };
+  L.off = take(8 * (N + 1));
+  L.lcnt = take(4 * N);
+  L.cur = take(4 * N);
+  L.hcol = take(4 * E);
+  L.hval = take(8 * E);
+  L.x = take(16 * N);
+  L.r = take(16 * N);
+  L.z = take(16 * N);
+  L.p = take(16 * N);
+  L.Ap = take(16 * N);
+  L.part = take(8 * 6 * QEQ_GRID);
+  L.part2 = take(8 * 6 * QEQ_GRID);
+  L.stt = take(sizeof(QEqState));
+  L.total = o;
+  return L;
+}
+
+reax_status half_pairs(reax_ctx* c, cudaStream_t s, int64_t* P) {
+  long long p = 0;
+  if (c->n > 0) {
+    if (scan<int, long long>(c, c->w.nbr_len, c->n, c->w.exp_off, s) != cudaSuccess ||
+        cudaMemcpyAsync(&p, c->w.exp_off + c->n, sizeof(long long), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return fail_cuda(cudaGetLastError());
+  }
+  *P = p;
+  return REAX_OK;
+}
+
+reax_status do_qeq_build(reax_ctx* c, void* scratch, size_t bytes, cudaStream_t s) {
+  if (!c) return REAX_ERR_ARG;
+  if (!c->bound || !c->lists_ok || !c->prm_valid) return REAX_ERR_STATE;
+  int64_t P = 0;
+  reax_status r = half_pairs(c, s, &P);
+  if (r != REAX_OK) return r;
+  const QLayout L = qeq_layout(c->n, P);
+  if (!scratch || bytes < L.total) return REAX_ERR_CAPACITY;
+  if (((uintptr_t)scratch) % 256 != 0) return REAX_ERR_ARG;
+  c->qeq_scratch = nullptr;
+  const int N = (int)c->n;
+  if (N > 0) {
+    char* b = (char*)scratch;
+    long long* off = (long long*)(b + L.off);
+    int* lcnt = (int*)(b + L.lcnt);
+    int* cur = (int*)(b + L.cur);
+    WS& w = c->w;
+    Timer t(c, 8, s);
+    const size_t sm = (size_t)c->cap.window_cap * (sizeof(int) + 1) + 64;
+    if (ensure_smem(k_qeq_hbuild, sm) != cudaSuccess) return fail_cuda(cudaGetLastError());
+    if (cudaMemsetAsync(lcnt, 0, 4 * (size_t)N, s) != cudaSuccess ||
+        cudaMemsetAsync(cur, 0, 4 * (size_t)N, s) != cudaSuccess)
+      return fail_cuda(cudaGetLastError());
+    k_qeq_hbuild<<<c->g.nblock, NBR_THREADS, sm, s>>>(c->g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len,
+                                                      c->cap.row_cap, c->cap.window_cap, 0, lcnt, nullptr, nullptr,
+                                                      nullptr, nullptr);
+    LAUNCH(c);
+    k_qeq_rowlen<<<nblk(N, TPB), TPB, 0, s>>>(N, w.nbr_len, lcnt);   // lcnt += len (row degree)
+    LAUNCH(c);
+    if (scan<int, long long>(c, lcnt, N, off, s) != cudaSuccess) return fail_cuda(cudaGetLastError());
+    k_qeq_hbuild<<<c->g.nblock, NBR_THREADS, sm, s>>>(c->g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len,
+                                                      c->cap.row_cap, c->cap.window_cap, 1, nullptr, off, cur,
+                                                      (int*)(b + L.hcol), (double*)(b + L.hval));
+    LAUNCH(c);
+    k_qeq_sortlow<<<QEQ_GRID * 2, QEQ_SORT_THREADS, 0, s>>>(N, off, w.nbr_len, (int*)(b + L.hcol), (double*)(b + L.hval), w.st);
+    LAUNCH(c);
+  }
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  r = read_status(c, s, true);
+  if (r != REAX_OK) return r;
+  c->qeq_scratch = scratch;
+  c->qeq_gen = c->list_gen;
+  c->qeq_P = P;
+  return REAX_OK;
+}
+
+reax_status qeq_types(reax_ctx* c, const double* chi, const double* eta, QEqType& ty) {
+  const int nt = c->h_prm->nt;
+  if (!eta) return REAX_ERR_ARG;
+  memset(&ty, 0, sizeof(ty));
+  for (int t = 0; t < nt; ++t) {
+    if (!(std::isfinite(eta[t]) && eta[t] > 0.0)) return REAX_ERR_PARAM;
+    if (chi && !std::isfinite(chi[t])) return REAX_ERR_PARAM;
+    ty.eta[t] = eta[t];
+    ty.chi[t] = chi ? chi[t] : 0.0;
+  }
+  return REAX_OK;
+}
+
+reax_status qeq_ready(reax_ctx* c, const void* scratch, size_t bytes, QLayout& L) {
+  if (!c->bound || !c->lists_ok || !c->prm_valid) return REAX_ERR_STATE;
+  if (!scratch || scratch != c->qeq_scratch || c->qeq_gen != c->list_gen) return REAX_ERR_STATE;
+  L = qeq_layout(c->n, c->qeq_P);
+  if (bytes < L.total) return REAX_ERR_CAPACITY;
+  return REAX_OK;
+}
+
+reax_status do_qeq_matvec(reax_ctx* c, const double* eta, void* scratch, size_t bytes, const double* x0,
+                          const double* x1, double* y0, double* y1, cudaStream_t s) {
+  if (!c) return REAX_ERR_ARG;
+  QLayout L;
+  reax_status r = qeq_ready(c, scratch, bytes, L);
+  if (r != REAX_OK) return r;
+  QEqType ty;
+  r = qeq_types(c, nullptr, eta, ty);
+  if (r != REAX_OK) return r;
+  const int N = (int)c->n;
+  if (N == 0) return REAX_OK;
+  if (!x0 || !x1 || !y0 || !y1) return REAX_ERR_ARG;
+  char* b = (char*)scratch;
+  double2* x = (double2*)(b + L.x);
+  double2* y = (double2*)(b + L.Ap);
+  WS& w = c->w;
+  k_qeq_gather<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, w.perm, x0, x1, x);
+  k_qeq_spmv<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, (const long long*)(b + L.off), (const int*)(b + L.hcol),
+                                             (const double*)(b + L.hval), w.stype, ty, x, y, nullptr);
+  k_qeq_scatter<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, w.perm, y, y0, y1, (double*)(b + L.part));
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
+  return REAX_OK;
+}
+
+reax_status do_qeq_solve(reax_ctx* c, const double* chi, const double* eta, double tol, int maxiter, void* scratch,
+                         size_t bytes, double* sv, double* tv, double* q, int32_t* iters, cudaStream_t s) {
+  if (!c || !chi || !iters) return REAX_ERR_ARG;
+  QLayout L;
+  reax_status r = qeq_ready(c, scratch, bytes, L);
+  if (r != REAX_OK) return r;
+  QEqType ty;
+  r = qeq_types(c, chi, eta, ty);
+  if (r != REAX_OK) return r;
+  if (!(std::isfinite(tol) && tol >= 0.0) || maxiter < 0) return REAX_ERR_ARG;
+  iters[0] = iters[1] = 0;
+  const int N = (int)c->n;
+  if (N == 0) return REAX_OK;
+  if (!sv || !tv || !q) return REAX_ERR_ARG;
+  char* b = (char*)scratch;
+  const long long* off = (const long long*)(b + L.off);
+  const int* hcol = (const int*)(b + L.hcol);
+  const double* hval = (const double*)(b + L.hval);
+  double2 *x = (double2*)(b + L.x), *rr = (double2*)(b + L.r), *z = (double2*)(b + L.z), *p = (double2*)(b + L.p),
+          *Ap = (double2*)(b + L.Ap);
+  double *part = (double*)(b + L.part), *part2 = (double*)(b + L.part2);
+  QEqState* stt = (QEqState*)(b + L.stt);
+  WS& w = c->w;
+  Timer tm(c, 8, s);
+  k_qeq_gather<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, w.perm, sv, tv, x);
+  k_qeq_spmv<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, off, hcol, hval, w.stype, ty, x, Ap, nullptr);
+  k_qeq_start<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, w.stype, ty, Ap, rr, z, p, part);
+  k_qeq_start_state<<<1, QEQ_THREADS, 0, s>>>(part, tol, maxiter, stt);
+  int act[2] = {1, 1};
+  for (int it = 0; it < maxiter; ++it) {
+    const int par = it & 1;
+    if (cudaMemcpyAsync(act, &stt->active[par][0], sizeof(act), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return fail_cuda(cudaGetLastError());
+    if (!act[0] && !act[1]) break;
+    k_qeq_spmv<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, off, hcol, hval, w.stype, ty, p, Ap, part);
+    k_qeq_update<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, w.stype, ty, part, stt, par, x, rr, z, p, Ap, part2);
+    k_qeq_direction<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, part2, stt, par, tol, maxiter, z, p);
+    c->launches_cur += 3;
+  }
+  k_qeq_scatter<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, w.perm, x, sv, tv, part);
+  k_qeq_charges<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, part, sv, tv, q);
+  if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
+  int it2[2] = {0, 0};
+  if (cudaMemcpyAsync(it2, stt->iters, sizeof(it2), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(act, &stt->active[maxiter & 1][0], sizeof(act), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return fail_cuda(cudaGetLastError());
+  iters[0] = it2[0];
+  iters[1] = it2[1];
+  r = read_status(c, s, true);
+  if (r != REAX_OK) return r;
+  // not converged within maxiter (iterations stopped by the cap)
+  double rr_h[2], bb_h[2];
+  if (cudaMemcpy(rr_h, stt->rr, sizeof(rr_h), cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(bb_h, stt->bb, sizeof(bb_h), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail_cuda(cudaGetLastError());
+  for (int k = 0; k < 2; ++k)
+    if (!(rr_h[k] <= tol * tol * bb_h[k])) return REAX_ERR_CONVERGENCE;
+  return REAX_OK;
+}
+
 }  // namespace
 
 // ==================================================================== ABI
@@ -1059,6 +1367,7 @@ const char* reax_status_str(reax_status s) {
     case REAX_ERR_CUDA: return "CUDA error";
     case REAX_ERR_STATE: return "invalid call sequence or binding";
     case REAX_ERR_RANGE: return "force contribution outside the fixed-point accumulator range (>= 65536 kcal/mol/A)";
+    case REAX_ERR_CONVERGENCE: return "QEq not converged within maxiter";
   }
   return "unknown";
 }
@@ -1396,6 +1705,44 @@ reax_status reax_selftest_math(reax_ctx* ctx, int64_t n, const double* x, double
   if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
   if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
   return REAX_OK;
+}
+
+reax_status reax_qeq_bytes(reax_ctx* ctx, size_t* bytes, void* stream) {
+  if (!ctx || !bytes) return REAX_ERR_ARG;
+  if (!ctx->bound || !ctx->lists_ok) return REAX_ERR_STATE;
+  int64_t P = 0;
+  reax_status r = half_pairs(ctx, (cudaStream_t)stream, &P);
+  if (r != REAX_OK) return r;
+  *bytes = qeq_layout(ctx->n, P).total;
+  return REAX_OK;
+}
+
+reax_status reax_qeq_build(reax_ctx* ctx, void* scratch, size_t scratch_bytes, void* stream) {
+  return do_qeq_build(ctx, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+reax_status reax_qeq_matvec(reax_ctx* ctx, const double* eta, void* scratch, size_t scratch_bytes, const double* x_s,
+                            const double* x_t, double* y_s, double* y_t, void* stream) {
+  return do_qeq_matvec(ctx, eta, scratch, scratch_bytes, x_s, x_t, y_s, y_t, (cudaStream_t)stream);
+}
+
+reax_status reax_qeq_solve(reax_ctx* ctx, const double* chi, const double* eta, double tol, int32_t maxiter,
+                           void* scratch, size_t scratch_bytes, double* s, double* t, double* q, int32_t* iters,
+                           void* stream) {
+  return do_qeq_solve(ctx, chi, eta, tol, maxiter, scratch, scratch_bytes, s, t, q, iters, (cudaStream_t)stream);
+}
+
+reax_status reax_species_bytes(int64_t n, int32_t ntypes, size_t* bytes) {
+  if (!bytes || n < 0 || ntypes < 1 || ntypes > REAX_MAX_TYPES) return REAX_ERR_ARG;
+  *bytes = sp_layout(n, ntypes).total;
+  return REAX_OK;
+}
+
+reax_status reax_species(reax_ctx* ctx, const double* bo_threshold, void* scratch, size_t scratch_bytes,
+                         int32_t* mol_id, int64_t* n_molecules, int32_t* species_comp, int64_t* species_count,
+                         int64_t species_cap, int64_t* n_species, void* stream) {
+  return do_species(ctx, bo_threshold, scratch, scratch_bytes, mol_id, n_molecules, species_comp, species_count,
+                    species_cap, n_species, (cudaStream_t)stream);
 }
 
 reax_status reax_interaction_counts(reax_ctx* ctx, const reax_ilist_params* params, int64_t* n_angles,

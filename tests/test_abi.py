@@ -36,7 +36,7 @@ def test_library_is_sm100a():
 
 
 def test_status_strings():
-    for code in range(10):
+    for code in range(11):
         assert len(rx.status_str(code)) > 0
 
 
