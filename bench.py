@@ -245,6 +245,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     ap.add_argument("--no-c1", action="store_true", help="skip the supplementary c1 measurement")
+    ap.add_argument("--no-next", action="store_true", help="skip the next_rows measurements (profiling runs)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -397,10 +398,12 @@ def main():
                "api": "reax_step_host (pinned host buffers in/out, copies inside the timed region)"}
     clocks = sample_clocks_stop(clk)
 
+    bond_energy = ilists = species = qeq = {"skipped": "--no-next"}
     # NEXT-1 (outside `value`): reax_bond_energy on the step's bond list, K
     # calls bracketed by events on the launching stream
-    bond_energy = None
     try:
+        if args.no_next:
+            raise StopIteration
         bp = gen.make_bond_params()
         Fb = torch.empty((n, 3), dtype=torch.float64, device=dev)
         Eb = torch.empty(1, dtype=torch.float64, device=dev)
@@ -418,12 +421,15 @@ def main():
         b_ms = sum(a.elapsed_time(b) for a, b in bev) / args.steps
         bond_energy = {"row": "NEXT-1 bond energy + forces (reax_bond_energy), timed separately", "ms_per_call": b_ms,
                        "bond_entries": B, "bonds_per_s": (B / 2) / (b_ms * 1e-3), "launches_per_call": 3}
+    except StopIteration:
+        pass
     except Exception as ex:   # reported, never silently dropped
         bond_energy = {"error": str(ex)}
     # NEXT-3 (outside `value`): reax_interaction_lists (counts + lists, both
     # synchronous), K calls bracketed by events
-    ilists = None
     try:
+        if args.no_next:
+            raise StopIteration
         for _ in range(2):
             ctx.interaction_lists()
         torch.cuda.synchronize()
@@ -439,11 +445,14 @@ def main():
         ilists = {"row": "NEXT-3 3-body + H-bond lists (reax_interaction_counts + reax_interaction_lists), timed separately",
                   "ms_per_call": sum(a.elapsed_time(b) for a, b in iev) / args.steps,
                   "angle_entries": sizes[0], "hbond_entries": sizes[1]}
+    except StopIteration:
+        pass
     except Exception as ex:   # reported, never silently dropped
         ilists = {"error": str(ex)}
     # NEXT-4 (outside `value`): reax_species on the step's bond orders
-    species = None
     try:
+        if args.no_next:
+            raise StopIteration
         one_step()
         torch.cuda.synchronize()
         ctx.species()
@@ -457,13 +466,16 @@ def main():
         species = {"row": "NEXT-4 species analysis (reax_species: union-find, renumbering, census; synchronous)",
                    "ms_per_call": sum(a.elapsed_time(b) for a, b in sev) / 3, "molecules": M, "species": len(comp),
                    "bo_threshold": 0.3}
+    except StopIteration:
+        pass
     except Exception as ex:   # reported, never silently dropped
         species = {"error": str(ex)}
     # NEXT-2 (outside `value`): QEq on the step's half list (H build, then the
     # dual Jacobi-PCG at the paper's tolerance 1e-6 from zero guesses), if the
     # doubly stored H fits beside the workspace
-    qeq = None
     try:
+        if args.no_next:
+            raise StopIteration
         qp = gen.make_qeq_params()
         free, _ = torch.cuda.mem_get_info(dev)
         need = 2 * P * 12 + n * 120
@@ -488,6 +500,8 @@ def main():
                    "achieved_gbs_per_iteration": (2 * P * 12 + n * 32) / (sms / max(1, max(it)) * 1e-3) / 1e9}
             ctx._qeq_scratch = None
             torch.cuda.empty_cache()
+    except StopIteration:
+        pass
     except Exception as ex:
         qeq = {"error": str(ex)}
     nb_ms, _ = kms["nonbonded"]
