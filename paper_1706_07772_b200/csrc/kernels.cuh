@@ -529,8 +529,18 @@ __device__ __forceinline__ int warp_find(int incl, int t) {
 // ========================================================= a3-a4 list build
 constexpr int NBR_THREADS = 256;
 
+// per (home sub-cell, forward run): the run's window cells and the
+// block-frame origin of its first cell (staged per CTA: the constant-bank
+// tables would be read with a different index per lane, which serialises)
+struct RunInfo {
+  short ka, kb, wxa, pad;
+  float oy, oz;
+};
+
 struct NbrSmem {
   WinSmem W;
+  RunInfo run[NHOME][MAX_RUNS];
+  int2 ivl[NBR_THREADS / 32][MAX_RUNS + 1];   // per warp: the non-empty intervals in run order
   float rcand2[NTP_MAX];
   int gbase[NHOME + 1];   // first row group of each home sub-cell (groups of NBR_G rows)
   int ncs[NBR_THREADS / 32][8];   // per warp: bond-candidate counters of its group's rows
@@ -587,7 +597,8 @@ struct SlotJK {
 #endif
 constexpr int NBR_G = NBR_GROUP;   // rows sharing one candidate stream
 template <bool BOND, typename SI>
-__device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, const float4* __restrict__ cand, SI sl,
+__device__ __forceinline__ void nbr_group_test(const WinSmem& W, const RunInfo* __restrict__ runs, int2* ivl,
+                                               int Wslots, const float4* __restrict__ cand, SI sl,
                                                const double4* __restrict__ spos, int si0, int nrow, int h,
                                                const Grid& g, const RowTest& rt, uint16_t* __restrict__ nbr,
                                                int row_cap, int* __restrict__ bc, int cand_cap,
@@ -621,11 +632,10 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, con
   const int nrun = c_win.nrun1[h];
   int ia = 0, il = 0;
   if (lane < nrun) {
-    const int ka = c_win.run1_a[h][lane], kb = c_win.run1_b[h][lane];
-    const int wba = c_win.wu[ka];
-    const int wxa = wba % WB - SR;                   // x cell offset (block frame) of the run's first cell
-    const float oy = (float)((wba / WB % WB - SR) * g.h[1]);
-    const float oz = (float)((wba / (WB * WB) - SR) * g.h[2]);
+    const RunInfo ru = runs[lane];
+    const int ka = ru.ka, kb = ru.kb;
+    const int wxa = ru.wxa;                          // x cell offset (block frame) of the run's first cell
+    const float oy = ru.oy, oz = ru.oz;
     float d2min = 1e30f;
 #pragma unroll
     for (int r = 0; r < NBR_G; ++r) {
@@ -670,11 +680,13 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, int Wslots, con
   }
   const int total = __shfl_sync(0xffffffffu, inc, 31);
   const int start_q = inc - il;
-  const unsigned src = __fns(ne, 0, lane + 1);      // lane of the (lane+1)-th set bit
-  const int srcl = src < 32 ? (int)src : 0;
-  const int cstart = __shfl_sync(0xffffffffu, start_q, srcl);
-  const int cshift = __shfl_sync(0xffffffffu, ia - start_q, srcl);
+  // lane k takes the k-th non-empty interval (scatter through shared memory;
+  // __fns is a ~40-instruction software sequence on sm_100a)
+  if (il > 0) ivl[__popc(ne & lt_mask)] = make_int2(start_q, ia - start_q);
+  __syncwarp();
   const int nint = __popc(ne);
+  const int2 iv = ivl[lane < nint ? lane : 0];
+  const int cstart = iv.x, cshift = iv.y;
   for (int p0 = 0; p0 < total; p0 += 32) {
     const int rel = cstart - p0;
     const bool here = lane < nint && rel >= 0 && rel < 32;
@@ -759,6 +771,21 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
   unsigned char* cand_k = reinterpret_cast<unsigned char*>(cand_j + window_cap + 32);
   const int nt = prm->nt;
   for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) S.rcand2[t] = prm->rcand2[t];
+  for (int t = threadIdx.x; t < NHOME * MAX_RUNS; t += blockDim.x) {
+    const int h = t / MAX_RUNS, q = t % MAX_RUNS;
+    if (q < c_win.nrun1[h]) {
+      const int ka = c_win.run1_a[h][q], kb = c_win.run1_b[h][q];
+      const int wba = c_win.wu[ka];
+      RunInfo ru;
+      ru.ka = (short)ka;
+      ru.kb = (short)kb;
+      ru.wxa = (short)(wba % WB - SR);
+      ru.pad = 0;
+      ru.oy = (float)((wba / WB % WB - SR) * g.h[1]);
+      ru.oz = (float)((wba / (WB * WB) - SR) * g.h[2]);
+      S.run[h][q] = ru;
+    }
+  }
   const float rcmax = prm->rcand2_max;
   const RowTest rt = make_rowtest(prm, g);
   int W = build_window(S.W, blk, g, cell_start);
@@ -831,8 +858,8 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
     const int nrow = min(NBR_G, S.W.cnt[kh] - a0);
     const int si0 = S.W.slot[kh] + a0;
     int len[NBR_G], nc[NBR_G];
-    nbr_group_test<true>(S.W, W, cand, sl, spos, si0, nrow, h, g, rt, nbr, row_cap, bc, cand_cap, S.rcand2, nt, rcmax,
-                         S.ncs[threadIdx.x >> 5], len, nc);
+    nbr_group_test<true>(S.W, S.run[h], S.ivl[threadIdx.x >> 5], W, cand, sl, spos, si0, nrow, h, g, rt, nbr, row_cap,
+                         bc, cand_cap, S.rcand2, nt, rcmax, S.ncs[threadIdx.x >> 5], len, nc);
     if (lane < nrow) {
       int l = len[0], c = nc[0];
 #pragma unroll
@@ -2340,7 +2367,7 @@ __global__ void k_sp_collect(unsigned size, const int2* __restrict__ table, cons
 // column, which makes every SpMV, and so the whole solve, deterministic.
 // Vectors of the two systems are interleaved (double2: s-system, t-system).
 constexpr int QEQ_THREADS = 256;
-constexpr int QEQ_GRID = 148 * 4;     // fixed grid: the reduction shape never changes
+constexpr int QEQ_GRID = 148 * 8;     // fixed grid: the reduction shape never changes
 constexpr int QEQ_SORT_CAP = 768;     // lower segment entries sorted in shared memory per warp
 constexpr int QEQ_SORT_THREADS = 128;
 
@@ -2509,11 +2536,25 @@ __global__ void __launch_bounds__(QEQ_THREADS) k_qeq_spmv(int n, const long long
   for (int row = blockIdx.x * (QEQ_THREADS / 32) + w; row < n; row += nw) {
     const long long a = off[row], b = off[row + 1];
     double a0 = 0.0, a1 = 0.0;
-    for (long long e = a + lane; e < b; e += 32) {
-      const double v = hval[e];
-      const double2 xc = x[hcol[e]];
-      a0 = fma(v, xc.x, a0);
-      a1 = fma(v, xc.y, a1);
+    // four entries per lane in flight (the same per-lane order as a plain
+    // stride-32 loop): the column loads, then the dependent gathers
+    for (long long e = a + lane; e < b; e += 128) {
+      double v[4];
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long q = e + 32 * u;
+        v[u] = q < b ? __ldcs(hval + q) : 0.0;
+        c[u] = q < b ? __ldcs(hcol + q) : row;
+      }
+      double2 xc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xc[u] = x[c[u]];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0 = fma(v[u], xc[u].x, a0);
+        a1 = fma(v[u], xc[u].y, a1);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
