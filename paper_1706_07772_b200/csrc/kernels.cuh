@@ -2529,7 +2529,9 @@ struct QEqType {
 // partial dots x . y of both systems
 __global__ void __launch_bounds__(QEQ_THREADS) k_qeq_spmv(int n, const long long* __restrict__ off,
     const int* __restrict__ hcol, const double* __restrict__ hval, const int* __restrict__ stype, QEqType ty,
-    const double2* __restrict__ x, double2* __restrict__ y, double* __restrict__ part) {
+    const double2* __restrict__ x, double2* __restrict__ y, double* __restrict__ part,
+    const QEqState* __restrict__ stt = nullptr, int par = 0) {
+  if (stt && !stt->active[par][0] && !stt->active[par][1]) return;   // both systems converged
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nw = gridDim.x * (QEQ_THREADS / 32);
   double d[2] = {0.0, 0.0};
@@ -2628,6 +2630,7 @@ __global__ void __launch_bounds__(QEQ_THREADS) k_qeq_update(int n, const int* __
     const double* __restrict__ part_pap, const QEqState* __restrict__ stt, int par, double2* __restrict__ x,
     double2* __restrict__ r, double2* __restrict__ z, const double2* __restrict__ p, const double2* __restrict__ Ap,
     double* __restrict__ part) {
+  if (!stt->active[par][0] && !stt->active[par][1]) return;   // both systems converged
   double pap[2];
   qeq_total<2>(part_pap, pap);
   const double al0 = stt->active[par][0] ? stt->rz[par][0] / pap[0] : 0.0;
@@ -2657,9 +2660,14 @@ __global__ void __launch_bounds__(QEQ_THREADS) k_qeq_update(int n, const int* __
 // (iteration counts, convergence ||r|| <= tol ||b||, the next r.z)
 __global__ void __launch_bounds__(QEQ_THREADS) k_qeq_direction(int n, const double* __restrict__ part_rz,
     QEqState* stt, int par, double tol, int maxiter, const double2* __restrict__ z, double2* __restrict__ p) {
+  const int a0 = stt->active[par][0], a1 = stt->active[par][1];
+  if (!a0 && !a1) {   // both converged: only carry the flags to the next parity
+    __syncthreads();  // every block has read the flags before block 0 writes the other parity
+    if (blockIdx.x == 0 && threadIdx.x == 0) stt->active[par ^ 1][0] = stt->active[par ^ 1][1] = 0;
+    return;
+  }
   double t[4];
   qeq_total<4>(part_rz, t);
-  const int a0 = stt->active[par][0], a1 = stt->active[par][1];
   const double be0 = a0 ? t[0] / stt->rz[par][0] : 0.0;
   const double be1 = a1 ? t[1] / stt->rz[par][1] : 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {

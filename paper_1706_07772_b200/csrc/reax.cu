@@ -1298,13 +1298,18 @@ reax_status do_qeq_solve(reax_ctx* c, const double* chi, const double* eta, doub
   k_qeq_start<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, w.stype, ty, Ap, rr, z, p, part);
   k_qeq_start_state<<<1, QEQ_THREADS, 0, s>>>(part, tol, maxiter, stt);
   int act[2] = {1, 1};
+  // the kernels of an iteration return at once when both systems have
+  // converged, so the host reads the flags only every QEQ_CHECK iterations
+  constexpr int QEQ_CHECK = 8;
   for (int it = 0; it < maxiter; ++it) {
     const int par = it & 1;
-    if (cudaMemcpyAsync(act, &stt->active[par][0], sizeof(act), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-      return fail_cuda(cudaGetLastError());
-    if (!act[0] && !act[1]) break;
-    k_qeq_spmv<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, off, hcol, hval, w.stype, ty, p, Ap, part);
+    if (it > 0 && it % QEQ_CHECK == 0) {
+      if (cudaMemcpyAsync(act, &stt->active[par][0], sizeof(act), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        return fail_cuda(cudaGetLastError());
+      if (!act[0] && !act[1]) break;
+    }
+    k_qeq_spmv<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, off, hcol, hval, w.stype, ty, p, Ap, part, stt, par);
     k_qeq_update<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, w.stype, ty, part, stt, par, x, rr, z, p, Ap, part2);
     k_qeq_direction<<<QEQ_GRID, QEQ_THREADS, 0, s>>>(N, part2, stt, par, tol, maxiter, z, p);
     c->launches_cur += 3;
