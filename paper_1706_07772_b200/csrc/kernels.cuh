@@ -363,7 +363,8 @@ __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int
                               const double* __restrict__ pos, const int* __restrict__ type, Grid g, int nt,
                               int* __restrict__ iperm, double4* __restrict__ spos, float4* __restrict__ sloc,
                               int* __restrict__ stype, const double* __restrict__ qin, Status* st,
-                              int* __restrict__ blk_pairs, int nblock) {
+                              int* __restrict__ blk_pairs, int nblock, unsigned long long* __restrict__ sfx,
+                              unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz) {
   pdl_wait();
   pdl_trigger();
   if (blk_pairs) {   // per-block pair counts of the next list build start at zero
@@ -427,6 +428,9 @@ __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int
     sloc[s] = make_float4(l[0], l[1], l[2], __int_as_float(t));
     stype[s] = t;
     iperm[i] = s;
+    sfx[s] = 0ull;   // the fixed-point force accumulators of this step start at zero
+    sfy[s] = 0ull;
+    sfz[s] = 0ull;
   }
 }
 
@@ -1719,22 +1723,25 @@ __device__ __forceinline__ void fin_block_sum(double& a, double& b, double (*red
     for (int k = 0; k < FIN_THREADS / 32; ++k) { a += red[0][k]; b += red[1][k]; }
   }
 }
-__global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __restrict__ perm,
-    unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
-    double* __restrict__ force, int nparts, const double2* __restrict__ epart, double* __restrict__ part,
-    unsigned* __restrict__ ticket, double* __restrict__ energy, int ne, Status* st) {
+__global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __restrict__ iperm,
+    const unsigned long long* __restrict__ sfx, const unsigned long long* __restrict__ sfy,
+    const unsigned long long* __restrict__ sfz, double* __restrict__ force, int nparts,
+    const double2* __restrict__ epart, double* __restrict__ part, unsigned* __restrict__ ticket,
+    double* __restrict__ energy, int ne, Status* st) {
   TL_SPAN(6);
   pdl_wait();
   pdl_trigger();
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < n) {
-    const int i = perm[s];
+  // input order: gathered (scattered 8-byte reads) and written as coalesced
+  // 24-byte rows (scattered partial-sector writes cost read-modify-writes in
+  // DRAM); the accumulators are zeroed by the next gather (k_cell_gather /
+  // k_nb_prep), not here
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int s = iperm[i];
     const double sc = 0x1.0p-35;
     static_assert(FIX_BITS == 35, "scale");
-    const double fx = (double)(long long)sfx[s] * sc, fy = (double)(long long)sfy[s] * sc, fz = (double)(long long)sfz[s] * sc;
-    sfx[s] = 0ull;
-    sfy[s] = 0ull;
-    sfz[s] = 0ull;
+    const double fx = (double)(long long)__ldcs(sfx + s) * sc, fy = (double)(long long)__ldcs(sfy + s) * sc,
+                 fz = (double)(long long)__ldcs(sfz + s) * sc;
     force[3 * (int64_t)i] = fx;
     force[3 * (int64_t)i + 1] = fy;
     force[3 * (int64_t)i + 2] = fz;

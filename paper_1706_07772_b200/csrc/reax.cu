@@ -677,7 +677,7 @@ void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, const do
     LAUNCH(c);
     launch_k(c, k_cell_gather, nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s, g.ncell, w.cell_start, w.perm, pos, type, g, nt,
                                                                w.iperm, w.spos, w.sloc, w.stype, q, w.st,
-             c->nb_plan ? w.blk_pairs : nullptr, g.nblock);
+             c->nb_plan ? w.blk_pairs : nullptr, g.nblock, w.sfx, w.sfy, w.sfz);
     LAUNCH(c);
   }
 }
@@ -797,7 +797,7 @@ void launch_finalize(reax_ctx* c, int N, double* force, double* energy, cudaStre
   WS& w = c->w;
   Timer t(c, 5, s);
   // one energy partial per half-list row (sorted order), summed in fixed order
-  launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.perm, w.sfx, w.sfy, w.sfz, force, N,
+  launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.iperm, w.sfx, w.sfy, w.sfz, force, N,
            w.erow, w.epart, w.ticket, energy, 2, w.st);
   LAUNCH(c);
 }
@@ -1507,7 +1507,7 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   cudaError_t e = cudaMemset(ctx->w.cell_cnt, 0, sizeof(int) * (g.ncell + 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.bdeg, 0, sizeof(int) * (std::max<int64_t>(n, 1) + 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.st, 0, sizeof(Status));
-  // fixed-point force accumulators: zero between steps (k_finalize resets them)
+  // fixed-point force accumulators: zeroed by every gather (k_cell_gather, k_nb_prep) before a nonbonded pass
   if (e == cudaSuccess) e = cudaMemset(ctx->w.sfx, 0, sizeof(long long) * std::max<int64_t>(n, 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.sfy, 0, sizeof(long long) * std::max<int64_t>(n, 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.sfz, 0, sizeof(long long) * std::max<int64_t>(n, 1));

@@ -125,3 +125,27 @@ def test_c3(params, qp):
     ctx, ref = _setup(s, params)
     hval = _matvec_check(ctx, ref, s, params, qp, seed=3)
     _solve_check(ctx, ref, s, params, qp, hval, tight=False)   # the serial oracle's tight solve takes minutes here
+
+
+def test_qeq_charges_drive_the_nonbonded_step(params, c0, c0_oracle, qp):
+    """A QEq step as an MD code runs it (charges re-distributed
+    every step): the GPU's QEq charges on the current lists feed
+    reax_nonbonded; energies and forces match the oracle's nonbonded terms at
+    the oracle's own QEq charges (both solved to 1e-11: the charges agree to
+    ~1e-10, far inside the energy/force tolerances)."""
+    ref = c0_oracle
+    qo, _, _, _ = oracle.qeq(ref["pos"], c0.type, c0.box, params, CUT["r_nonb"], ref["hrow"], ref["hcol"], qp.chi,
+                             qp.eta, tol=1e-11)
+    Eo, Fo = oracle.nonbonded_rows(ref["pos"], c0.type, qo, c0.box, params, CUT["r_nonb"])
+    pos = torch.from_numpy(c0.pos).to(DEV)
+    typ = torch.from_numpy(c0.type).to(DEV)
+    ctx = rx.Reax(len(c0.pos), c0.box, params, CUT, device=DEV)
+    ctx.build_lists(pos, typ)      # the lists of this step (positions only)
+    ctx.bond_orders()
+    ctx.qeq_build()
+    q, _, _, _ = ctx.qeq_solve(qp.chi, qp.eta, tol=1e-11)
+    F, E = ctx.nonbonded(pos, typ, q)
+    torch.cuda.synchronize()
+    F, E = F.cpu().numpy(), E.cpu().numpy()
+    assert np.all(np.abs(E - Eo) <= 1e-9 * np.abs(Eo)), (E, Eo)
+    assert np.max(np.abs(F - Fo) / (1 + np.abs(Fo))) <= 1e-8
