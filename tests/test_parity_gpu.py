@@ -260,3 +260,23 @@ def test_plan_near_limit_grid(params):
     L = 95.0
     s = gen.make_system(int(0.0978 * L ** 3), (L, L, L), gen.SEED_BASE + 1234)
     full_parity(s, params)
+
+
+@pytest.mark.parametrize("seed,ntypes", [(11, 4), (12, 4), (13, 1), (14, 7), (15, 16)])
+def test_parameter_draws_and_type_counts(seed, ntypes):
+    """Other seeded parameter tables from the same ranges (DESIGN.md reading
+    10), and other type counts (1 type; 7; the 16-type maximum,
+    REAX_MAX_TYPES): types drawn uniformly; full parity on c0-sized boxes."""
+    p = gen.make_params(seed=gen.SEED_BASE + seed, ntypes=ntypes)
+    s = gen.make_system(1500, (25.0, 24.0, 26.5), gen.SEED_BASE + 900 + seed)
+    rng = np.random.default_rng(seed)
+    s = gen.System(s.pos, rng.integers(0, ntypes, len(s.pos)).astype(np.int32), s.q, s.box)
+    full_parity(s, p)
+
+
+def test_zero_charges_zero_coulomb(params, c0):
+    """q = 0 everywhere: E_Coul is exactly 0 and the forces are
+    the vdW forces alone (the oracle at q = 0)."""
+    s = gen.System(c0.pos, c0.type, np.zeros_like(c0.q), c0.box)
+    ctx, ref, F, E = full_parity(s, params)
+    assert E[1] == 0.0
