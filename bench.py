@@ -154,10 +154,13 @@ def run_cpu_oracle(k, evals, threads):
     oracle.build()
     s, sample = oracle_sample(k, ORACLE_BUDGET_S / max(1, evals), threads)
     t0 = time.perf_counter()
+    phases = {}
     for _ in range(evals):
-        oracle.evaluate_stream(s, params, gen.CUTOFFS, threads=threads)
+        r = oracle.evaluate_stream(s, params, gen.CUTOFFS, threads=threads)
+        for k, v in r["phase_s"].items():
+            phases[k] = phases.get(k, 0.0) + v / evals
     dt = time.perf_counter() - t0
-    return len(s.pos) * evals / dt, dt, sample
+    return len(s.pos) * evals / dt, dt, sample, phases
 
 
 def reference_arm(args, rank, world):
@@ -604,9 +607,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         threads = oracle.THREADS
-        v, dt, sample = run_cpu_oracle(args.config, 1, threads)
+        v, dt, sample, phases = run_cpu_oracle(args.config, 1, threads)
         line["cpu_baseline"] = {"value": v, "unit": "atom-steps/s", "cores": threads, "cpu": cpu_model(),
-                                "kind": "oracle", "sample": f"{sample}; {dt:.1f} s on {threads} threads"}
+                                "kind": "oracle", "sample": f"{sample}; {dt:.1f} s on {threads} threads",
+                                "ns_per_atom_step": 1e9 / v, "phase_s": phases}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

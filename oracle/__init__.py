@@ -359,15 +359,21 @@ def evaluate_stream(system, params, cut, threads=None):
     """The whole path without a stored half list (c3/c4: 3.4e9 pairs at c4):
     per-atom digests of the list, the full bond list with BO', Delta' and
     corrected BO, energies and forces — each row straight from the cell grid."""
+    import time
+    t = [time.perf_counter()]
     pos = wrap(system.pos, system.box)
     cnt, dig = digest_cells(pos, system.box, cut["r_nonb"], threads)
+    t.append(time.perf_counter())
     brow, bcol, mir, raw = bonds(pos, system.type, system.box, params, cut["r_bond"], cut["bo_cut"], None, None,
                                  threads)
     dlt = delta(system.type, params, brow, raw)
     corr = bo_correct(system.type, params, brow, bcol, mir, raw, dlt)
+    t.append(time.perf_counter())
     E, F = nonbonded_rows(pos, system.type, system.q, system.box, params, cut["r_nonb"], threads)
+    t.append(time.perf_counter())
     return dict(pos=pos, cnt=cnt, dig=dig, brow=brow, bcol=bcol, mirror=mir, raw=raw, delta=dlt, corr=corr,
-                E=E, F=F)
+                E=E, F=F, phase_s={"lists (per-atom rows + digests)": t[1] - t[0], "bond orders": t[2] - t[1],
+                                   "nonbonded": t[3] - t[2]})
 
 
 def bond_energy_pair(r, raw, di, dboci, dj, dbocj, ti, tj, params, bparams):
