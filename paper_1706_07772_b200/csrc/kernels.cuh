@@ -544,7 +544,6 @@ struct RunInfo {
 struct NbrSmem {
   WinSmem W;
   RunInfo run[NHOME][MAX_RUNS];
-  int2 ivl[NBR_THREADS / 32][MAX_RUNS + 1];   // per warp: the non-empty intervals in run order
   float rcand2[NTP_MAX];
   int gbase[NHOME + 1];   // first row group of each home sub-cell (groups of NBR_G rows)
   int ncs[NBR_THREADS / 32][8];   // per warp: bond-candidate counters of its group's rows
@@ -554,7 +553,7 @@ struct NbrSmem {
 
 // Per-kernel constants of the half-list candidate test.
 struct RowTest {
-  float R2lo, R2mid, R2half, Rt, hy, hz, ihx;
+  float R2lo, R2mid, R2half, Rt, hy, hz, ihx;   // band [R2lo, R2lo + 2 R2half] = [R2lo, R2hi]
   double R2;
 };
 __device__ __forceinline__ RowTest make_rowtest(const DevParams* __restrict__ prm, const Grid& g) {
@@ -569,83 +568,85 @@ __device__ __forceinline__ RowTest make_rowtest(const DevParams* __restrict__ pr
   t.R2 = prm->R2;
   return t;
 }
-// window slot -> (sorted atom, window cell): two staging layouts
-struct SlotJK {
-  const int* j;
-  const unsigned char* k;
-  __device__ __forceinline__ int J(int t) const { return j[t]; }
-  __device__ __forceinline__ int K(int t) const { return k[t]; }
-};
+#ifndef NBR_GROUP
+#define NBR_GROUP 3   // measured at 4 CTAs/SM, 64 registers (c4): 3 rows 18.13 ms, 2 rows 18.53, 4 rows 18.84 (spills)
+#endif
+constexpr int NBR_G = NBR_GROUP;   // rows sharing one candidate stream
+
+__device__ __forceinline__ float4 lds_f4(unsigned a) {   // explicit 32-bit shared address (no per-use re-derivation)
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
 
 // A group of up to NBR_G consecutive rows (atoms) of one home sub-cell,
 // tested by one warp (Write Lists).  The atoms of a cell are
 // x-sorted, so the rows of a group are x-neighbours and share one candidate
-// stream: the forward runs of the sub-cell's half stencil, each cut to the
-// cells meeting [x_min - w, x_max + w] and then, the run being x-sorted, to
-// that x-window by binary search (w = sqrt(R^2 - d_yz^2), d_yz the smallest
-// distance of the group's atoms to the run's y-z cross-section, so no partner
-// is ever cut), then the own cell after the group's first row.  Each lane
-// loads one candidate (32 per step) and tests it against every row of the
-// group held in registers: the candidate's load and stream bookkeeping are
-// shared by the rows.  r^2 in fp32 against a band of +-m around R^2 (~70x the
-// fp32 error bound), the band settled by the exact FMA-free fp64 test (bit-
-// identical to the oracle's r^2); accepted window slots of row r are compacted
-// with one ballot per row and stored coalesced.  With BOND, the rare
-// candidates below the conservative BO' = bo_cut radius (~3 per row) are
-// appended per lane through a shared-memory counter of the row: no warp vote
-// (POPC/VOTE issue to the narrow XU pipe on sm_100a, 16 lanes/SM/clk, and
-// bound the list build); their order is irrelevant because k_bond_rank sorts
-// each bond row.  len[r] may exceed row_cap (the caller flags it).
-#ifndef NBR_GROUP
-#define NBR_GROUP 2   // measured at 4 CTAs/SM, 64 registers: 2 beats 1, 3, 4, 6 (c1 70 vs 75 us for 4)
-#endif
-constexpr int NBR_G = NBR_GROUP;   // rows sharing one candidate stream
-template <bool BOND, typename SI>
-__device__ __forceinline__ void nbr_group_test(const WinSmem& W, const RunInfo* __restrict__ runs, int2* ivl,
-                                               int Wslots, const float4* __restrict__ cand, SI sl,
-                                               const double4* __restrict__ spos, int si0, int nrow, int h,
-                                               const Grid& g, const RowTest& rt, uint16_t* __restrict__ nbr,
-                                               int row_cap, int* __restrict__ bc, int cand_cap,
-                                               const float* __restrict__ rc2, int nt, float rcmax, int* ncs,
-                                               int (&len)[NBR_G], int (&nc)[NBR_G]) {
+// stream: the forward runs of the sub-cell's half stencil, each cut first to
+// the cells meeting [x_min - w, x_max + w] and then, the run being x-sorted,
+// to that x-window by binary search (w = sqrt(R^2 - d_yz^2), d_yz the
+// smallest distance of the group's atoms to the run's y-z cross-section, so
+// no partner is ever cut), then the own cell after the group's first row.
+// The runs + own cell fit lanes 0..15 (empty intervals included), so stream
+// position p -> slot is a 4-step binary search over the lane-held interval
+// offsets (the interval of p is the largest q with excl(q) <= p): no
+// compaction, no vote.  Each lane loads one candidate (32 per step) and tests
+// it against every row of the group held in registers (bare coordinates; rows
+// beyond nrow are parked at -1e30 so they never test true): r^2 in fp32
+// against a band of +-m around R^2 (~70x the fp32 error bound), the band
+// settled by the exact FMA-free fp64 test (bit-identical to the oracle's
+// r^2); accepted window slots of row r are compacted with one ballot per row
+// and stored coalesced.  The rare candidates below the conservative BO' =
+// bo_cut radius (~3 per row) are appended per lane through a shared-memory
+// counter of the row (no warp vote; their order is irrelevant because
+// k_bond_rank sorts each bond row); the rare paths re-read what they need
+// (row type, atom index, bond row) from shared memory, so the hot loop
+// carries only coordinates, row pointers and lengths.  len[r] may exceed
+// row_cap (the caller flags it).
+__device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo* __restrict__ runs, int Wslots,
+                                                 const float4* __restrict__ cand, const int* __restrict__ cand_j,
+                                                 const unsigned char* __restrict__ cand_k,
+                                                 const double4* __restrict__ spos, int si0, int nrow, int h,
+                                                 const RowTest& rt, uint16_t* __restrict__ nbr, int row_cap,
+                                                 int* __restrict__ bc, int cand_cap, const float* __restrict__ rc2,
+                                                 int nt, float rcmax, int* ncs, int (&len)[NBR_G]) {
+  constexpr int G = NBR_G;
   const int lane = threadIdx.x & 31;
-  if (BOND && lane < NBR_G) ncs[lane] = 0;   // per-row bond-candidate counters (shared, this warp's)
+  if (lane < G) ncs[lane] = 0;   // per-row bond-candidate counters (shared, this warp's)
   __syncwarp();
-  const unsigned lt_mask = (1u << lane) - 1u, le_mask = lt_mask | (1u << lane);
-  float4 ri[NBR_G];
-  int sr[NBR_G];
-  uint16_t* rowp[NBR_G];
-  int* crowp[NBR_G];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  float rx[G], ry[G], rz[G];
+  uint16_t* rowp[G];
+  float xmin = 1e30f, xmax = -1e30f;
 #pragma unroll
-  for (int r = 0; r < NBR_G; ++r) {
-    const int q = si0 + (r < nrow ? r : 0);
-    ri[r] = cand[q];
-    sr[r] = sl.J(q);
-    rowp[r] = nbr + (int64_t)sr[r] * row_cap;
-    crowp[r] = BOND ? bc + (int64_t)sr[r] * cand_cap : nullptr;
+  for (int r = 0; r < G; ++r) {
     len[r] = 0;
-    nc[r] = 0;
+    if (r < nrow) {
+      const float4 c = cand[si0 + r];
+      rx[r] = c.x; ry[r] = c.y; rz[r] = c.z;
+      rowp[r] = nbr + (int64_t)cand_j[si0 + r] * row_cap;
+      xmin = fminf(xmin, c.x);
+      xmax = fmaxf(xmax, c.x);
+    } else {
+      rx[r] = ry[r] = rz[r] = -1e30f;   // r^2 overflows to inf (also against the +1e30 sentinel)
+      rowp[r] = nbr;
+    }
   }
   const int kh = c_win.home_k[h];
   const int ownlo = W.slot[kh];
-  float xmin = ri[0].x, xmax = ri[0].x;
-#pragma unroll
-  for (int r = 1; r < NBR_G; ++r)
-    if (r < nrow) { xmin = fminf(xmin, ri[r].x); xmax = fmaxf(xmax, ri[r].x); }
   // ---- intervals: lane q < nrun cuts run q, lane nrun takes the own cell
   const int nrun = c_win.nrun1[h];
   int ia = 0, il = 0;
   if (lane < nrun) {
     const RunInfo ru = runs[lane];
     const int ka = ru.ka, kb = ru.kb;
-    const int wxa = ru.wxa;                          // x cell offset (block frame) of the run's first cell
-    const float oy = ru.oy, oz = ru.oz;
+    const int wxa = ru.wxa;   // x cell offset (block frame) of the run's first cell
     float d2min = 1e30f;
 #pragma unroll
-    for (int r = 0; r < NBR_G; ++r) {
+    for (int r = 0; r < G; ++r) {
       if (r < nrow) {
-        const float dy = fmaxf(0.f, fmaxf(oy - ri[r].y, ri[r].y - (oy + rt.hy)));
-        const float dz = fmaxf(0.f, fmaxf(oz - ri[r].z, ri[r].z - (oz + rt.hz)));
+        const float dy = fmaxf(0.f, fmaxf(ru.oy - ry[r], ry[r] - (ru.oy + rt.hy)));
+        const float dz = fmaxf(0.f, fmaxf(ru.oz - rz[r], rz[r] - (ru.oz + rt.hz)));
         d2min = fminf(d2min, dy * dy + dz * dz);
       }
     }
@@ -655,7 +656,7 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, const RunInfo* 
       const int c0 = max(wxa, (int)floorf((xmin - w) * rt.ihx));
       const int c1 = min(wxa + (kb - ka), (int)floorf((xmax + w) * rt.ihx));
       if (c0 <= c1) {
-        int lo = W.slot[ka + (c0 - wxa)], hi = W.slot[ka + (c1 - wxa) + 1];
+        const int lo = W.slot[ka + (c0 - wxa)], hi = W.slot[ka + (c1 - wxa) + 1];
         const float xlo = xmin - w, xhi = xmax + w;
         int l = lo, u = hi;
         while (l < u) {
@@ -675,89 +676,79 @@ __device__ __forceinline__ void nbr_group_test(const WinSmem& W, const RunInfo* 
     ia = si0 + 1;
     il = W.slot[kh + 1] - ia;
   }
-  // compact the non-empty intervals, then exclusive offsets
-  const unsigned ne = __ballot_sync(0xffffffffu, il > 0);
   int inc = il;
-  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc += y;
   }
-  const int total = __shfl_sync(0xffffffffu, inc, 31);
-  const int start_q = inc - il;
-  // lane k takes the k-th non-empty interval (scatter through shared memory;
-  // __fns is a ~40-instruction software sequence on sm_100a)
-  if (il > 0) ivl[__popc(ne & lt_mask)] = make_int2(start_q, ia - start_q);
-  __syncwarp();
-  const int nint = __popc(ne);
-  const int2 iv = ivl[lane < nint ? lane : 0];
-  const int cstart = iv.x, cshift = iv.y;
+  const int total = __shfl_sync(0xffffffffu, inc, 15);
+  const int excl = inc - il;
+  const int shift = ia - excl;   // slot = p + shift inside the lane's interval
+  // own-cell partners of row r: slots after si0 + r only (tself > thr0 + r)
+  const unsigned thr0 = (unsigned)(si0 - ownlo);
+  const unsigned cand_s = (unsigned)__cvta_generic_to_shared(cand);
   for (int p0 = 0; p0 < total; p0 += 32) {
-    const int rel = cstart - p0;
-    const bool here = lane < nint && rel >= 0 && rel < 32;
-    const unsigned M = __reduce_or_sync(0xffffffffu, here ? (1u << rel) : 0u);
-    const int before = __popc(__ballot_sync(0xffffffffu, lane < nint && rel < 0));
-    const int q = before + __popc(M & le_mask) - 1;
     const int p = p0 + lane;
-    const int slot = p + __shfl_sync(0xffffffffu, cshift, q);
-    const bool valid = p < total;
-    const float4 c = cand[valid ? slot : Wslots];   // Wslots: sentinel
+    int q = 0;
+#pragma unroll
+    for (int step = 8; step >= 1; step >>= 1)
+      if (__shfl_sync(0xffffffffu, excl, q + step) <= p) q += step;
+    const int sh = __shfl_sync(0xffffffffu, shift, q);
+    const int slot = p < total ? p + sh : Wslots;   // Wslots: sentinel at 1e30
+    const float4 c = lds_f4(cand_s + 16u * (unsigned)slot);
     const unsigned tself = (unsigned)(slot - ownlo);
-    // all rows first (independent chains), then the rare band / bond paths
-    float r2v[NBR_G];
-    bool in[NBR_G], band[NBR_G];
-    bool anyband = false, anybond = false;
+    float r2v[G];
+    unsigned mk[G];
+    bool rare = false;
 #pragma unroll
-    for (int r = 0; r < NBR_G; ++r) {
-      const float dx = c.x - ri[r].x, dy = c.y - ri[r].y, dz = c.z - ri[r].z;
+    for (int r = 0; r < G; ++r) {
+      const float dx = c.x - rx[r], dy = c.y - ry[r], dz = c.z - rz[r];
       r2v[r] = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const bool ok = r < nrow && tself > (unsigned)(si0 + r - ownlo);   // own-cell partners after row r only
-      in[r] = ok && r2v[r] < rt.R2lo;
-      band[r] = ok && !in[r] && fabsf(r2v[r] - rt.R2mid) <= rt.R2half;
-      anyband |= band[r];
+      const bool ok = tself > thr0 + r;
+      mk[r] = __ballot_sync(0xffffffffu, ok & (r2v[r] < rt.R2lo));
+      // rare: inside the fp32 band around R^2 (settled exactly below) or a
+      // possible bond candidate (rcmax < R2lo); bitwise, so no branches
+      rare |= ok & ((fabsf(r2v[r] - rt.R2mid) <= rt.R2half) | (r2v[r] <= rcmax));
     }
-    if (__any_sync(0xffffffffu, anyband)) {
-#pragma unroll
-      for (int r = 0; r < NBR_G; ++r) {
-        if (band[r]) {  // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
-          const double4 xi = spos[sr[r]];
-          const double4 xj = spos[sl.J(slot)];
-          const double4 sh = W.shift[sl.K(slot)];
-          const double ex = __dadd_rn(__dsub_rn(xj.x, xi.x), sh.x);
-          const double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), sh.y);
-          const double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), sh.z);
-          const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
-          in[r] = d2 <= rt.R2;
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < NBR_G; ++r) {
-      const unsigned mk = __ballot_sync(0xffffffffu, in[r]);
-      const int pp = len[r] + __popc(mk & lt_mask);
-      if (in[r] && pp < row_cap) rowp[r][pp] = (uint16_t)slot;
-      len[r] += __popc(mk);
-      anybond |= in[r] && r2v[r] <= rcmax;
-    }
-    if (BOND && anybond) {   // rare (~3 bond candidates per row): per-lane append, no warp vote
+    if (__any_sync(0xffffffffu, rare)) {
       const int tj = __float_as_int(c.w);
 #pragma unroll
-      for (int r = 0; r < NBR_G; ++r) {
-        if (in[r] && r2v[r] <= rc2[__float_as_int(ri[r].w) * nt + tj]) {
-          const int pc = atomicAdd(ncs + r, 1);
-          if (pc < cand_cap) crowp[r][pc] = sl.J(slot);
+      for (int r = 0; r < G; ++r) {
+        const bool ok = tself > thr0 + r;
+        bool in = ((mk[r] >> lane) & 1u) != 0u;
+        if (ok && !in && fabsf(r2v[r] - rt.R2mid) <= rt.R2half) {
+          // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
+          const int k = cand_k[slot];
+          const double4 xi = spos[cand_j[si0 + r]];
+          const double4 xj = spos[cand_j[slot]];
+          const double4 sw = W.shift[k];
+          const double ex = __dadd_rn(__dsub_rn(xj.x, xi.x), sw.x);
+          const double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), sw.y);
+          const double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), sw.z);
+          const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+          in = d2 <= rt.R2;
+        } else if (in && r2v[r] <= rc2[__float_as_int(cand[si0 + r].w) * nt + tj]) {
+          const int pc = atomicAdd(ncs + r, 1);   // per-lane append, no warp vote
+          if (pc < cand_cap) bc[(int64_t)cand_j[si0 + r] * cand_cap + pc] = cand_j[slot];
         }
+        mk[r] = __ballot_sync(0xffffffffu, in);
       }
+    }
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      const int pp = len[r] + __popc(mk[r] & lt_mask);
+      if (((mk[r] >> lane) & 1u) && pp < row_cap) rowp[r][pp] = (uint16_t)slot;
+      len[r] += __popc(mk[r]);
     }
   }
   __syncwarp();
-#pragma unroll
-  for (int r = 0; r < NBR_G; ++r) nc[r] = BOND ? ncs[r] : 0;
 }
 
 // One CTA per (home block, split).  Candidates of the window are staged in
 // shared memory as fp32 coordinates relative to the block origin.  A warp
 // takes a group of NBR_G rows of one home sub-cell at a time (dynamically)
-// and runs nbr_group_test on it (with bond candidates).
+// and runs nbr_group_stream on it (with bond candidates).
 #ifndef NBR_MINB
 #define NBR_MINB 4   // 4 CTAs x 8 warps at <= 64 registers (36 B of spills; measured faster than 3 at 80)
 #endif
@@ -845,7 +836,6 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
   if (threadIdx.x < 32) cand[W + threadIdx.x] = make_float4(1e30f, 1e30f, 1e30f, 0.f);  // sentinel
   __syncthreads();
   TL_MARK(0, 1, W);
-  const SlotJK sl{cand_j, cand_k};
   // groups of NBR_G consecutive rows of one home sub-cell; this CTA takes
   // groups split, split + nsplit, ...
   const int ngroups = S.gbase[NHOME];
@@ -862,8 +852,10 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
     const int nrow = min(NBR_G, S.W.cnt[kh] - a0);
     const int si0 = S.W.slot[kh] + a0;
     int len[NBR_G], nc[NBR_G];
-    nbr_group_test<true>(S.W, S.run[h], S.ivl[threadIdx.x >> 5], W, cand, sl, spos, si0, nrow, h, g, rt, nbr, row_cap,
-                         bc, cand_cap, S.rcand2, nt, rcmax, S.ncs[threadIdx.x >> 5], len, nc);
+    nbr_group_stream(S.W, S.run[h], W, cand, cand_j, cand_k, spos, si0, nrow, h, rt, nbr, row_cap, bc, cand_cap,
+                     S.rcand2, nt, rcmax, S.ncs[threadIdx.x >> 5], len);
+#pragma unroll
+    for (int r = 0; r < NBR_G; ++r) nc[r] = S.ncs[threadIdx.x >> 5][r];
     if (lane < nrow) {
       int l = len[0], c = nc[0];
 #pragma unroll
@@ -893,6 +885,97 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
 #endif
 }
 
+// ---- branch-free fp64 math for the nonbonded pair (inputs in known, finite,
+// normal ranges; ~1-2 ulp).  Tables live in shared memory.
+constexpr int EXP_TBL = 64;    // 2^(j/64)
+// polynomial / reduction constants as constant-bank operands (ptxas otherwise
+// re-materialises 64-bit literals with register moves inside the pair loop)
+__constant__ double c_nb[28] = {
+    0x1.71547652b82fep+6,      // 0  64 / ln 2
+    6755399441055744.0,        // 1  1.5 * 2^52
+    0x1.62e42fee00000p-7,      // 2  ln2_hi / 64
+    0x1.a39ef35793c76p-39,     // 3  ln2_lo / 64
+    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5,   // 4-7  exp polynomial
+    -1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5,   // 8-12 log1p polynomial
+    0x1.62e42fee00000p-1,      // 13 ln2_hi
+    0x1.a39ef35793c76p-33,     // 14 ln2_lo
+    0.375, 2.0 / 9.0, 1.0 / 3.0,   // 15-17 Halley rsqrt / rcbrt
+    20.0, -70.0, 84.0, -35.0, -140.0,   // 18-22 taper
+    1.0,                       // 23
+    14.0 / 81.0,               // 24 rcbrt quartic term
+    0x1.0p35,                  // 25 fixed-point force scale 2^FIX_BITS
+    6755399441055744.0,        // 26 1.5 * 2^52 (round-to-integer magic)
+    65536.0};                  // 27 fixed-point range limit per contribution
+
+constexpr int LOG_TBL = 128;   // {1/c_j, -log(1/c_j)}, c_j = 1 + (j + 1/2)/128
+
+// e^x for |x| < 700: x = k ln2/64 + r, |r| <= ln2/128; e^r - 1 by a degree-5
+// polynomial (error r^6/720 < 4e-17); 2^(k/64) = 2^(k>>6) * T[k & 63].
+__device__ __forceinline__ double fexp(double x, const double* __restrict__ T) {
+  double t = fma(x, c_nb[0], c_nb[1]);
+  double kd = t - c_nb[1];
+  int k = __double2loint(t);
+  double r = fma(kd, -c_nb[2], x);
+  r = fma(kd, -c_nb[3], r);
+  double q = fma(r, c_nb[4], c_nb[5]);
+  q = fma(q, r, c_nb[6]);
+  q = fma(q, r, c_nb[7]);
+  double p = fma(q, r * r, r);
+  double tj = T[k & (EXP_TBL - 1)];
+  double y = fma(tj, p, tj);
+  return __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
+}
+
+// ln x for finite normal x > 0: x = 2^e m, m in [1,2); m/c_j = 1 + r with
+// |r| < 2^-8; log1p(r) by a degree-6 polynomial (error < 3e-18).
+__device__ __forceinline__ double flog(double x, const double2* __restrict__ LT) {
+  int hi = __double2hiint(x);
+  int e = (hi >> 20) - 1023;
+  int j = (hi >> 13) & (LOG_TBL - 1);
+  double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(x));
+  double2 t = LT[j];
+  double r = fma(m, t.x, -c_nb[23]);
+  double q = fma(r, c_nb[8], c_nb[9]);
+  q = fma(q, r, c_nb[10]);
+  q = fma(q, r, c_nb[11]);
+  q = fma(q, r, c_nb[12]);
+  double p = fma(q, r * r, r);
+  // (double)e without I2F.F64 (an XU op): 2^52 + 2^31 + e, minus 2^52 + 2^31
+  double ed = __hiloint2double(0x43300000, e ^ 0x80000000) - 4503601774854144.0;
+  return fma(ed, c_nb[13], t.y) + fma(ed, c_nb[14], p);
+}
+
+// approximate seeds from the MUFU unit, then one Halley-type correction:
+// (1-e)^(-1/2) = 1 + e/2 + 3e^2/8 + ..., (1-e)^(-1/3) = 1 + e/3 + 2e^2/9 + ...,
+// 1/(1-e) = 1 + e + e^2: relative error ~ (2^-22)^3
+__device__ __forceinline__ double frsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x * y, y, c_nb[23]);
+  return fma(y * e, fma(e, c_nb[15], c_nb[7]), y);
+}
+__device__ __forceinline__ double frcp(double x) {
+  // MUFU.RCP64H seed (~2^-22), then 1/(1-e) = 1 + e + e^2: ~1e-20
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, c_nb[23]);
+  return fma(y * e, c_nb[23] + e, y);
+}
+__device__ __forceinline__ double frcbrt(double x) {
+  // fp32 seed x^(-1/3) = 2^(-log2(x)/3) from MUFU.LG2/EX2 (~1e-6), then one
+  // quartic correction (1-e)^(-1/3) = 1 + e/3 + 2e^2/9 + 14e^3/81: ~1e-23
+  const float xf = __double2float_rn(x);
+  float lf, yf;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lf) : "f"(xf));
+  lf *= -0.333333343f;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(lf));
+  double y = (double)yf;
+  double e = fma(-x * y, y * y, c_nb[23]);
+  double q = fma(e, c_nb[24], c_nb[16]);
+  q = fma(e, q, c_nb[17]);
+  return fma(y * e, q, y);
+}
+
 // =================================================== a4 bond orders (B1-B2)
 __device__ __forceinline__ double min_image(double d, double L) {
   // same rule as the definition: [-L/2, L/2)
@@ -911,6 +994,17 @@ __device__ __forceinline__ double4 bo_raw(double r, const BOPair& c) {
   return make_double4(v[0], v[1], v[2], (v[0] + v[1]) + v[2]);
 }
 
+// bo_raw with the table exp/log of the nonbonded kernel (~1-2 ulp; the
+// outer exponent is clamped at -700, where BO' < 1e-304 stands for 0)
+__device__ __forceinline__ double4 bo_raw_fast(double r, const BOPair& c, const double* __restrict__ ET,
+                                               const double2* __restrict__ LT) {
+  const double lr = flog(r, LT);
+  double v[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v[k] = fexp(fmax(c.pa[k] * fexp(c.pb[k] * (lr - c.lr0[k]), ET), -700.0), ET);
+  return make_double4(v[0], v[1], v[2], (v[0] + v[1]) + v[2]);
+}
+
 // Bond candidates are flattened across a warp: lane i owns atom a0+i, the
 // warp scans the candidate counts and every lane then evaluates one
 // (atom, candidate) pair per round: the exact FMA-free r^2 <= r_bond^2 test,
@@ -925,8 +1019,12 @@ __global__ void k_bond_eval(int n, const double4* __restrict__ spos, const int* 
   pdl_trigger();
   clear_status(scan_status, scan_tiles);
   __shared__ BOPair sbo[NTP_MAX];
+  __shared__ double ET[EXP_TBL];
+  __shared__ double2 LT[LOG_TBL];
   const int nt = prm->nt;
   for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) sbo[t] = prm->bo[t];
+  for (int t = threadIdx.x; t < EXP_TBL; t += blockDim.x) ET[t] = prm->exp_tbl[t];
+  for (int t = threadIdx.x; t < LOG_TBL; t += blockDim.x) LT[t] = make_double2(prm->log_tbl[2 * t], prm->log_tbl[2 * t + 1]);
   __syncthreads();
   const double rb2 = prm->rb2, bo_cut = prm->bo_cut;
   const int lane = threadIdx.x & 31;
@@ -956,7 +1054,7 @@ __global__ void k_bond_eval(int n, const double4* __restrict__ spos, const int* 
     bool keep = false;
     double4 v = make_double4(0, 0, 0, 0);
     if (r2 <= rb2) {
-      v = bo_raw(__dsqrt_rn(r2), sbo[stype[s] * nt + stype[j]]);
+      v = bo_raw_fast(__dsqrt_rn(r2), sbo[stype[s] * nt + stype[j]], ET, LT);
       keep = v.w >= bo_cut;
     }
     if (keep) {
@@ -1128,97 +1226,6 @@ __global__ void k_nb_prep(int n, const double* __restrict__ q, const int* __rest
 struct NBConst {
   double invR, phalf, inv_p, m140invR;
 };
-
-// ---- branch-free fp64 math for the nonbonded pair (inputs in known, finite,
-// normal ranges; ~1-2 ulp).  Tables live in shared memory.
-constexpr int EXP_TBL = 64;    // 2^(j/64)
-// polynomial / reduction constants as constant-bank operands (ptxas otherwise
-// re-materialises 64-bit literals with register moves inside the pair loop)
-__constant__ double c_nb[28] = {
-    0x1.71547652b82fep+6,      // 0  64 / ln 2
-    6755399441055744.0,        // 1  1.5 * 2^52
-    0x1.62e42fee00000p-7,      // 2  ln2_hi / 64
-    0x1.a39ef35793c76p-39,     // 3  ln2_lo / 64
-    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5,   // 4-7  exp polynomial
-    -1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5,   // 8-12 log1p polynomial
-    0x1.62e42fee00000p-1,      // 13 ln2_hi
-    0x1.a39ef35793c76p-33,     // 14 ln2_lo
-    0.375, 2.0 / 9.0, 1.0 / 3.0,   // 15-17 Halley rsqrt / rcbrt
-    20.0, -70.0, 84.0, -35.0, -140.0,   // 18-22 taper
-    1.0,                       // 23
-    14.0 / 81.0,               // 24 rcbrt quartic term
-    0x1.0p35,                  // 25 fixed-point force scale 2^FIX_BITS
-    6755399441055744.0,        // 26 1.5 * 2^52 (round-to-integer magic)
-    65536.0};                  // 27 fixed-point range limit per contribution
-
-constexpr int LOG_TBL = 128;   // {1/c_j, -log(1/c_j)}, c_j = 1 + (j + 1/2)/128
-
-// e^x for |x| < 700: x = k ln2/64 + r, |r| <= ln2/128; e^r - 1 by a degree-5
-// polynomial (error r^6/720 < 4e-17); 2^(k/64) = 2^(k>>6) * T[k & 63].
-__device__ __forceinline__ double fexp(double x, const double* __restrict__ T) {
-  double t = fma(x, c_nb[0], c_nb[1]);
-  double kd = t - c_nb[1];
-  int k = __double2loint(t);
-  double r = fma(kd, -c_nb[2], x);
-  r = fma(kd, -c_nb[3], r);
-  double q = fma(r, c_nb[4], c_nb[5]);
-  q = fma(q, r, c_nb[6]);
-  q = fma(q, r, c_nb[7]);
-  double p = fma(q, r * r, r);
-  double tj = T[k & (EXP_TBL - 1)];
-  double y = fma(tj, p, tj);
-  return __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
-}
-
-// ln x for finite normal x > 0: x = 2^e m, m in [1,2); m/c_j = 1 + r with
-// |r| < 2^-8; log1p(r) by a degree-6 polynomial (error < 3e-18).
-__device__ __forceinline__ double flog(double x, const double2* __restrict__ LT) {
-  int hi = __double2hiint(x);
-  int e = (hi >> 20) - 1023;
-  int j = (hi >> 13) & (LOG_TBL - 1);
-  double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(x));
-  double2 t = LT[j];
-  double r = fma(m, t.x, -c_nb[23]);
-  double q = fma(r, c_nb[8], c_nb[9]);
-  q = fma(q, r, c_nb[10]);
-  q = fma(q, r, c_nb[11]);
-  q = fma(q, r, c_nb[12]);
-  double p = fma(q, r * r, r);
-  // (double)e without I2F.F64 (an XU op): 2^52 + 2^31 + e, minus 2^52 + 2^31
-  double ed = __hiloint2double(0x43300000, e ^ 0x80000000) - 4503601774854144.0;
-  return fma(ed, c_nb[13], t.y) + fma(ed, c_nb[14], p);
-}
-
-// approximate seeds from the MUFU unit, then one Halley-type correction:
-// (1-e)^(-1/2) = 1 + e/2 + 3e^2/8 + ..., (1-e)^(-1/3) = 1 + e/3 + 2e^2/9 + ...,
-// 1/(1-e) = 1 + e + e^2: relative error ~ (2^-22)^3
-__device__ __forceinline__ double frsqrt(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x * y, y, c_nb[23]);
-  return fma(y * e, fma(e, c_nb[15], c_nb[7]), y);
-}
-__device__ __forceinline__ double frcp(double x) {
-  // MUFU.RCP64H seed (~2^-22), then 1/(1-e) = 1 + e + e^2: ~1e-20
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, c_nb[23]);
-  return fma(y * e, c_nb[23] + e, y);
-}
-__device__ __forceinline__ double frcbrt(double x) {
-  // fp32 seed x^(-1/3) = 2^(-log2(x)/3) from MUFU.LG2/EX2 (~1e-6), then one
-  // quartic correction (1-e)^(-1/3) = 1 + e/3 + 2e^2/9 + 14e^3/81: ~1e-23
-  const float xf = __double2float_rn(x);
-  float lf, yf;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lf) : "f"(xf));
-  lf *= -0.333333343f;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(lf));
-  double y = (double)yf;
-  double e = fma(-x * y, y * y, c_nb[23]);
-  double q = fma(e, c_nb[24], c_nb[16]);
-  q = fma(e, q, c_nb[17]);
-  return fma(y * e, q, y);
-}
 
 // device self-test of the nonbonded math (tests/test_math_gpu.py)
 __global__ void k_selftest_math(int n, const double* __restrict__ x, double* __restrict__ out,

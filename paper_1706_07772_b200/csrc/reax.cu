@@ -87,6 +87,7 @@ WindowTables make_tables() {
         runs.push_back({wk(oxa, oy, oz), wk(oxb, oy, oz)});
       }
     T.nrun1[h] = (int)runs.size();
+    if (T.nrun1[h] + 1 > 16) abort();   // k_nbr_build keeps the runs + own cell in lanes 0..15
     for (size_t q = 0; q < runs.size(); ++q) {
       T.run1_a[h][q] = runs[q].first;
       T.run1_b[h][q] = runs[q].second;
