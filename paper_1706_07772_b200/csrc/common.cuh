@@ -129,18 +129,17 @@ struct WS {
   int* bkey;         // bond_cap  partner (original index): the row sort key
   int* bown;         // bond_cap  row owner (sorted index)
   int* bmir;         // bond_cap
-  double* bo;        // bond_cap * 8
+  double* bo;        // 8 arrays of bond_cap: BO'sigma, BO'pi, BO'pipi, BO', BO, BOsigma, BOpi, BOpipi (entry e of array k at k * bond_cap + e)
   double2* delta;    // n
-  unsigned long long* sfx;   // n  sorted-order forces, int64 fixed point (2^-35 kcal/mol/A)
-  unsigned long long* sfy;   // n
-  unsigned long long* sfz;   // n
+  unsigned long long* sf;    // 3n: sorted-order forces {x, y, z} per atom (one 24-byte record),
+                             //     int64 fixed point (2^-35 kcal/mol/A)
   double2* erow;     // n   per-row (E_vdW, E_Coul)
   double* epart;     // energy reduction partials
   unsigned* ticket;  // last-block counter of the energy reduction
   int* ucol;         // bond_cap  unsorted full-list entries (fill order)
   int* ukey;         // bond_cap
   int* uown;         // bond_cap
-  double4* uraw;     // bond_cap
+  double4* uraw;     // bond_cap: first 8 bytes per entry = its candidate index (fill -> rank)
   long long* scan_tmp;  // scan partials
   long long* exp_off;   // n + 1 (export scratch)
   unsigned long long* lb_status;  // look-back scan tile status

@@ -359,12 +359,48 @@ __device__ __forceinline__ double wrap_key(double x, double L) { return isfinite
 
 // Per cell (one warp): order the cell's atoms by x (rank sort in registers;
 // deterministic), then gather the sorted arrays.
+// One atom record of the sorted arrays (sorted position sp, staged record v,
+// input index i, cell cc)
+__device__ __forceinline__ void gather_one(int sp, int i, const double4& v, int t, const int (&cc)[3], const Grid& g,
+                                           int nt, bool has_q, int* __restrict__ perm, int* __restrict__ iperm,
+                                           double4* __restrict__ spos, float4* __restrict__ sloc,
+                                           int* __restrict__ stype, Status* st, unsigned long long* __restrict__ sf) {
+  const double x[3] = {v.x, v.y, v.z};
+  double w[3];
+  float l[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    w[d] = isfinite(x[d]) ? wrap_coord(x[d], g.L[d]) : 0.0;
+    l[d] = (float)(w[d] - cc[d] * g.h[d]);
+  }
+  t = (t < 0 || t >= nt) ? 0 : t;   // flagged by k_bin; clamp keeps every table index valid
+  const double qs = has_q ? v.w : 0.0;   // reax_step: charges staged by k_scatter (reax_nonbonded: k_nb_prep)
+  if (has_q && !isfinite(qs)) set_flag(st, ST_NONFINITE_IN);
+  perm[sp] = i;
+  spos[sp] = make_double4(w[0], w[1], w[2], qs);
+  sloc[sp] = make_float4(l[0], l[1], l[2], __int_as_float(t));
+  stype[sp] = t;
+  iperm[i] = sp;
+  // the fixed-point force accumulators of this step start at zero (one 24-byte record per atom)
+  sf[3 * (int64_t)sp] = 0ull;
+  sf[3 * (int64_t)sp + 1] = 0ull;
+  sf[3 * (int64_t)sp + 2] = 0ull;
+}
+
+// Warp per cell: order the cell's atoms by (wrapped x, original index) —
+// deterministic, and every run of cells along x is then x-sorted, which lets
+// the list build cut each run to the x-window of a row by binary search —
+// and write the sorted arrays.  Each lane reads its atom's input record once
+// (scattered) and writes it to its sorted position.
+__device__ __forceinline__ double4 in_rec(const double* __restrict__ pos, const double* __restrict__ qin, int i) {
+  return make_double4(pos[3 * (int64_t)i], pos[3 * (int64_t)i + 1], pos[3 * (int64_t)i + 2], qin ? qin[i] : 0.0);
+}
 __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int* __restrict__ perm,
-                              const double* __restrict__ pos, const int* __restrict__ type, Grid g, int nt,
+                              const double* __restrict__ pos, const int* __restrict__ type,
+                              const double* __restrict__ qin, Grid g, int nt,
                               int* __restrict__ iperm, double4* __restrict__ spos, float4* __restrict__ sloc,
-                              int* __restrict__ stype, const double* __restrict__ qin, Status* st,
-                              int* __restrict__ blk_pairs, int nblock, unsigned long long* __restrict__ sfx,
-                              unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz) {
+                              int* __restrict__ stype, Status* st,
+                              int* __restrict__ blk_pairs, int nblock, unsigned long long* __restrict__ sf) {
   pdl_wait();
   pdl_trigger();
   if (blk_pairs) {   // per-block pair counts of the next list build start at zero
@@ -374,63 +410,47 @@ __global__ void k_cell_gather(int ncell, const int* __restrict__ cell_start, int
   int c = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   int lane = threadIdx.x & 31;
   if (c >= ncell) return;
-  int a = cell_start[c], b = cell_start[c + 1], m = b - a;
-  // order the cell's atoms by (wrapped x, original index): deterministic, and
-  // every run of cells along x is then x-sorted, which lets the list build
-  // cut each run to the x-window of a row by binary search
+  const int a = cell_start[c], b = cell_start[c + 1], m = b - a;
+  const int cc[3] = {c % g.nc[0], (c / g.nc[0]) % g.nc[1], c / (g.nc[0] * g.nc[1])};
   if (m <= 32) {
     const int v = lane < m ? perm[a + lane] : 0x7fffffff;
-    const double xv = lane < m ? wrap_key(pos[3 * (int64_t)v], g.L[0]) : 0.0;
+    const double4 r = lane < m ? in_rec(pos, qin, v) : make_double4(0.0, 0.0, 0.0, 0.0);
+    const int t = lane < m ? type[v] : 0;
+    const double xv = wrap_key(r.x, g.L[0]);
     int rank = 0;
     for (int q = 0; q < m; ++q) {
       const int vq = __shfl_sync(0xffffffffu, v, q);
       const double xq = __shfl_sync(0xffffffffu, xv, q);
       rank += (xq < xv) || (xq == xv && vq < v);
     }
+    __syncwarp();   // every lane has read its perm entry before any is overwritten
+    if (lane < m) gather_one(a + rank, v, r, t, cc, g, nt, qin != nullptr, perm, iperm, spos, sloc, stype, st, sf);
+  } else {   // rare (Poisson tail): serial insertion sort of the input indices, scratch in the cell's force records
+    unsigned long long* key = sf + 3 * (int64_t)a;   // key q at key[3 q]; zeroed by gather_one afterwards
+    for (int q = lane; q < m; q += 32) key[3 * q] = (unsigned long long)(unsigned)perm[a + q];
     __syncwarp();
-    if (lane < m) perm[a + rank] = v;
-  } else if (lane == 0) {  // rare (Poisson tail): serial insertion sort
-    for (int i = a + 1; i < b; ++i) {
-      const int v = perm[i];
-      const double xv = wrap_key(pos[3 * (int64_t)v], g.L[0]);
-      int j = i - 1;
-      while (j >= a) {
-        const int u = perm[j];
-        const double xu = wrap_key(pos[3 * (int64_t)u], g.L[0]);
-        if (!(xu > xv || (xu == xv && u > v))) break;
-        perm[j + 1] = u;
-        --j;
+    if (lane == 0) {
+      for (int q = 1; q < m; ++q) {
+        const unsigned long long kv = key[3 * q];
+        const int vv = (int)kv;
+        const double xv = wrap_key(pos[3 * (int64_t)vv], g.L[0]);
+        int u = q - 1;
+        while (u >= 0) {
+          const unsigned long long ku = key[3 * u];
+          const double xu = wrap_key(pos[3 * (int64_t)(int)ku], g.L[0]);
+          if (!(xu > xv || (xu == xv && (int)ku > vv))) break;
+          key[3 * (u + 1)] = ku;
+          --u;
+        }
+        key[3 * (u + 1)] = kv;
       }
-      perm[j + 1] = v;
     }
-  }
-  __syncwarp();
-  int cc[3] = {c % g.nc[0], (c / g.nc[0]) % g.nc[1], c / (g.nc[0] * g.nc[1])};
-  for (int q = lane; q < m; q += 32) {
-    int s = a + q;
-    int i = perm[s];
-    double w[3];
-    float l[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      double x = pos[3 * (int64_t)i + d];
-      w[d] = isfinite(x) ? wrap_coord(x, g.L[d]) : 0.0;
-      l[d] = (float)(w[d] - cc[d] * g.h[d]);
+    __syncwarp();
+    for (int q = lane; q < m; q += 32) {
+      const int i = (int)key[3 * q];
+      gather_one(a + q, i, in_rec(pos, qin, i), type[i], cc, g, nt, qin != nullptr, perm, iperm, spos, sloc, stype, st,
+                 sf);
     }
-    int t = type[i];
-    t = (t < 0 || t >= nt) ? 0 : t;  // flagged by k_bin; clamp keeps every table index valid
-    double qs = 0.0;
-    if (qin) {   // reax_step: charges gathered here (reax_nonbonded does it in k_nb_prep)
-      qs = qin[i];
-      if (!isfinite(qs)) set_flag(st, ST_NONFINITE_IN);
-    }
-    spos[s] = make_double4(w[0], w[1], w[2], qs);
-    sloc[s] = make_float4(l[0], l[1], l[2], __int_as_float(t));
-    stype[s] = t;
-    iperm[i] = s;
-    sfx[s] = 0ull;   // the fixed-point force accumulators of this step start at zero
-    sfy[s] = 0ull;
-    sfz[s] = 0ull;
   }
 }
 
@@ -1072,9 +1092,9 @@ __global__ void k_bond_eval(int n, const double4* __restrict__ spos, const int* 
 // slot", as an atomic decrement); bdeg returns to zero.  The
 // sort key (original partner index) is stored beside each entry.
 __global__ void k_bond_fill(int n, const int* __restrict__ bc, const int* __restrict__ bc_len,
-                            const double4* __restrict__ bc_raw, int cand_cap, const int* __restrict__ brow,
+                            int cand_cap, const int* __restrict__ brow,
                             const int* __restrict__ perm, int* __restrict__ bdeg, int* __restrict__ ucol,
-                            int* __restrict__ ukey, int* __restrict__ uown, double4* __restrict__ uraw,
+                            int* __restrict__ ukey, int* __restrict__ uown, long long* __restrict__ usrc,
                             long long bond_cap, Status* st) {
   TL_SPAN(2);
   pdl_wait();
@@ -1100,12 +1120,12 @@ __global__ void k_bond_fill(int n, const int* __restrict__ bc, const int* __rest
     int64_t slot = (int64_t)s * cand_cap + (t - excl_q);
     int j = bc[slot];
     if (j < 0) continue;
-    double4 v = bc_raw[slot];
     long long e1 = (long long)brow[s] + atomicSub(&bdeg[s], 1) - 1;
     long long e2 = (long long)brow[j] + atomicSub(&bdeg[j], 1) - 1;
-    // each side independently: every entry below the capacity is written
-    if (e1 < bond_cap) { ucol[e1] = j; ukey[e1] = perm[j]; uown[e1] = s; uraw[e1] = v; }
-    if (e2 < bond_cap) { ucol[e2] = s; ukey[e2] = perm[s]; uown[e2] = j; uraw[e2] = v; }
+    // each side independently: every entry below the capacity is written; the
+    // entry keeps the index of its candidate (k_bond_rank gathers BO' from it)
+    if (e1 < bond_cap) { ucol[e1] = j; ukey[e1] = perm[j]; uown[e1] = s; usrc[e1] = slot; }
+    if (e2 < bond_cap) { ucol[e2] = s; ukey[e2] = perm[s]; uown[e2] = j; usrc[e2] = slot; }
     if (e1 >= bond_cap || e2 >= bond_cap) set_flag(st, ST_BOND_OVF);
   }
 }
@@ -1115,7 +1135,8 @@ __global__ void k_bond_fill(int n, const int* __restrict__ bc, const int* __rest
 // number of smaller keys; it moves the entry to that position of the sorted
 // arrays.  Then one thread per atom sums BO' in that order: Delta'.
 __global__ void k_bond_rank(const int* __restrict__ brow, const int* __restrict__ ucol, const int* __restrict__ ukey,
-                            const int* __restrict__ uown, const double4* __restrict__ uraw, int* __restrict__ bcol,
+                            const int* __restrict__ uown, const long long* __restrict__ usrc,
+                            const double4* __restrict__ bc_raw, int* __restrict__ bcol,
                             int* __restrict__ bkey, int* __restrict__ bown, double* __restrict__ bo, long long bond_cap,
                             const Status* __restrict__ st) {
   TL_SPAN(3);
@@ -1133,9 +1154,11 @@ __global__ void k_bond_rank(const int* __restrict__ brow, const int* __restrict_
     bcol[o] = ucol[e];
     bkey[o] = key;
     bown[o] = s;
-    double4 v = uraw[e];
-    double* p = bo + 8 * o;
-    p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w;
+    const double4 v = bc_raw[usrc[e]];
+    bo[o] = v.x;                     // bond orders are stored as 8 arrays of bond_cap (BO_K)
+    bo[bond_cap + o] = v.y;
+    bo[2 * bond_cap + o] = v.z;
+    bo[3 * bond_cap + o] = v.w;
   }
 }
 
@@ -1150,7 +1173,7 @@ __global__ void k_bond_delta(int n, const int* __restrict__ brow, const int* __r
   int a = brow[s], b = brow[s + 1];
   if (b > bond_cap) b = (int)bond_cap;
   double sum = 0.0;
-  for (int e = a; e < b; ++e) sum += bo[8 * (int64_t)e + 3];
+  for (int e = a; e < b; ++e) sum += bo[3 * bond_cap + e];
   int t = stype[s];
   delta[s] = make_double2(sum - prm->val[t], sum - prm->val_boc[t]);
 }
@@ -1187,8 +1210,7 @@ __global__ void k_bond_correct(const int* __restrict__ brow, const int* __restri
     int ta = stype[ia], tb = stype[ib];
     double2 da = delta[ia], db = delta[ib];
     const BOPair& c = sbo[ta * nt + tb];
-    double* q = bo + 8 * e;
-    double bpi = q[1], bpp = q[2], bp = q[3];
+    double bpi = bo[bond_cap + e], bpp = bo[2 * bond_cap + e], bp = bo[3 * bond_cap + e];
     double f2 = exp(-p1 * da.x) + exp(-p1 * db.x);
     double f3 = -inv_p2 * log(0.5 * (exp(-p2 * da.x) + exp(-p2 * db.x)));
     double va = sval[ta], vb = sval[tb];
@@ -1200,17 +1222,16 @@ __global__ void k_bond_correct(const int* __restrict__ brow, const int* __restri
     double BO = bp * f145;
     double BOpi = bpi * f1 * f145;
     double BOpp = bpp * f1 * f145;
-    q[4] = BO;
-    q[5] = BO - BOpi - BOpp;
-    q[6] = BOpi;
-    q[7] = BOpp;
+    bo[4 * bond_cap + e] = BO;
+    bo[5 * bond_cap + e] = BO - BOpi - BOpp;
+    bo[6 * bond_cap + e] = BOpi;
+    bo[7 * bond_cap + e] = BOpp;
   }
 }
 
 // ====================================================== a7-a8 nonbonded
 __global__ void k_nb_prep(int n, const double* __restrict__ q, const int* __restrict__ perm, double4* __restrict__ spos,
-                          unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy,
-                          unsigned long long* __restrict__ sfz, Status* st) {
+                          unsigned long long* __restrict__ sf, Status* st) {
   pdl_wait();
   pdl_trigger();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1218,9 +1239,9 @@ __global__ void k_nb_prep(int n, const double* __restrict__ q, const int* __rest
   double qs = q[perm[s]];
   if (!isfinite(qs)) set_flag(st, ST_NONFINITE_IN);
   spos[s].w = qs;
-  sfx[s] = 0ull;
-  sfy[s] = 0ull;
-  sfz[s] = 0ull;
+  sf[3 * (int64_t)s] = 0ull;
+  sf[3 * (int64_t)s + 1] = 0ull;
+  sf[3 * (int64_t)s + 2] = 0ull;
 }
 
 struct NBConst {
@@ -1340,7 +1361,10 @@ __device__ void zero_rows_erow(const WinSmem& W, int split, int nsplit, double2*
   }
 }
 
-constexpr int NB_THREADS = 256;
+#ifndef NB_THREADS_DEF
+#define NB_THREADS_DEF 256
+#endif
+constexpr int NB_THREADS = NB_THREADS_DEF;
 constexpr int NB_WARPS = NB_THREADS / 32;
 #ifndef NB_MINB
 #define NB_MINB 2   // 2 CTAs x 8 warps at <= 128 registers (3 CTAs at 80 registers spills; measured slower)
@@ -1467,7 +1491,7 @@ struct NBSmem {
 __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const int* __restrict__ cell_start,
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
-    unsigned long long* __restrict__ sfx, unsigned long long* __restrict__ sfy, unsigned long long* __restrict__ sfz,
+    unsigned long long* __restrict__ sf,
     double2* __restrict__ erow, int nsplit, Status* st, const int* __restrict__ units, const int* __restrict__ nunits,
     int* __restrict__ blkrow) {
   pdl_wait();
@@ -1687,19 +1711,18 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   if (__any_sync(0xffffffffu, bad) && lane == 0) S.bad = 1;
   __syncthreads();
   if (threadIdx.x == 0 && S.bad) set_flag(st, ST_RANGE);
-  unsigned long long* gf[3] = {sfx, sfy, sfz};
   bool wide = false;
-  for (int t = threadIdx.x; t < W; t += blockDim.x) {
+  // lanes over (slot, component): a warp's reductions cover consecutive words
+  // of the force records
+  for (int u = threadIdx.x; u < 3 * W; u += blockDim.x) {
+    const int t = u / 3, c = u - 3 * t;
     const int j = sinfo[t].x;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int b = fb[c * window_cap + t];
-      // the high word wraps mod 2^32 at |F| = 2^16 kcal/mol/A: a slot's
-      // accumulated F_j beyond half of that (|B| > 2^30) is flagged too
-      wide |= b > (1 << 30) || b < -(1 << 30);
-      const long long v = ((long long)b << 20) + (long long)fa[c * window_cap + t];
-      if (v != 0) atomicAdd(&gf[c][j], (unsigned long long)v);
-    }
+    const int b = fb[c * window_cap + t];
+    // the high word wraps mod 2^32 at |F| = 2^16 kcal/mol/A: a slot's
+    // accumulated F_j beyond half of that (|B| > 2^30) is flagged too
+    wide |= b > (1 << 30) || b < -(1 << 30);
+    const long long v = ((long long)b << 20) + (long long)fa[c * window_cap + t];
+    if (v != 0) atomicAdd(sf + 3 * (int64_t)j + c, (unsigned long long)v);
   }
   if (wide) set_flag(st, ST_RANGE);
 #ifdef REAX_TIMELINE
@@ -1731,14 +1754,13 @@ __device__ __forceinline__ void fin_block_sum(double& a, double& b, double (*red
   }
 }
 __global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __restrict__ iperm,
-    const unsigned long long* __restrict__ sfx, const unsigned long long* __restrict__ sfy,
-    const unsigned long long* __restrict__ sfz, double* __restrict__ force, int nparts,
+    const unsigned long long* __restrict__ sf, double* __restrict__ force, int nparts,
     const double2* __restrict__ epart, double* __restrict__ part, unsigned* __restrict__ ticket,
     double* __restrict__ energy, int ne, Status* st) {
   TL_SPAN(6);
   pdl_wait();
   pdl_trigger();
-  // input order: gathered (scattered 8-byte reads) and written as coalesced
+  // input order: gathered (one scattered 24-byte record per atom) and written as coalesced
   // 24-byte rows (scattered partial-sector writes cost read-modify-writes in
   // DRAM); the accumulators are zeroed by the next gather (k_cell_gather /
   // k_nb_prep), not here
@@ -1747,8 +1769,9 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(int n, const int* __re
     const int s = iperm[i];
     const double sc = 0x1.0p-35;
     static_assert(FIX_BITS == 35, "scale");
-    const double fx = (double)(long long)__ldcs(sfx + s) * sc, fy = (double)(long long)__ldcs(sfy + s) * sc,
-                 fz = (double)(long long)__ldcs(sfz + s) * sc;
+    const unsigned long long* r = sf + 3 * (int64_t)s;
+    const double fx = (double)(long long)__ldcs(r) * sc, fy = (double)(long long)__ldcs(r + 1) * sc,
+                 fz = (double)(long long)__ldcs(r + 2) * sc;
     force[3 * (int64_t)i] = fx;
     force[3 * (int64_t)i + 1] = fy;
     force[3 * (int64_t)i + 2] = fz;
@@ -1835,8 +1858,8 @@ __global__ void k_bond_energy_terms(const int* __restrict__ perm, const int* __r
     const BEPair& q = sbe[ta * nt + tb];
     double d[3];
     const double r = bond_vec(spos[s], spos[j], g, d);
-    const double* raw = bo + 8 * e;
-    const double bpi = raw[1], bpp = raw[2], bp = raw[3];
+    const double raw[3] = {bo[e], bo[bond_cap + e], bo[2 * bond_cap + e]};
+    const double bpi = raw[1], bpp = raw[2], bp = bo[3 * bond_cap + e];
     const double2 da = delta[s], db = delta[j];
     // B4-B8 (as k_bond_correct) and the derivative of every factor
     const double ea1 = exp(-p1 * da.x), eb1 = exp(-p1 * db.x);
@@ -1996,11 +2019,11 @@ __global__ void k_ang_count(const int* __restrict__ brow, const int* __restrict_
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
     const int s = bown[e];
     const int f0 = brow[s], f1 = brow[s + 1];
-    const double be = bo[8 * e + 4];
+    const double be = bo[4 * bond_cap + e];
     int c = 0;
     if (be > il.thb_cut)
       for (int f = f0; f < f1; ++f) {
-        const double bf = bo[8 * (long long)f + 4];
+        const double bf = bo[4 * bond_cap + f];
         c += (f != e && bf > il.thb_cut && be * bf > il.thb_cutsq);
       }
     if (acnt) acnt[orow[perm[s]] + (e - f0)] = c;
@@ -2022,11 +2045,11 @@ __global__ void k_ang_fill(const int* __restrict__ brow, const int* __restrict__
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < B; e += (long long)gridDim.x * blockDim.x) {
     const int s = bown[e];
     const int f0 = brow[s], f1 = brow[s + 1];
-    const double be = bo[8 * e + 4];
+    const double be = bo[4 * bond_cap + e];
     if (!(be > il.thb_cut)) continue;
     long long o = ang_off[orow[perm[s]] + (e - f0)];
     for (int f = f0; f < f1; ++f) {
-      const double bf = bo[8 * (long long)f + 4];
+      const double bf = bo[4 * bond_cap + f];
       if (f != e && bf > il.thb_cut && be * bf > il.thb_cutsq) ang_k[o++] = bkey[f];
     }
   }
@@ -2219,7 +2242,7 @@ __global__ void k_export_bond_deg(int n, const int* __restrict__ iperm, const in
 
 __global__ void k_export_bonds(int n, const int* __restrict__ iperm, const int* __restrict__ perm,
                                const int* __restrict__ brow, const int* __restrict__ bcol, const int* __restrict__ bmir,
-                               const double* __restrict__ bo, const double2* __restrict__ delta,
+                               const double* __restrict__ bo, long long bcap, const double2* __restrict__ delta,
                                const long long* __restrict__ orow, int64_t* __restrict__ out_row, int* __restrict__ out_col,
                                int* __restrict__ out_mir, double* __restrict__ out_bo, double* __restrict__ out_delta) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2237,7 +2260,7 @@ __global__ void k_export_bonds(int n, const int* __restrict__ iperm, const int* 
       out_mir[o] = (int)(orow[perm[j]] + (em - brow[j]));
     }
     if (out_bo)
-      for (int q = 0; q < 8; ++q) out_bo[8 * o + q] = bo[8 * (int64_t)e + q];
+      for (int q = 0; q < 8; ++q) out_bo[8 * o + q] = bo[q * bcap + e];
   }
   if (out_delta) {
     out_delta[2 * (int64_t)i] = delta[s].x;
@@ -2277,14 +2300,14 @@ __global__ void k_sp_init(int n, int* __restrict__ parent) {
 // one canonical entry (original i < j) per bond: unite(i, j) if BO > thr
 __global__ void k_sp_union(const int* __restrict__ brow, int n, const int* __restrict__ bown,
                            const int* __restrict__ bcol, const int* __restrict__ bkey, const int* __restrict__ perm,
-                           const int* __restrict__ stype, const double* __restrict__ bo, int nt, SpThr thr,
-                           int* parent) {
+                           const int* __restrict__ stype, const double* __restrict__ bo, long long bcap, int nt,
+                           SpThr thr, int* parent) {
   const int B = brow[n];
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < B; e += gridDim.x * blockDim.x) {
     const int so = bown[e];
     int a = perm[so], b = bkey[e];
     if (a >= b) continue;
-    if (!(bo[8 * (int64_t)e + 4] > thr.t[stype[so] * nt + stype[bcol[e]]])) continue;
+    if (!(bo[4 * bcap + e] > thr.t[stype[so] * nt + stype[bcol[e]]])) continue;
     for (;;) {
       a = sp_find(parent, a);
       b = sp_find(parent, b);

@@ -349,9 +349,7 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
   t.bmir = (int*)take(sizeof(int) * (size_t)c.bond_cap);
   t.bo = (double*)take(sizeof(double) * 8 * (size_t)c.bond_cap);
   t.delta = (double2*)take(sizeof(double2) * N);
-  t.sfx = (unsigned long long*)take(sizeof(long long) * N);
-  t.sfy = (unsigned long long*)take(sizeof(long long) * N);
-  t.sfz = (unsigned long long*)take(sizeof(long long) * N);
+  t.sf = (unsigned long long*)take(3 * sizeof(long long) * N);
   t.erow = (double2*)take(sizeof(double2) * std::max<size_t>(N, (size_t)g.nblock * MAX_SPLIT * NB_WARPS));
   t.epart = (double*)take(sizeof(double) * 2 * ((size_t)nblk((int64_t)std::max<int64_t>(N, 1), FIN_THREADS) + 1));   // k_finalize block partials
   t.ticket = (unsigned*)take(sizeof(unsigned) * 4);
@@ -685,9 +683,9 @@ void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, const do
     if (!fused_scan) scan1(c, w.cell_cnt, g.ncell, w.cell_start, w.lb_status, s);
     launch_k(c, k_scatter, nblk(N, TPB), TPB, 0, s, N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
     LAUNCH(c);
-    launch_k(c, k_cell_gather, nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s, g.ncell, w.cell_start, w.perm, pos, type, g, nt,
-                                                               w.iperm, w.spos, w.sloc, w.stype, q, w.st,
-             c->nb_plan ? w.blk_pairs : nullptr, g.nblock, w.sfx, w.sfy, w.sfz);
+    launch_k(c, k_cell_gather, nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s, g.ncell, w.cell_start, w.perm, pos, type, q, g,
+             nt, w.iperm, w.spos, w.sloc, w.stype, w.st,
+             c->nb_plan ? w.blk_pairs : nullptr, g.nblock, w.sf);
     LAUNCH(c);
   }
 }
@@ -718,10 +716,11 @@ void launch_bonds(reax_ctx* c, int N, cudaStream_t s) {
       N, w.spos, w.stype, g, w.prm, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.bdeg, w.lb_status, btiles);
   LAUNCH(c);
   scan1(c, w.bdeg, N, w.brow, w.lb_status, s);
-  launch_k(c, k_bond_fill, nblk(N, TPB), TPB, 0, s, N, w.bc, w.bc_len, w.bc_raw, c->cap.cand_cap, w.brow, w.perm, w.bdeg,
-                                          w.ucol, w.ukey, w.uown, w.uraw, c->cap.bond_cap, w.st);
+  launch_k(c, k_bond_fill, nblk(N, TPB), TPB, 0, s, N, w.bc, w.bc_len, c->cap.cand_cap, w.brow, w.perm, w.bdeg,
+                                          w.ucol, w.ukey, w.uown, reinterpret_cast<long long*>(w.uraw), c->cap.bond_cap, w.st);
   LAUNCH(c);
-  launch_k(c, k_bond_rank, 148 * 4, TPB, 0, s, w.brow, w.ucol, w.ukey, w.uown, w.uraw, w.bcol, w.bkey, w.bown, w.bo,
+  launch_k(c, k_bond_rank, 148 * 4, TPB, 0, s, w.brow, w.ucol, w.ukey, w.uown,
+           reinterpret_cast<const long long*>(w.uraw), (const double4*)w.bc_raw, w.bcol, w.bkey, w.bown, w.bo,
                                      c->cap.bond_cap, w.st);
   LAUNCH(c);
   launch_k(c, k_bond_delta, nblk(N, TPB), TPB, 0, s, N, w.brow, w.stype, w.prm, w.bo, w.delta, c->cap.bond_cap);
@@ -797,7 +796,7 @@ void launch_nb(reax_ctx* c, int nt, cudaStream_t s) {
   Timer t(c, 4, s);
   launch_k(c, k_nonbonded, c->nb_plan ? c->nb_umax : g.nblock * c->nsplit, NB_THREADS,
            nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s, g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len,
-           c->cap.row_cap, c->cap.window_cap, w.sfx, w.sfy, w.sfz, w.erow, c->nsplit, w.st,
+           c->cap.row_cap, c->cap.window_cap, w.sf, w.erow, c->nsplit, w.st,
            c->nb_plan ? (const int*)w.units : nullptr, c->nb_plan ? (const int*)w.nunits : nullptr, w.blkrow);
   LAUNCH(c);
 }
@@ -807,7 +806,7 @@ void launch_finalize(reax_ctx* c, int N, double* force, double* energy, cudaStre
   WS& w = c->w;
   Timer t(c, 5, s);
   // one energy partial per half-list row (sorted order), summed in fixed order
-  launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.iperm, w.sfx, w.sfy, w.sfz, force, N,
+  launch_k(c, k_finalize, nblk(N, FIN_THREADS), FIN_THREADS, 0, s, N, w.iperm, w.sf, force, N,
            w.erow, w.epart, w.ticket, energy, 2, w.st);
   LAUNCH(c);
 }
@@ -818,7 +817,7 @@ void launch_nonbonded(reax_ctx* c, int N, const double* q, double* force, double
   WS& w = c->w;
   if (q) {
     Timer t(c, 5, s);
-    launch_k(c, k_nb_prep, nblk(N, TPB), TPB, 0, s, N, q, w.perm, w.spos, w.sfx, w.sfy, w.sfz, w.st);
+    launch_k(c, k_nb_prep, nblk(N, TPB), TPB, 0, s, N, q, w.perm, w.spos, w.sf, w.st);
     LAUNCH(c);
   }
   launch_nb(c, nt, s);
@@ -1107,7 +1106,8 @@ reax_status do_species(reax_ctx* c, const double* thresh, void* scratch, size_t 
       return fail_cuda(cudaGetLastError());
     k_sp_init<<<nblk(N, TPB), TPB, 0, s>>>(N, parent);
     LAUNCH(c);
-    k_sp_union<<<148 * 8, TPB, 0, s>>>(w.brow, N, w.bown, w.bcol, w.bkey, w.perm, w.stype, w.bo, nt, thr, parent);
+    k_sp_union<<<148 * 8, TPB, 0, s>>>(w.brow, N, w.bown, w.bcol, w.bkey, w.perm, w.stype, w.bo, c->cap.bond_cap, nt,
+                                        thr, parent);
     LAUNCH(c);
     k_sp_count<<<nblk(N, TPB), TPB, 0, s>>>(N, w.perm, w.stype, nt, parent, isroot, comp);
     LAUNCH(c);
@@ -1521,9 +1521,7 @@ reax_status reax_bind_workspace(reax_ctx* ctx, void* ws, size_t bytes, int64_t n
   if (e == cudaSuccess) e = cudaMemset(ctx->w.bdeg, 0, sizeof(int) * (std::max<int64_t>(n, 1) + 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.st, 0, sizeof(Status));
   // fixed-point force accumulators: zeroed by every gather (k_cell_gather, k_nb_prep) before a nonbonded pass
-  if (e == cudaSuccess) e = cudaMemset(ctx->w.sfx, 0, sizeof(long long) * std::max<int64_t>(n, 1));
-  if (e == cudaSuccess) e = cudaMemset(ctx->w.sfy, 0, sizeof(long long) * std::max<int64_t>(n, 1));
-  if (e == cudaSuccess) e = cudaMemset(ctx->w.sfz, 0, sizeof(long long) * std::max<int64_t>(n, 1));
+  if (e == cudaSuccess) e = cudaMemset(ctx->w.sf, 0, 3 * sizeof(long long) * std::max<int64_t>(n, 1));
   if (e == cudaSuccess) e = cudaMemset(ctx->w.ticket, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaMemset(ctx->w.lb_ticket, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess) e = cudaMemset(ctx->w.bin_ticket, 0, sizeof(unsigned) * 4);
@@ -1839,7 +1837,7 @@ reax_status reax_export_bonds(reax_ctx* ctx, int64_t* brow, int32_t* bcol, int32
   // original-order row offsets; bc_len is free scratch outside a step
   k_export_bond_deg<<<nblk(N, TPB), TPB, 0, s>>>(N, w.iperm, w.brow, w.bc_len);
   if (scan<int, long long>(ctx, w.bc_len, N, w.exp_off, s) != cudaSuccess) return REAX_ERR_CUDA;
-  k_export_bonds<<<nblk(N + 1, TPB), TPB, 0, s>>>(N, w.iperm, w.perm, w.brow, w.bcol, w.bmir, w.bo, w.delta,
+  k_export_bonds<<<nblk(N + 1, TPB), TPB, 0, s>>>(N, w.iperm, w.perm, w.brow, w.bcol, w.bmir, w.bo, ctx->cap.bond_cap, w.delta,
                                                  w.exp_off, brow, bcol, mirror, bo, delta);
   if (cudaError_t e_ = cudaGetLastError()) return fail_cuda(e_);
   if (cudaError_t e_ = cudaStreamSynchronize(s)) return fail_cuda(e_);
