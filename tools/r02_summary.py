@@ -96,6 +96,21 @@ def main():
           f"warps active {q['warps_active_pct']:.1f}%.", "",
           "Launch list of the bench step: `r02_launches_c4.csv` (ncu --metrics gpu__time_duration.sum --clock-control "
           "none; cold, serialised).", "",
+          "Binning, bond chain and finalize at c4 (`r02_ncu_full_chain_c4.ncu-rep`, one cold launch each):", "",
+          "| kernel | cold ms | issue active | warps active | DRAM bytes | DRAM % of peak |", "|---|---|---|---|---|---|"]
+    chain = {}
+    for k in ("k_cell_gather", "k_bond_eval", "k_bond_fill", "k_bond_rank", "k_bond_delta", "k_bond_correct",
+              "k_finalize"):
+        try:
+            e = entry("profiles/r02_ncu_full_chain_c4.ncu-rep", k)
+        except KeyError:
+            continue
+        chain[k] = e
+        L.append(f"| {k} | {e['duration_us_cold'] / 1000:.3f} | {e['issue_active_pct']:.1f}% | "
+                 f"{e['warps_active_pct']:.1f}% | {e['dram_bytes_per_launch'] / 1e9:.2f} GB | {e['dram_pct_of_peak']:.1f}% |")
+    s["c4"]["chain"] = chain
+    json.dump(s, open(summ_path, "w"), indent=1)
+    L += ["",
           "Rejected list-build variants and the reasons are in DESIGN.md §6 (k_nbr_build in round 2)."]
     open(os.path.join(ROOT, "profiles", "r02_summary.md"), "w").write("\n".join(L) + "\n")
     print("\n".join(L))
