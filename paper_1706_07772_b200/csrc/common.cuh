@@ -80,8 +80,8 @@ struct DevParams {
   double val[NT_MAX], val_boc[NT_MAX];
   NBPair nb[NTP_MAX];
   BOPair bo[NTP_MAX];
-  double exp_tbl[64];        // 2^(j/64)
-  double log_tbl[2 * 128];   // {1/c_j rounded, -log(that value)}, c_j = 1 + (j + 1/2)/128
+  double exp_tbl[256];       // 2^(j/256)
+  double log_tbl[2 * 256];   // {1/c_j rounded, -log(that value)}, c_j = 1 + (j + 1/2)/256
 };
 
 // ------------------------------------------------------------------ status

@@ -907,15 +907,15 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
 
 // ---- branch-free fp64 math for the nonbonded pair (inputs in known, finite,
 // normal ranges; ~1-2 ulp).  Tables live in shared memory.
-constexpr int EXP_TBL = 64;    // 2^(j/64)
+constexpr int EXP_TBL = 256;   // 2^(j/256)
 // polynomial / reduction constants as constant-bank operands (ptxas otherwise
 // re-materialises 64-bit literals with register moves inside the pair loop)
 __constant__ double c_nb[28] = {
-    0x1.71547652b82fep+6,      // 0  64 / ln 2
+    0x1.71547652b82fep+8,      // 0  256 / ln 2
     6755399441055744.0,        // 1  1.5 * 2^52
-    0x1.62e42fee00000p-7,      // 2  ln2_hi / 64
-    0x1.a39ef35793c76p-39,     // 3  ln2_lo / 64
-    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5,   // 4-7  exp polynomial
+    0x1.62e42fee00000p-9,      // 2  ln2_hi / 256
+    0x1.a39ef35793c76p-41,     // 3  ln2_lo / 256
+    0.0, 1.0 / 24.0, 1.0 / 6.0, 0.5,   // 4-7  exp polynomial (4 unused)
     -1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5,   // 8-12 log1p polynomial
     0x1.62e42fee00000p-1,      // 13 ln2_hi
     0x1.a39ef35793c76p-33,     // 14 ln2_lo
@@ -927,36 +927,34 @@ __constant__ double c_nb[28] = {
     6755399441055744.0,        // 26 1.5 * 2^52 (round-to-integer magic)
     65536.0};                  // 27 fixed-point range limit per contribution
 
-constexpr int LOG_TBL = 128;   // {1/c_j, -log(1/c_j)}, c_j = 1 + (j + 1/2)/128
+constexpr int LOG_TBL = 256;   // {1/c_j, -log(1/c_j)}, c_j = 1 + (j + 1/2)/256
 
-// e^x for |x| < 700: x = k ln2/64 + r, |r| <= ln2/128; e^r - 1 by a degree-5
-// polynomial (error r^6/720 < 4e-17); 2^(k/64) = 2^(k>>6) * T[k & 63].
+// e^x for |x| < 700: x = k ln2/256 + r, |r| <= ln2/512; e^r - 1 by a degree-4
+// polynomial (error r^5/120 < 4e-17); 2^(k/256) = 2^(k>>8) * T[k & 255].
 __device__ __forceinline__ double fexp(double x, const double* __restrict__ T) {
   double t = fma(x, c_nb[0], c_nb[1]);
   double kd = t - c_nb[1];
   int k = __double2loint(t);
   double r = fma(kd, -c_nb[2], x);
   r = fma(kd, -c_nb[3], r);
-  double q = fma(r, c_nb[4], c_nb[5]);
-  q = fma(q, r, c_nb[6]);
+  double q = fma(r, c_nb[5], c_nb[6]);
   q = fma(q, r, c_nb[7]);
   double p = fma(q, r * r, r);
   double tj = T[k & (EXP_TBL - 1)];
   double y = fma(tj, p, tj);
-  return __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
+  return __hiloint2double(__double2hiint(y) + ((k >> 8) << 20), __double2loint(y));
 }
 
 // ln x for finite normal x > 0: x = 2^e m, m in [1,2); m/c_j = 1 + r with
-// |r| < 2^-8; log1p(r) by a degree-6 polynomial (error < 3e-18).
+// |r| < 2^-9; log1p(r) by a degree-5 polynomial (error r^6/6 < 1e-17).
 __device__ __forceinline__ double flog(double x, const double2* __restrict__ LT) {
   int hi = __double2hiint(x);
   int e = (hi >> 20) - 1023;
-  int j = (hi >> 13) & (LOG_TBL - 1);
+  int j = (hi >> 12) & (LOG_TBL - 1);
   double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(x));
   double2 t = LT[j];
   double r = fma(m, t.x, -c_nb[23]);
-  double q = fma(r, c_nb[8], c_nb[9]);
-  q = fma(q, r, c_nb[10]);
+  double q = fma(r, c_nb[9], c_nb[10]);
   q = fma(q, r, c_nb[11]);
   q = fma(q, r, c_nb[12]);
   double p = fma(q, r * r, r);

@@ -236,9 +236,9 @@ reax_status build_params(const reax_params* p, const reax_cutoffs* cut, DevParam
     d.val_boc[t] = p->val_boc[t];
   }
   // tables of the nonbonded's exp/log (x86 long double: 64-bit mantissa)
-  for (int j = 0; j < 64; ++j) d.exp_tbl[j] = (double)exp2l((long double)j / 64.0L);
-  for (int j = 0; j < 128; ++j) {
-    long double cj = 1.0L + ((long double)j + 0.5L) / 128.0L;
+  for (int j = 0; j < EXP_TBL; ++j) d.exp_tbl[j] = (double)exp2l((long double)j / (long double)EXP_TBL);
+  for (int j = 0; j < LOG_TBL; ++j) {
+    long double cj = 1.0L + ((long double)j + 0.5L) / (long double)LOG_TBL;
     double inv = (double)(1.0L / cj);
     d.log_tbl[2 * j] = inv;
     d.log_tbl[2 * j + 1] = (double)(-logl((long double)inv));
