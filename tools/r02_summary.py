@@ -96,14 +96,19 @@ def main():
           f"warps active {q['warps_active_pct']:.1f}%.", "",
           "Launch list of the bench step: `r02_launches_c4.csv` (ncu --metrics gpu__time_duration.sum --clock-control "
           "none; cold, serialised).", "",
-          "Binning, bond chain and finalize at c4 (`r02_ncu_full_chain_c4.ncu-rep`, one cold launch each):", "",
+          "Binning, bond chain and finalize at c4 (`r02_ncu_full_chain_c4.ncu-rep`, `r02_ncu_full_chain2_c4.ncu-rep`; one cold launch each):", "",
           "| kernel | cold ms | issue active | warps active | DRAM bytes | DRAM % of peak |", "|---|---|---|---|---|---|"]
     chain = {}
     for k in ("k_cell_gather", "k_bond_eval", "k_bond_fill", "k_bond_rank", "k_bond_delta", "k_bond_correct",
               "k_finalize"):
-        try:
-            e = entry("profiles/r02_ncu_full_chain_c4.ncu-rep", k)
-        except KeyError:
+        e = None
+        for rep in ("profiles/r02_ncu_full_chain_c4.ncu-rep", "profiles/r02_ncu_full_chain2_c4.ncu-rep"):
+            try:
+                e = entry(rep, k)
+                break
+            except KeyError:
+                continue
+        if e is None:
             continue
         chain[k] = e
         L.append(f"| {k} | {e['duration_us_cold'] / 1000:.3f} | {e['issue_active_pct']:.1f}% | "
