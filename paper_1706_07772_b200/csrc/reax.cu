@@ -447,10 +447,12 @@ struct reax_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool serial = getenv("REAX_SERIAL") != nullptr;
   bool pdl = getenv("REAX_NO_PDL") == nullptr;   // programmatic dependent launch on the hot path
-  // REAX_CHAIN_PRIO=1 (measurement): the side-stream bond chain at the greatest stream priority
-  // (c4 82.74 -> 82.44 ms, c1 0.2335 -> 0.2619 ms: off by default)
-  bool chain_prio_on = getenv("REAX_CHAIN_PRIO") && atoi(getenv("REAX_CHAIN_PRIO")) != 0;
-  int chain_prio = 0;
+  // the side-stream bond chain's kernels at the device's greatest priority for
+  // large grids (no nonbonded work plan: c4 77.32 -> 77.07 ms), the default
+  // priority for small ones (c1 0.227 -> 0.243 ms with it); REAX_CHAIN_PRIO=0/1
+  // forces it off/on (measurement)
+  int chain_prio_env = getenv("REAX_CHAIN_PRIO") ? (atoi(getenv("REAX_CHAIN_PRIO")) != 0 ? 1 : 0) : -1;
+  int prio_hi = 0, prio_lo = 0;   // the device's greatest and least stream priorities
 };
 
 namespace {
@@ -528,9 +530,10 @@ void launch_k(reax_ctx* c, void (*k)(KArgs...), int grid, int block, size_t smem
   at[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (s == c->side && c->chain_prio != 0) {   // kept by graph capture as the kernel node's priority
+  if (s == c->side) {   // kept by graph capture as the kernel node's priority
+    const bool hi = c->chain_prio_env == 1 || (c->chain_prio_env < 0 && c->g.nblock > NB_PLAN_MAX);
     at[1].id = cudaLaunchAttributePriority;
-    at[1].val.priority = c->chain_prio;
+    at[1].val.priority = hi ? c->prio_hi : c->prio_lo;
     cfg.numAttrs = 2;
   }
   cudaLaunchKernelEx(&cfg, k, args...);
@@ -1403,8 +1406,10 @@ reax_status reax_create(reax_ctx** out) {
   memset(c->h_st, 0, sizeof(Status));
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  c->chain_prio = c->chain_prio_on ? prio_hi : 0;
-  bool ok = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, c->chain_prio) == cudaSuccess &&
+  c->prio_hi = prio_hi;
+  c->prio_lo = prio_lo;
+  // the side stream at the greatest priority; its kernels carry their own (launch attribute)
+  bool ok = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->cap_s, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) == cudaSuccess;
