@@ -629,7 +629,8 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
                                                  const double4* __restrict__ spos, int si0, int nrow, int h,
                                                  const RowTest& rt, uint16_t* __restrict__ nbr, int row_cap,
                                                  int* __restrict__ bc, int cand_cap, const float* __restrict__ rc2,
-                                                 int nt, float rcmax, int* ncs, int (&len)[NBR_G]) {
+                                                 int nt, float rcmax, int* ncs, int (&len)[NBR_G],
+                                                 const double* __restrict__ R2p) {
   constexpr int G = NBR_G;
   const int lane = threadIdx.x & 31;
   if (lane < G) ncs[lane] = 0;   // per-row bond-candidate counters (shared, this warp's)
@@ -747,7 +748,7 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
           const double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), sw.y);
           const double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), sw.z);
           const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
-          in = d2 <= rt.R2;
+          in = d2 <= *R2p;   // read here: one live register pair less in the loop
         } else if (in && r2v[r] <= rc2[__float_as_int(cand[si0 + r].w) * nt + tj]) {
           const int pc = atomicAdd(ncs + r, 1);   // per-lane append, no warp vote
           if (pc < cand_cap) bc[(int64_t)cand_j[si0 + r] * cand_cap + pc] = cand_j[slot];
@@ -873,7 +874,7 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
     const int si0 = S.W.slot[kh] + a0;
     int len[NBR_G], nc[NBR_G];
     nbr_group_stream(S.W, S.run[h], W, cand, cand_j, cand_k, spos, si0, nrow, h, rt, nbr, row_cap, bc, cand_cap,
-                     S.rcand2, nt, rcmax, S.ncs[threadIdx.x >> 5], len);
+                     S.rcand2, nt, rcmax, S.ncs[threadIdx.x >> 5], len, &prm->R2);
 #pragma unroll
     for (int r = 0; r < NBR_G; ++r) nc[r] = S.ncs[threadIdx.x >> 5][r];
     if (lane < nrow) {
