@@ -706,8 +706,9 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
   const int total = __shfl_sync(0xffffffffu, inc, 15);
   const int excl = inc - il;
   const int shift = ia - excl;   // slot = p + shift inside the lane's interval
-  // own-cell partners of row r: slots after si0 + r only (tself > thr0 + r)
-  const unsigned thr0 = (unsigned)(si0 - ownlo);
+  // own-cell partners of row r: slots after si0 + r only.  The stream holds
+  // the own cell from si0 + 1 on, so the only slots to exclude for row r are
+  // the group's rows si0 + 1 .. si0 + r: ok(r) <=> (unsigned)(slot - si0 - 1) >= r
   const unsigned cand_s = (unsigned)__cvta_generic_to_shared(cand);
   for (int p0 = 0; p0 < total; p0 += 32) {
     const int p = p0 + lane;
@@ -718,7 +719,7 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
     const int sh = __shfl_sync(0xffffffffu, shift, q);
     const int slot = p < total ? p + sh : Wslots;   // Wslots: sentinel at 1e30
     const float4 c = lds_f4(cand_s + 16u * (unsigned)slot);
-    const unsigned tself = (unsigned)(slot - ownlo);
+    const unsigned tself = (unsigned)(slot - si0 - 1);
     float r2v[G];
     unsigned mk[G];
     bool rare = false;
@@ -726,7 +727,7 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
     for (int r = 0; r < G; ++r) {
       const float dx = c.x - rx[r], dy = c.y - ry[r], dz = c.z - rz[r];
       r2v[r] = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const bool ok = tself > thr0 + r;
+      const bool ok = tself >= (unsigned)r;
       mk[r] = __ballot_sync(0xffffffffu, ok & (r2v[r] < rt.R2lo));
       // rare: inside the fp32 band around R^2 (settled exactly below) or a
       // possible bond candidate (rcmax < R2lo); bitwise, so no branches
@@ -736,7 +737,7 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
       const int tj = __float_as_int(c.w);
 #pragma unroll
       for (int r = 0; r < G; ++r) {
-        const bool ok = tself > thr0 + r;
+        const bool ok = tself >= (unsigned)r;
         bool in = ((mk[r] >> lane) & 1u) != 0u;
         if (ok && !in && fabsf(r2v[r] - rt.R2mid) <= rt.R2half) {
           // exact, FMA-free fp64 decision (bit-identical to the oracle's r^2)
