@@ -447,11 +447,12 @@ struct reax_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool serial = getenv("REAX_SERIAL") != nullptr;
   bool pdl = getenv("REAX_NO_PDL") == nullptr;   // programmatic dependent launch on the hot path
-  // the side-stream bond chain's kernels at the device's greatest priority for
-  // large grids (no nonbonded work plan: c4 77.32 -> 77.07 ms), the default
-  // priority for small ones (c1 0.227 -> 0.243 ms with it); REAX_CHAIN_PRIO=0/1
-  // forces it off/on (measurement)
-  int chain_prio_env = getenv("REAX_CHAIN_PRIO") ? (atoi(getenv("REAX_CHAIN_PRIO")) != 0 ? 1 : 0) : -1;
+  // REAX_CHAIN_PRIO (measurement): 1 = the side-stream bond chain's kernels at
+  // the device's greatest priority, -1 = that on grids without a nonbonded work
+  // plan only; default 0 (the default priority).  c4: the step 77.33 -> 77.08 ms
+  // with it, but the nonbonded kernel's span in the step 51.8 -> 56.2 ms (the
+  // chain's CTAs are dispatched ahead of its pending ones); c1 0.227 -> 0.243 ms
+  int chain_prio_env = getenv("REAX_CHAIN_PRIO") ? atoi(getenv("REAX_CHAIN_PRIO")) : 0;
   int prio_hi = 0, prio_lo = 0;   // the device's greatest and least stream priorities
 };
 
