@@ -571,23 +571,14 @@ struct NbrSmem {
   int pairs;                      // half-list entries of this CTA's rows (nonbonded work plan)
 };
 
-// Per-kernel constants of the half-list candidate test.
+// Per-kernel constants of the half-list candidate test, made on the host
+// (make_rowtest in reax.cu) and passed by value: the kernel reads them from the
+// constant bank, so they hold no registers in the chunk loop.
 struct RowTest {
   float R2lo, R2mid, R2half, Rt, hy, hz, ihx;   // band [R2lo, R2lo + 2 R2half] = [R2lo, R2hi]
+  float rcmax;                                  // largest bond-candidate radius^2 (fp32, conservative)
   double R2;
 };
-__device__ __forceinline__ RowTest make_rowtest(const DevParams* __restrict__ prm, const Grid& g) {
-  RowTest t;
-  t.R2lo = prm->R2lo;
-  t.R2mid = 0.5f * (prm->R2lo + prm->R2hi);
-  t.R2half = 0.5f * (prm->R2hi - prm->R2lo);
-  t.Rt = sqrtf(prm->R2hi) + 1e-3f;                 // trimming radius (conservative)
-  t.hy = (float)g.h[1];
-  t.hz = (float)g.h[2];
-  t.ihx = 1.0f / (float)g.h[0];
-  t.R2 = prm->R2;
-  return t;
-}
 #ifndef NBR_GROUP
 #define NBR_GROUP 3   // measured at 4 CTAs/SM, 64 registers (c4): 3 rows 18.13 ms, 2 rows 18.53, 4 rows 18.84 (spills)
 #endif
@@ -629,8 +620,7 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
                                                  const double4* __restrict__ spos, int si0, int nrow, int h,
                                                  const RowTest& rt, uint16_t* __restrict__ nbr, int row_cap,
                                                  int* __restrict__ bc, int cand_cap, const float* __restrict__ rc2,
-                                                 int nt, float rcmax, int* ncs, int (&len)[NBR_G],
-                                                 const double* __restrict__ R2p) {
+                                                 int nt, int* ncs, int (&len)[NBR_G]) {
   constexpr int G = NBR_G;
   const int lane = threadIdx.x & 31;
   if (lane < G) ncs[lane] = 0;   // per-row bond-candidate counters (shared, this warp's)
@@ -717,7 +707,7 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
     for (int step = 8; step >= 1; step >>= 1)
       if (__shfl_sync(0xffffffffu, excl, q + step) <= p) q += step;
     const int sh = __shfl_sync(0xffffffffu, shift, q);
-    const int slot = p < total ? p + sh : Wslots;   // Wslots: sentinel at 1e30
+    const int slot = p < total ? p + sh : Wslots;   // Wslots (window_cap, a kernel constant): sentinel at 1e30
     const float4 c = lds_f4(cand_s + 16u * (unsigned)slot);
     const unsigned tself = (unsigned)(slot - si0 - 1);
     float r2v[G];
@@ -731,7 +721,7 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
       mk[r] = __ballot_sync(0xffffffffu, ok & (r2v[r] < rt.R2lo));
       // rare: inside the fp32 band around R^2 (settled exactly below) or a
       // possible bond candidate (rcmax < R2lo); bitwise, so no branches
-      rare |= ok & ((fabsf(r2v[r] - rt.R2mid) <= rt.R2half) | (r2v[r] <= rcmax));
+      rare |= ok & ((fabsf(r2v[r] - rt.R2mid) <= rt.R2half) | (r2v[r] <= rt.rcmax));
     }
     if (__any_sync(0xffffffffu, rare)) {
       const int tj = __float_as_int(c.w);
@@ -749,7 +739,7 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
           const double ey = __dadd_rn(__dsub_rn(xj.y, xi.y), sw.y);
           const double ez = __dadd_rn(__dsub_rn(xj.z, xi.z), sw.z);
           const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
-          in = d2 <= *R2p;   // read here: one live register pair less in the loop
+          in = d2 <= rt.R2;
         } else if (in && r2v[r] <= rc2[__float_as_int(cand[si0 + r].w) * nt + tj]) {
           const int pc = atomicAdd(ncs + r, 1);   // per-lane append, no warp vote
           if (pc < cand_cap) bc[(int64_t)cand_j[si0 + r] * cand_cap + pc] = cand_j[slot];
@@ -777,7 +767,8 @@ __device__ __forceinline__ void nbr_group_stream(const WinSmem& W, const RunInfo
 __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, const int* __restrict__ cell_start,
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
-    int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st, int* __restrict__ blk_pairs) {
+    int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st, int* __restrict__ blk_pairs,
+    const RowTest rt) {
   pdl_wait();
   TL_MARK(0, 0);
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -803,8 +794,6 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
       S.run[h][q] = ru;
     }
   }
-  const float rcmax = prm->rcand2_max;
-  const RowTest rt = make_rowtest(prm, g);
   int W = build_window(S.W, blk, g, cell_start);
   const int nwu = c_win.nwu;
   const int lane = threadIdx.x & 31;
@@ -855,7 +844,7 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
     cand[t] = make_float4(l.x + ox, l.y + oy, l.z + oz, l.w);
     cand_j[t] = j;
   }
-  if (threadIdx.x < 32) cand[W + threadIdx.x] = make_float4(1e30f, 1e30f, 1e30f, 0.f);  // sentinel
+  if (threadIdx.x < 32) cand[window_cap + threadIdx.x] = make_float4(1e30f, 1e30f, 1e30f, 0.f);   // sentinel
   __syncthreads();
   TL_MARK(0, 1, W);
   // groups of NBR_G consecutive rows of one home sub-cell; this CTA takes
@@ -874,8 +863,8 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
     const int nrow = min(NBR_G, S.W.cnt[kh] - a0);
     const int si0 = S.W.slot[kh] + a0;
     int len[NBR_G], nc[NBR_G];
-    nbr_group_stream(S.W, S.run[h], W, cand, cand_j, cand_k, spos, si0, nrow, h, rt, nbr, row_cap, bc, cand_cap,
-                     S.rcand2, nt, rcmax, S.ncs[threadIdx.x >> 5], len, &prm->R2);
+    nbr_group_stream(S.W, S.run[h], window_cap, cand, cand_j, cand_k, spos, si0, nrow, h, rt, nbr, row_cap, bc, cand_cap,
+                     S.rcand2, nt, S.ncs[threadIdx.x >> 5], len);
 #pragma unroll
     for (int r = 0; r < NBR_G; ++r) nc[r] = S.ncs[threadIdx.x >> 5][r];
     if (lane < nrow) {

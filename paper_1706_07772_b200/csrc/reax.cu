@@ -694,6 +694,21 @@ void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, const do
   }
 }
 
+// constants of the list build's candidate test (fp32 as the kernel would compute them)
+RowTest make_rowtest(const DevParams& p, const Grid& g) {
+  RowTest t;
+  t.R2lo = p.R2lo;
+  t.R2mid = 0.5f * (p.R2lo + p.R2hi);
+  t.R2half = 0.5f * (p.R2hi - p.R2lo);
+  t.Rt = sqrtf(p.R2hi) + 1e-3f;   // trimming radius (conservative)
+  t.hy = (float)g.h[1];
+  t.hz = (float)g.h[2];
+  t.ihx = 1.0f / (float)g.h[0];
+  t.rcmax = p.rcand2_max;
+  t.R2 = p.R2;
+  return t;
+}
+
 // a3-a4: the half list and the bond candidates
 void launch_nbr(reax_ctx* c, cudaStream_t s) {
   const Grid& g = c->g;
@@ -701,7 +716,8 @@ void launch_nbr(reax_ctx* c, cudaStream_t s) {
   Timer t(c, 1, s);
   launch_k(c, k_nbr_build, g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s,
            g, w.cell_start, w.sloc, w.spos, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, w.bc, w.bc_len,
-           c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st, c->nb_plan ? w.blk_pairs : nullptr);
+           c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st, c->nb_plan ? w.blk_pairs : nullptr,
+           make_rowtest(*c->h_prm, g));
   LAUNCH(c);
 }
 
