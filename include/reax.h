@@ -268,7 +268,14 @@ reax_status reax_step(reax_ctx* ctx, int64_t n, const double* pos, const int32_t
 
 /* reax_step with HOST buffers: pos/type/q [host], force [host] n*3,
  * energy [host] 2.  Copies in, runs the step, copies out and synchronises
- * `stream`.  Host buffers should be pinned for full copy bandwidth. */
+ * `stream`.  Host buffers should be pinned for full copy bandwidth.  The
+ * input copies run on a context-owned copy stream in the order positions,
+ * types, charges; the step waits for each array only where it first needs
+ * it (binning: positions; cell gather: types; nonbonded kernel: charges), so
+ * the type and charge copies overlap the binning and the list build.  The
+ * host buffers must stay unchanged until the call returns.  The whole
+ * sequence is captured into a CUDA graph and replayed while the buffers,
+ * box and parameters stay the same. */
 reax_status reax_step_host(reax_ctx* ctx, int64_t n, const double* pos, const int32_t* type,
                            const double* q, const double box[3], const reax_params* params,
                            const reax_cutoffs* cut, double* force, double* energy, void* stream);

@@ -288,8 +288,10 @@ __global__ void __launch_bounds__(256) k_bin(int n, const double* __restrict__ p
       c[k] = ck >= g.nc[k] ? g.nc[k] - 1 : ck;
     }
     if (bad) set_flag(st, ST_NONFINITE_IN);
-    int t = type[i];
-    if (t < 0 || t >= nt) set_flag(st, ST_TYPE);
+    if (type) {   // else checked by the cell gather (reax_step_host: the types arrive later)
+      int t = type[i];
+      if (t < 0 || t >= nt) set_flag(st, ST_TYPE);
+    }
     int cid = (c[2] * g.nc[1] + c[1]) * g.nc[0] + c[0];
     cell_of[i] = cid;
     atomicAdd(&cell_cnt[cid], 1);
@@ -373,7 +375,10 @@ __device__ __forceinline__ void gather_one(int sp, int i, const double4& v, int 
     w[d] = isfinite(x[d]) ? wrap_coord(x[d], g.L[d]) : 0.0;
     l[d] = (float)(w[d] - cc[d] * g.h[d]);
   }
-  t = (t < 0 || t >= nt) ? 0 : t;   // flagged by k_bin; clamp keeps every table index valid
+  if (t < 0 || t >= nt) {   // flagged (also by k_bin when it had the types); clamp keeps every table index valid
+    set_flag(st, ST_TYPE);
+    t = 0;
+  }
   const double qs = has_q ? v.w : 0.0;   // reax_step: charges staged by k_scatter (reax_nonbonded: k_nb_prep)
   if (has_q && !isfinite(qs)) set_flag(st, ST_NONFINITE_IN);
   perm[sp] = i;
@@ -1219,6 +1224,19 @@ __global__ void k_bond_correct(const int* __restrict__ brow, const int* __restri
 }
 
 // ====================================================== a7-a8 nonbonded
+// reax_step_host: the charges gathered into the sorted records after their
+// host-to-device copy (the cell gather ran without them)
+__global__ void k_q_gather(int n, const double* __restrict__ q, const int* __restrict__ perm, double4* __restrict__ spos,
+                           Status* st) {
+  pdl_wait();
+  pdl_trigger();
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double qs = q[perm[s]];
+  if (!isfinite(qs)) set_flag(st, ST_NONFINITE_IN);
+  spos[s].w = qs;
+}
+
 __global__ void k_nb_prep(int n, const double* __restrict__ q, const int* __restrict__ perm, double4* __restrict__ spos,
                           unsigned long long* __restrict__ sf, Status* st) {
   pdl_wait();

@@ -445,6 +445,12 @@ struct reax_ctx {
   cudaStream_t side = nullptr;
   cudaStream_t cap_s = nullptr;   // capture stream of the reax_step_host graph
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // reax_step_host: host-to-device copies on their own stream, so that the
+  // charges (needed only by the nonbonded kernel) and the types (needed from
+  // the cell gather on) arrive while the binning and the list build run
+  cudaStream_t copy_s = nullptr;
+  cudaEvent_t ev_in0 = nullptr, ev_pos = nullptr, ev_type = nullptr, ev_q = nullptr;
+  bool host_in = false;   // do_step: the inputs arrive through ev_pos / ev_type / ev_q
   bool serial = getenv("REAX_SERIAL") != nullptr;
   bool pdl = getenv("REAX_NO_PDL") == nullptr;   // programmatic dependent launch on the hot path
   // REAX_CHAIN_PRIO (measurement): 1 = the side-stream bond chain's kernels at
@@ -674,24 +680,38 @@ reax_status check_common(reax_ctx* c, int64_t n, const double box[3], const reax
 }
 
 // a1-a3: binning and the half list (+ bond candidates)
+// host_in (reax_step_host): k_bin waits for the positions only (the type
+// check moves to the cell gather), the cell gather for the types, and the
+// charges are gathered later (launch_q_gather), after their copy
 void launch_bin(reax_ctx* c, int N, const double* pos, const int* type, const double* q, int nt, cudaStream_t s) {
   const Grid& g = c->g;
   WS& w = c->w;
   {
+    if (c->host_in) cudaStreamWaitEvent(s, c->ev_pos, 0);
     Timer t(c, 0, s);
     const int ctiles = nblk(g.ncell, LB_TILE);
     const bool fused_scan = g.ncell <= BIN_FUSED_SCAN_MAX;
-    launch_k(c, k_bin, nblk(std::max<int64_t>(N, ctiles), TPB), TPB, 0, s, N, pos, type, g, nt, w.cell_of, w.cell_cnt,
-             w.st, w.lb_status, ctiles, fused_scan ? w.cell_start : nullptr, w.bin_ticket);
+    launch_k(c, k_bin, nblk(std::max<int64_t>(N, ctiles), TPB), TPB, 0, s, N, pos, c->host_in ? nullptr : type, g, nt,
+             w.cell_of, w.cell_cnt, w.st, w.lb_status, ctiles, fused_scan ? w.cell_start : nullptr, w.bin_ticket);
     LAUNCH(c);
     if (!fused_scan) scan1(c, w.cell_cnt, g.ncell, w.cell_start, w.lb_status, s);
     launch_k(c, k_scatter, nblk(N, TPB), TPB, 0, s, N, w.cell_of, w.cell_start, w.cell_cnt, w.perm);
     LAUNCH(c);
-    launch_k(c, k_cell_gather, nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s, g.ncell, w.cell_start, w.perm, pos, type, q, g,
-             nt, w.iperm, w.spos, w.sloc, w.stype, w.st,
+    if (c->host_in) cudaStreamWaitEvent(s, c->ev_type, 0);
+    launch_k(c, k_cell_gather, nblk((int64_t)g.ncell * 32, TPB), TPB, 0, s, g.ncell, w.cell_start, w.perm, pos, type,
+             c->host_in ? nullptr : q, g, nt, w.iperm, w.spos, w.sloc, w.stype, w.st,
              c->nb_plan ? w.blk_pairs : nullptr, g.nblock, w.sf);
     LAUNCH(c);
   }
+}
+
+// host_in: the charges into the sorted records once their copy has landed
+void launch_q_gather(reax_ctx* c, int N, const double* q, cudaStream_t s) {
+  WS& w = c->w;
+  cudaStreamWaitEvent(s, c->ev_q, 0);
+  Timer t(c, 5, s);
+  launch_k(c, k_q_gather, nblk(N, TPB), TPB, 0, s, N, q, w.perm, w.spos, w.st);
+  LAUNCH(c);
 }
 
 // constants of the list build's candidate test (fp32 as the kernel would compute them)
@@ -904,6 +924,7 @@ reax_status do_step(reax_ctx* c, int64_t n, const double* pos, const int* type, 
   }
   launch_bonds(c, N, sb);
   launch_bond_correct(c, sb);
+  if (c->host_in) launch_q_gather(c, N, q, s);
   launch_nb(c, nt, s);
   if (fork && (cudaEventRecord(c->ev_join, c->side) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join, 0) != cudaSuccess))
     return fail_cuda(cudaGetLastError());
@@ -1429,7 +1450,12 @@ reax_status reax_create(reax_ctx** out) {
   bool ok = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->cap_s, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-            cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) == cudaSuccess;
+            cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->copy_s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_in0, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_pos, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_type, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_q, cudaEventDisableTiming) == cudaSuccess;
   if (!ok) {
     reax_destroy(c);
     return REAX_ERR_CUDA;
@@ -1454,6 +1480,9 @@ reax_status reax_destroy(reax_ctx* c) {
   if (c->cap_s) cudaStreamDestroy(c->cap_s);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->copy_s) cudaStreamDestroy(c->copy_s);
+  for (cudaEvent_t e : {c->ev_in0, c->ev_pos, c->ev_type, c->ev_q})
+    if (e) cudaEventDestroy(e);
   delete c;
   return REAX_OK;
 }
@@ -1596,14 +1625,31 @@ reax_status step_host_enqueue(reax_ctx* ctx, int64_t n, const double* pos, const
                               const double box[3], const reax_params* params, const reax_cutoffs* cut, double* force,
                               cudaStream_t s) {
   WS& w = ctx->w;
+  // copies on the context's copy stream (positions, types, charges, each
+  // followed by an event the step waits on where it first needs the array),
+  // except in REAX_SERIAL mode; the step joins every event before it ends
+  const bool overlap = n > 0 && !ctx->serial;
+  cudaStream_t cs = overlap ? ctx->copy_s : s;
   if (n > 0) {
-    if (cudaMemcpyAsync(w.h_pos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(w.h_type, type, sizeof(int) * n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(w.h_q, q, sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    if (overlap && (cudaEventRecord(ctx->ev_in0, s) != cudaSuccess || cudaStreamWaitEvent(cs, ctx->ev_in0, 0) != cudaSuccess))
+      return fail_cuda(cudaGetLastError());
+    if (cudaMemcpyAsync(w.h_pos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        (overlap && cudaEventRecord(ctx->ev_pos, cs) != cudaSuccess) ||
+        cudaMemcpyAsync(w.h_type, type, sizeof(int) * n, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        (overlap && cudaEventRecord(ctx->ev_type, cs) != cudaSuccess) ||
+        cudaMemcpyAsync(w.h_q, q, sizeof(double) * n, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        (overlap && cudaEventRecord(ctx->ev_q, cs) != cudaSuccess))
       return fail_cuda(cudaGetLastError());
   }
+  ctx->host_in = overlap;
   reax_status r = reax_step(ctx, n, w.h_pos, w.h_type, w.h_q, box, params, cut, w.h_force, w.h_energy, s);
-  if (r != REAX_OK) return r;
+  ctx->host_in = false;
+  if (r != REAX_OK) {
+    if (overlap) {   // an early return may leave the copy stream unjoined: join it
+      cudaStreamWaitEvent(s, ctx->ev_q, 0);
+    }
+    return r;
+  }
   if (n > 0 && cudaMemcpyAsync(force, w.h_force, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return fail_cuda(cudaGetLastError());
   return REAX_OK;

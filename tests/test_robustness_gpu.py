@@ -111,3 +111,34 @@ def test_err_range_close_pair(params):
     with pytest.raises(rx.ReaxError) as ei:
         gpu_run(s, p)
     assert ei.value.code == rx.ERR_RANGE
+
+
+def test_step_host_overlapped_inputs(params):
+    """reax_step_host copies the inputs on its own stream (the types are first
+    needed by the cell gather, the charges by the nonbonded kernel): the
+    results equal the device-input step bitwise at c1, the checks that moved
+    with the inputs (type range in the cell gather, non-finite charges in the
+    charge gather) still report, and the context works afterwards."""
+    s = gen.make_config(1)
+    n = len(s.pos)
+    ctx = rx.Reax(n, s.box, params, CUT, device=DEV)
+    pos, typ, q = _host(s)
+    F = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    E = torch.empty(2, dtype=torch.float64).pin_memory()
+    Fd, Ed = ctx.step(pos.to(DEV), typ.to(DEV), q.to(DEV))
+    for _ in range(3):   # direct + capture, then graph replays
+        F.zero_()
+        ctx.step_host(pos, typ, q, F, E)
+        assert np.array_equal(F.numpy(), Fd.cpu().numpy()) and np.array_equal(E.numpy(), Ed.cpu().numpy())
+    bad = typ.clone().pin_memory()
+    bad[11] = params.ntypes + 2
+    with pytest.raises(rx.ReaxError) as e:
+        ctx.step_host(pos, bad, q, F, E)
+    assert e.value.code == rx.ERR_ARG
+    qn = q.clone().pin_memory()
+    qn[5] = float("nan")
+    with pytest.raises(rx.ReaxError) as e:
+        ctx.step_host(pos, typ, qn, F, E)
+    assert e.value.code == rx.ERR_NONFINITE
+    ctx.step_host(pos, typ, q, F, E)
+    assert np.array_equal(F.numpy(), Fd.cpu().numpy()) and np.array_equal(E.numpy(), Ed.cpu().numpy())
