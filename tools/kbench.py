@@ -34,6 +34,14 @@ def main():
     ctx.check()
     nbr = ctx.kernel_ms(reset=True)["nbr"][0] / reps
     ctx.bond_orders()
+    ctx.kernel_ms(reset=True)
+    for i in range(reps):
+        flush.fill_(float(i))
+        ctx.bond_orders()
+    torch.cuda.synchronize()
+    ctx.check()
+    km = ctx.kernel_ms(reset=True)
+    bonds, bo = km["bonds"][0] / reps, km["bond_orders"][0] / reps
     F = torch.empty((n, 3), dtype=torch.float64, device=dev)
     E = torch.empty(2, dtype=torch.float64, device=dev)
     ctx.nonbonded(pos, typ, q, F, E)
@@ -46,6 +54,7 @@ def main():
     nb = ctx.kernel_ms(reset=True)["nonbonded"][0] / reps
     P, _ = ctx.pair_count()
     print(json.dumps({"lib": os.environ.get("REAX_LIBRARY", "default"), "config": k, "nbr_ms": nbr, "nb_ms": nb,
+                      "bonds_ms": bonds, "bond_correct_ms": bo,
                       "pairs": P, "E": E.cpu().tolist()}), flush=True)
 
 
