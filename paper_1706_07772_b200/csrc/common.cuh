@@ -78,10 +78,10 @@ struct DevParams {
   float rcand2[NTP_MAX];     // fp32 bond-candidate radius^2 (conservative)
   float rcand2_max;
   double val[NT_MAX], val_boc[NT_MAX];
-  NBPair nb[NTP_MAX];
+  alignas(16) NBPair nb[NTP_MAX];   // 16-byte aligned: the nonbonded kernel copies these with cp.async
   BOPair bo[NTP_MAX];
-  double exp_tbl[256];       // 2^(j/256)
-  double log_tbl[2 * 256];   // {1/c_j rounded, -log(that value)}, c_j = 1 + (j + 1/2)/256
+  alignas(16) double exp_tbl[256];       // 2^(j/256)
+  alignas(16) double log_tbl[2 * 256];   // {1/c_j rounded, -log(that value)}, c_j = 1 + (j + 1/2)/256
 };
 
 // ------------------------------------------------------------------ status
@@ -120,6 +120,8 @@ struct WS {
   int* stype;        // n
   uint16_t* nbr;     // n * row_cap   half list: window slots
   int* nbr_len;      // n
+  int* wpack;        // nblock * WPACK_INTS: each home block's window as the list build made it
+  int2* wsinfo;      // nblock * window_cap: its slot info {sorted atom, window cell | type << 8}
   int* bc;           // n * cand_cap  bond candidates (sorted j), then kept half bonds
   int* bc_len;       // n
   double4* bc_raw;   // n * cand_cap  BO'sigma, BO'pi, BO'pipi, BO' of kept half bonds

@@ -466,6 +466,7 @@ struct WinSmem {
   int cnt[NWU_MAX];
   int slot[NWU_MAX + 1];    // slot base (prefix of cnt)
   double4 shift[NWU_MAX];   // periodic image shift (0 or +-L) of each window cell (x, y, z, 0)
+  int shc[NWU_MAX];         // the same as a code: sum over axes a of (m_a + 1) << 2a, m_a in {-1, 0, 1}
   int home_ok[NHOME];       // home sub-cell exists (odd nc leaves the last block partial)
   int has_shift;            // some window cell is a periodic image
 };
@@ -485,6 +486,7 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
     hok |= ((base[0] + h % HB < g.nc[0]) && (base[1] + (h / HB) % HB < g.nc[1]) && (base[2] + h / (HB * HB) < g.nc[2]))
                ? (1u << h) : 0u;
   for (int k = threadIdx.x; k < nwu; k += blockDim.x) {
+    int code = 0;
     bool need = false;
 #pragma unroll
     for (int h = 0; h < NHOME; ++h) need |= ((hok >> h) & 1u) && ((c_win.mask[h][k >> 5] >> (k & 31)) & 1u);
@@ -499,9 +501,11 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
       int m = u < 0 ? -1 : (u >= g.nc[a] ? 1 : 0);
       cc[a] = u - m * g.nc[a];
       sh[a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
+      code |= (m + 1) << (2 * a);
       my_shift |= need && (m != 0);
     }
     W.shift[k] = make_double4(sh[0], sh[1], sh[2], 0.0);
+    W.shc[k] = code;
     int cid = (cc[2] * g.nc[1] + cc[1]) * g.nc[0] + cc[0];
     int s0 = cell_start[cid];
     W.start[k] = s0;
@@ -527,6 +531,62 @@ __device__ int build_window(WinSmem& W, int b, const Grid& g, const int* __restr
   }
   __syncthreads();
   return W.slot[nwu];
+}
+
+// The window of a home block as the list build made it, for the nonbonded
+// kernel (which then skips its own window build and slot-info staging):
+// {W, home_ok bits, has_shift, 0}, start[NWU_MAX], cnt[NWU_MAX],
+// slot[NWU_MAX + 1], shift codes[NWU_MAX] per block in `wpack`, and the
+// slot info {sorted atom, window cell | type << 8} of every slot in `wsinfo`
+// (window_cap entries per block); then the lengths of the block's first
+// WP_MAXROWS rows in home order (written by the list-build CTA that made the
+// row).
+constexpr int WP_MAXROWS = 256;
+constexpr int WP_START = 4, WP_CNT = WP_START + NWU_MAX, WP_SLOT = WP_CNT + NWU_MAX, WP_SHC = WP_SLOT + NWU_MAX + 1;
+constexpr int WP_LEN = (WP_SHC + NWU_MAX + 3) & ~3;
+constexpr int WPACK_INTS = WP_LEN + WP_MAXROWS;
+__device__ void win_store(const WinSmem& W, int Wslots, int* __restrict__ wp) {
+  const int nwu = c_win.nwu;
+  for (int t = threadIdx.x; t < WP_LEN; t += blockDim.x) {
+    int v = 0;
+    if (t == 0) v = Wslots;
+    else if (t == 1) {
+      for (int h = 0; h < NHOME; ++h) v |= W.home_ok[h] ? 1 << h : 0;
+    } else if (t == 2) v = W.has_shift;
+    else if (t >= WP_START && t < WP_START + nwu) v = W.start[t - WP_START];
+    else if (t >= WP_CNT && t < WP_CNT + nwu) v = W.cnt[t - WP_CNT];
+    else if (t >= WP_SLOT && t <= WP_SLOT + nwu) v = W.slot[t - WP_SLOT];
+    else if (t >= WP_SHC && t < WP_SHC + nwu) v = W.shc[t - WP_SHC];
+    wp[t] = v;
+  }
+}
+// the inverse (all threads; ends with __syncthreads), row lengths into
+// lens[WP_MAXROWS]; returns W
+__device__ int win_load(WinSmem& W, const Grid& g, const int* __restrict__ wp, int* lens) {
+  const int nwu = c_win.nwu;
+  for (int t = threadIdx.x; t < WPACK_INTS; t += blockDim.x) {
+    const int v = wp[t];
+    if (t >= WP_LEN) lens[t - WP_LEN] = v;
+    else if (t == 1) {
+      for (int h = 0; h < NHOME; ++h) W.home_ok[h] = (v >> h) & 1;
+    } else if (t == 2) W.has_shift = v;
+    else if (t >= WP_START && t < WP_START + nwu) W.start[t - WP_START] = v;
+    else if (t >= WP_CNT && t < WP_CNT + nwu) W.cnt[t - WP_CNT] = v;
+    else if (t >= WP_SLOT && t <= WP_SLOT + nwu) W.slot[t - WP_SLOT] = v;
+    else if (t >= WP_SHC && t < WP_SHC + nwu) {
+      const int k = t - WP_SHC;
+      double sh[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int m = ((v >> (2 * a)) & 3) - 1;
+        sh[a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
+      }
+      W.shift[k] = make_double4(sh[0], sh[1], sh[2], 0.0);
+      W.shc[k] = v;
+    }
+  }
+  __syncthreads();
+  return wp[0];
 }
 
 // rows of the block: home sub-cell h, slot range [slot[home_k[h]], slot[home_k[h]+1])
@@ -571,6 +631,7 @@ struct NbrSmem {
   RunInfo run[NHOME][MAX_RUNS];
   float rcand2[NTP_MAX];
   int gbase[NHOME + 1];   // first row group of each home sub-cell (groups of NBR_G rows)
+  int rbase[NHOME];       // first row (block order) of each home sub-cell
   int ncs[NBR_THREADS / 32][8];   // per warp: bond-candidate counters of its group's rows
   int next_row;
   int pairs;                      // half-list entries of this CTA's rows (nonbonded work plan)
@@ -773,7 +834,7 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
     const float4* __restrict__ sloc, const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     uint16_t* __restrict__ nbr, int* __restrict__ nbr_len, int row_cap, int* __restrict__ bc,
     int* __restrict__ bc_len, int cand_cap, int window_cap, int nsplit, Status* st, int* __restrict__ blk_pairs,
-    const RowTest rt) {
+    const RowTest rt, int* __restrict__ wpack, int2* __restrict__ wsinfo) {
   pdl_wait();
   TL_MARK(0, 0);
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -803,16 +864,21 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
   const int nwu = c_win.nwu;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {   // row groups of the block (home sub-cell order)
-    int gb = 0;
+    int gb = 0, rb = 0;
     for (int h = 0; h < NHOME; ++h) {
       S.gbase[h] = gb;
-      if (S.W.home_ok[h]) gb += (S.W.cnt[c_win.home_k[h]] + NBR_G - 1) / NBR_G;
+      S.rbase[h] = rb;
+      if (S.W.home_ok[h]) {
+        gb += (S.W.cnt[c_win.home_k[h]] + NBR_G - 1) / NBR_G;
+        rb += S.W.cnt[c_win.home_k[h]];
+      }
     }
     S.gbase[NHOME] = gb;
     S.next_row = 0;
     S.pairs = 0;
   }
   __syncthreads();
+  if (split == 0) win_store(S.W, W, wpack + (int64_t)blk * WPACK_INTS);   // for the nonbonded kernel
   if (W > window_cap) {
     if (threadIdx.x == 0) {
       set_flag(st, ST_WIN_OVF);
@@ -851,6 +917,11 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
   }
   if (threadIdx.x < 32) cand[window_cap + threadIdx.x] = make_float4(1e30f, 1e30f, 1e30f, 0.f);   // sentinel
   __syncthreads();
+  if (split == 0) {   // slot info of the window, for the nonbonded kernel
+    int2* ws = wsinfo + (int64_t)blk * window_cap;
+    for (int t = threadIdx.x; t < W; t += blockDim.x)
+      ws[t] = make_int2(cand_j[t], (int)cand_k[t] | (__float_as_int(cand[t].w) << 8));
+  }
   TL_MARK(0, 1, W);
   // groups of NBR_G consecutive rows of one home sub-cell; this CTA takes
   // groups split, split + nsplit, ...
@@ -879,6 +950,8 @@ __global__ void __launch_bounds__(NBR_THREADS, NBR_MINB) k_nbr_build(Grid g, con
         if (lane == r) { l = len[r]; c = nc[r]; }
       const int s = cand_j[si0 + lane];
       nbr_len[s] = l < row_cap ? l : row_cap;
+      const int rblk = S.rbase[h] + a0 + lane;   // row index in the block (home order)
+      if (rblk < WP_MAXROWS) wpack[(int64_t)blk * WPACK_INTS + WP_LEN + rblk] = l < row_cap ? l : row_cap;
       bc_len[s] = c < cand_cap ? c : cand_cap;
       if (l > row_cap) { set_flag(st, ST_ROW_OVF); atomicMax(&st->max_row, l); }
       if (c > cand_cap) { set_flag(st, ST_CAND_OVF); atomicMax(&st->max_cand, c); }
@@ -1490,7 +1563,9 @@ struct NBSmem {
   int order[NB_MAX_ROWS];        // row window slots, longest row first
   int rlen[NB_MAX_ROWS];         // their lengths
   int next_row;                  // dynamic row counter
+  int blen[WP_MAXROWS];          // lengths of the block's rows (home order), from the list build
 };
+static_assert(NB_MAX_ROWS <= WP_MAXROWS, "row lengths of the ranked rows");
 
 // One CTA per (home block, split) (Alg. 2, re-designed): a
 // warp streams the half-list entries of its rows 32 at a time (lanes over
@@ -1503,13 +1578,16 @@ struct NBSmem {
 // GPU form of the paper's thread-private tprivForce) and flushed to the
 // global int64 sorted force array once per CTA.  Energies: per-lane sums in
 // the row's pair order, one partial per row, reduced later in fixed order.
-// Forces and energies are bitwise reproducible.
-__global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const int* __restrict__ cell_start,
+// Forces and energies are bitwise reproducible.  The CTA does not rebuild
+// its window: the list build stored it (window arrays, slot info and row
+// lengths, `wpack` / `wsinfo`), and the setup is one round trip for them plus
+// cp.async copies of the tables and slot info (c4: 9.2 -> ~6 us per CTA).
+__global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(int nt, Grid g, const int* __restrict__ cell_start,
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
     unsigned long long* __restrict__ sf,
     double2* __restrict__ erow, int nsplit, Status* st, const int* __restrict__ units, const int* __restrict__ nunits,
-    int* __restrict__ blkrow) {
+    int* __restrict__ blkrow, const int* __restrict__ wpack, const int2* __restrict__ wsinfo) {
   pdl_wait();
   TL_MARK(1, 0);
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -1527,7 +1605,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     blk = blockIdx.x / nsplit;
     split = blockIdx.x % nsplit;
   }
-  const int nt = prm->nt;
   double* ET = reinterpret_cast<double*>(dyn);                  // exp table
   double2* LT = reinterpret_cast<double2*>(ET + EXP_TBL);       // log table
   NBPair* pc = reinterpret_cast<NBPair*>(LT + LOG_TBL);         // nt*nt pair constants
@@ -1538,14 +1615,30 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   // a multiple of 32), typed from the shared base: shared-space loads (LDS)
   const int rb_cap = (row_cap + 7) & ~7;                                          // row buffer entries (16-byte multiple)
   uint16_t* rbuf = reinterpret_cast<uint16_t*>(fb + 3 * window_cap);              // [NB_WARPS][2][rb_cap]
-  unsigned char* kmap = reinterpret_cast<unsigned char*>(rbuf + NB_WARPS * 2 * rb_cap);   // slot -> window cell
-  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) pc[t] = prm->nb[t];
-  for (int t = threadIdx.x; t < EXP_TBL; t += blockDim.x) ET[t] = prm->exp_tbl[t];
-  for (int t = threadIdx.x; t < LOG_TBL; t += blockDim.x) LT[t] = make_double2(prm->log_tbl[2 * t], prm->log_tbl[2 * t + 1]);
+  // tables, pair constants and the window's slot info, copied asynchronously
+  // (16-byte pieces; exp and log tables are contiguous in DevParams, as in
+  // shared memory) while the window arrays are read
+  {
+    auto cp16 = [&](void* dst, const void* src, int bytes) {
+      for (int p = threadIdx.x; p < (bytes >> 4); p += blockDim.x) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(reinterpret_cast<char*>(dst) + 16 * p);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(reinterpret_cast<const char*>(src) + 16 * p));
+      }
+    };
+    static_assert(sizeof(NBPair) % 16 == 0, "pair constants in 16-byte pieces");
+    cp16(pc, prm->nb, (int)sizeof(NBPair) * nt * nt);
+    cp16(ET, prm->exp_tbl, (int)sizeof(double) * EXP_TBL);
+    cp16(LT, prm->log_tbl, (int)sizeof(double) * 2 * LOG_TBL);
+    const int Wg = wpack[(int64_t)blk * WPACK_INTS];   // W (the list build flagged W > window_cap)
+    cp16(sinfo, wsinfo + (int64_t)blk * window_cap, Wg <= window_cap ? 8 * ((Wg + 1) & ~1) : 0);
+    asm volatile("cp.async.commit_group;");
+  }
   NBConst kc;
   kc.invR = prm->invR; kc.phalf = 0.5 * prm->p_vdw; kc.inv_p = prm->inv_p; kc.m140invR = -140.0 * prm->invR;
   const double C = prm->C;
-  const int W = build_window(S.W, blk, g, cell_start);
+  // the window as the list build made it (and the block's row lengths)
+  const int W = win_load(S.W, g, wpack + (int64_t)blk * WPACK_INTS, S.blen);
+  (void)cell_start;
   TL_MARK(1, 4);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (W > window_cap) {
@@ -1554,6 +1647,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
       atomicMax(&st->max_window, W);
     }
     zero_rows_erow(S.W, split, nsplit, erow);
+    asm volatile("cp.async.wait_all;" ::: "memory");
     return;
   }
   const int nwu = c_win.nwu;
@@ -1563,18 +1657,19 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
     if (S.W.home_ok[h]) nrows_blk += S.W.cnt[c_win.home_k[h]];
   const int nrows = nrows_blk > split ? (nrows_blk - split + nsplit - 1) / nsplit : 0;
   const int nsorted = nrows < NB_MAX_ROWS ? nrows : NB_MAX_ROWS;
-  // phase 1 (no global dependence between threads): slot -> cell map, row
-  // lengths, F window zero
-  for (int k = threadIdx.x; k < nwu; k += blockDim.x) {
-    const int b0 = S.W.slot[k], c = S.W.cnt[k];
-    for (int a = 0; a < c; ++a) kmap[b0 + a] = (unsigned char)k;
-  }
+  // phase 1 (no global dependence between threads): row ranking keys, F window zero
+  (void)nwu;
   int my_si = 0, my_len = 0;
   if ((int)threadIdx.x < nsorted) {
     int h;
-    row_of(S.W, split + threadIdx.x * nsplit, h, my_si);
-    const int k = c_win.home_k[h];
-    my_len = nbr_len[S.W.start[k] + (my_si - S.W.slot[k])];
+    const int r = split + threadIdx.x * nsplit;
+    row_of(S.W, r, h, my_si);
+    if (r < WP_MAXROWS) {
+      my_len = S.blen[r];
+    } else {
+      const int k = c_win.home_k[h];
+      my_len = nbr_len[S.W.start[k] + (my_si - S.W.slot[k])];
+    }
     S.rkey[threadIdx.x] = (my_len << 8) | (NB_MAX_ROWS - 1 - (int)threadIdx.x);
   } else if ((int)threadIdx.x < NB_MAX_ROWS) {
     S.rkey[threadIdx.x] = -1;
@@ -1589,14 +1684,10 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(Grid g, const
   }
   __syncthreads();
   TL_MARK(1, 5);
-  // phase 2: slot info (flattened over slots: the type loads are independent),
-  // row ranking (longest first; ties by home order)
-#pragma unroll 8
-  for (int t = threadIdx.x; t < W; t += blockDim.x) {
-    const int k = kmap[t];
-    const int j = S.W.start[k] + (t - S.W.slot[k]);
-    sinfo[t] = make_int2(j, k | (stype[j] << 8));
-  }
+  // phase 2: row ranking (longest first; ties by home order); the tables and
+  // the slot info have landed
+  (void)stype;
+  asm volatile("cp.async.wait_all;" ::: "memory");
   static_assert(NB_MAX_ROWS <= NB_THREADS, "one ranked row per thread");
   static_assert(NB_MAX_ROWS <= 256, "ranking keys: 8-bit index");
   if ((int)threadIdx.x < nsorted) {   // longest first, ties by home order: count the greater keys

@@ -338,6 +338,8 @@ size_t layout(int64_t n, const Grid& g, const reax_capacity& c, char* base, WS* 
   t.stype = (int*)take(sizeof(int) * N);
   t.nbr = (uint16_t*)take(sizeof(uint16_t) * N * (size_t)c.row_cap);
   t.nbr_len = (int*)take(sizeof(int) * N);
+  t.wpack = (int*)take(sizeof(int) * WPACK_INTS * (size_t)g.nblock);
+  t.wsinfo = (int2*)take(sizeof(int2) * (size_t)c.window_cap * (size_t)g.nblock);
   t.bc = (int*)take(sizeof(int) * N * (size_t)c.cand_cap);
   t.bc_len = (int*)take(sizeof(int) * N);
   t.bkey = (int*)take(sizeof(int) * (size_t)c.bond_cap);
@@ -659,7 +661,7 @@ size_t nbr_smem(int wcap, int row_cap = 0) {
   return (size_t)(wcap + 32) * (sizeof(float4) + sizeof(int) + 1) + 64;
 }
 size_t nb_smem(int wcap, int row_cap, int nt) {
-  return sizeof(double) * (EXP_TBL + 2 * LOG_TBL) + sizeof(NBPair) * nt * nt + (size_t)wcap * (sizeof(int2) + 6 * sizeof(int) + 1) +
+  return sizeof(double) * (EXP_TBL + 2 * LOG_TBL) + sizeof(NBPair) * nt * nt + (size_t)wcap * (sizeof(int2) + 6 * sizeof(int)) +
          16 + (size_t)NB_WARPS * 2 * ((row_cap + 7) & ~7) * sizeof(uint16_t) + 64;
 }
 size_t exp_smem(int wcap) { return (size_t)wcap * sizeof(int) + 64; }
@@ -737,7 +739,7 @@ void launch_nbr(reax_ctx* c, cudaStream_t s) {
   launch_k(c, k_nbr_build, g.nblock * c->nsplit_nbr, NBR_THREADS, nbr_smem(c->cap.window_cap, c->cap.row_cap), s,
            g, w.cell_start, w.sloc, w.spos, w.prm, w.nbr, w.nbr_len, c->cap.row_cap, w.bc, w.bc_len,
            c->cap.cand_cap, c->cap.window_cap, c->nsplit_nbr, w.st, c->nb_plan ? w.blk_pairs : nullptr,
-           make_rowtest(*c->h_prm, g));
+           make_rowtest(*c->h_prm, g), w.wpack, w.wsinfo);
   LAUNCH(c);
 }
 
@@ -835,9 +837,10 @@ void launch_nb(reax_ctx* c, int nt, cudaStream_t s) {
   }
   Timer t(c, 4, s);
   launch_k(c, k_nonbonded, c->nb_plan ? c->nb_umax : g.nblock * c->nsplit, NB_THREADS,
-           nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s, g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len,
+           nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s, nt, g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len,
            c->cap.row_cap, c->cap.window_cap, w.sf, w.erow, c->nsplit, w.st,
-           c->nb_plan ? (const int*)w.units : nullptr, c->nb_plan ? (const int*)w.nunits : nullptr, w.blkrow);
+           c->nb_plan ? (const int*)w.units : nullptr, c->nb_plan ? (const int*)w.nunits : nullptr, w.blkrow,
+           (const int*)w.wpack, (const int2*)w.wsinfo);
   LAUNCH(c);
 }
 
