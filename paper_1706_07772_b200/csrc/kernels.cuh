@@ -561,32 +561,43 @@ __device__ void win_store(const WinSmem& W, int Wslots, int* __restrict__ wp) {
   }
 }
 // the inverse (all threads; ends with __syncthreads), row lengths into
-// lens[WP_MAXROWS]; returns W
+// lens[WP_MAXROWS]; returns W.  NT threads: every load is issued before any
+// is used (one round trip).
+template <int NT>
 __device__ int win_load(WinSmem& W, const Grid& g, const int* __restrict__ wp, int* lens) {
+  constexpr int PER = (WPACK_INTS + NT - 1) / NT;
   const int nwu = c_win.nwu;
-  for (int t = threadIdx.x; t < WPACK_INTS; t += blockDim.x) {
-    const int v = wp[t];
-    if (t >= WP_LEN) lens[t - WP_LEN] = v;
+  int v[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int t = threadIdx.x + u * NT;
+    v[u] = t < WPACK_INTS ? wp[t] : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int t = threadIdx.x + u * NT;
+    if (t >= WPACK_INTS) break;
+    if (t >= WP_LEN) lens[t - WP_LEN] = v[u];
     else if (t == 1) {
-      for (int h = 0; h < NHOME; ++h) W.home_ok[h] = (v >> h) & 1;
-    } else if (t == 2) W.has_shift = v;
-    else if (t >= WP_START && t < WP_START + nwu) W.start[t - WP_START] = v;
-    else if (t >= WP_CNT && t < WP_CNT + nwu) W.cnt[t - WP_CNT] = v;
-    else if (t >= WP_SLOT && t <= WP_SLOT + nwu) W.slot[t - WP_SLOT] = v;
+      for (int h = 0; h < NHOME; ++h) W.home_ok[h] = (v[u] >> h) & 1;
+    } else if (t == 2) W.has_shift = v[u];
+    else if (t >= WP_START && t < WP_START + nwu) W.start[t - WP_START] = v[u];
+    else if (t >= WP_CNT && t < WP_CNT + nwu) W.cnt[t - WP_CNT] = v[u];
+    else if (t >= WP_SLOT && t <= WP_SLOT + nwu) W.slot[t - WP_SLOT] = v[u];
     else if (t >= WP_SHC && t < WP_SHC + nwu) {
       const int k = t - WP_SHC;
       double sh[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        const int m = ((v >> (2 * a)) & 3) - 1;
+        const int m = ((v[u] >> (2 * a)) & 3) - 1;
         sh[a] = m == 0 ? 0.0 : (m > 0 ? g.L[a] : -g.L[a]);
       }
       W.shift[k] = make_double4(sh[0], sh[1], sh[2], 0.0);
-      W.shc[k] = v;
+      W.shc[k] = v[u];
     }
   }
   __syncthreads();
-  return wp[0];
+  return W.slot[nwu];   // W (the slot total, also when the list build found W > window_cap)
 }
 
 // rows of the block: home sub-cell h, slot range [slot[home_k[h]], slot[home_k[h]+1])
@@ -1581,7 +1592,7 @@ static_assert(NB_MAX_ROWS <= WP_MAXROWS, "row lengths of the ranked rows");
 // Forces and energies are bitwise reproducible.  The CTA does not rebuild
 // its window: the list build stored it (window arrays, slot info and row
 // lengths, `wpack` / `wsinfo`), and the setup is one round trip for them plus
-// cp.async copies of the tables and slot info (c4: 9.2 -> ~6 us per CTA).
+// cp.async copies of the tables and slot info (c4: 9.2 -> 5.1 us per CTA).
 __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(int nt, Grid g, const int* __restrict__ cell_start,
     const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
@@ -1629,15 +1640,19 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(int nt, Grid 
     cp16(pc, prm->nb, (int)sizeof(NBPair) * nt * nt);
     cp16(ET, prm->exp_tbl, (int)sizeof(double) * EXP_TBL);
     cp16(LT, prm->log_tbl, (int)sizeof(double) * 2 * LOG_TBL);
-    const int Wg = wpack[(int64_t)blk * WPACK_INTS];   // W (the list build flagged W > window_cap)
-    cp16(sinfo, wsinfo + (int64_t)blk * window_cap, Wg <= window_cap ? 8 * ((Wg + 1) & ~1) : 0);
+    // the whole capacity (not the block's W, which would cost a dependent round trip first)
+    cp16(sinfo, wsinfo + (int64_t)blk * window_cap, 8 * window_cap);
     asm volatile("cp.async.commit_group;");
   }
   NBConst kc;
   kc.invR = prm->invR; kc.phalf = 0.5 * prm->p_vdw; kc.inv_p = prm->inv_p; kc.m140invR = -140.0 * prm->invR;
   const double C = prm->C;
+  {   // zero F window (while the loads below are in flight)
+    uint4* z = reinterpret_cast<uint4*>(fa);          // fa and fb are contiguous: 6 window_cap words
+    for (int t = threadIdx.x; t < (6 * window_cap) / 4; t += blockDim.x) z[t] = make_uint4(0u, 0u, 0u, 0u);
+  }
   // the window as the list build made it (and the block's row lengths)
-  const int W = win_load(S.W, g, wpack + (int64_t)blk * WPACK_INTS, S.blen);
+  const int W = win_load<NB_THREADS>(S.W, g, wpack + (int64_t)blk * WPACK_INTS, S.blen);
   (void)cell_start;
   TL_MARK(1, 4);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1674,10 +1689,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(int nt, Grid 
   } else if ((int)threadIdx.x < NB_MAX_ROWS) {
     S.rkey[threadIdx.x] = -1;
   }
-  {
-    uint4* z = reinterpret_cast<uint4*>(fa);          // fa and fb are contiguous: 6 window_cap words
-    for (int t = threadIdx.x; t < (6 * window_cap) / 4; t += blockDim.x) z[t] = make_uint4(0u, 0u, 0u, 0u);
-  }
   if (threadIdx.x == 0) {
     S.bad = 0;
     S.next_row = 0;
@@ -1694,6 +1705,7 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(int nt, Grid 
     const int key = (my_len << 8) | (NB_MAX_ROWS - 1 - (int)threadIdx.x);
     const int4* k4 = reinterpret_cast<const int4*>(S.rkey);
     int rank = 0;
+#pragma unroll 4
     for (int q = 0; q < (nsorted + 3) >> 2; ++q) {
       const int4 v = k4[q];
       rank += (v.x > key) + (v.y > key) + (v.z > key) + (v.w > key);
