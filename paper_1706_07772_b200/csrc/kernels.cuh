@@ -1593,8 +1593,8 @@ static_assert(NB_MAX_ROWS <= WP_MAXROWS, "row lengths of the ranked rows");
 // its window: the list build stored it (window arrays, slot info and row
 // lengths, `wpack` / `wsinfo`), and the setup is one round trip for them plus
 // cp.async copies of the tables and slot info (c4: 9.2 -> 5.1 us per CTA).
-__global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(int nt, Grid g, const int* __restrict__ cell_start,
-    const double4* __restrict__ spos, const int* __restrict__ stype, const DevParams* __restrict__ prm,
+__global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(int nt, Grid g,
+    const double4* __restrict__ spos, const DevParams* __restrict__ prm,
     const uint16_t* __restrict__ nbr, const int* __restrict__ nbr_len, int row_cap, int window_cap,
     unsigned long long* __restrict__ sf,
     double2* __restrict__ erow, int nsplit, Status* st, const int* __restrict__ units, const int* __restrict__ nunits,
@@ -1653,7 +1653,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(int nt, Grid 
   }
   // the window as the list build made it (and the block's row lengths)
   const int W = win_load<NB_THREADS>(S.W, g, wpack + (int64_t)blk * WPACK_INTS, S.blen);
-  (void)cell_start;
   TL_MARK(1, 4);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (W > window_cap) {
@@ -1697,7 +1696,6 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINB) k_nonbonded(int nt, Grid 
   TL_MARK(1, 5);
   // phase 2: row ranking (longest first; ties by home order); the tables and
   // the slot info have landed
-  (void)stype;
   asm volatile("cp.async.wait_all;" ::: "memory");
   static_assert(NB_MAX_ROWS <= NB_THREADS, "one ranked row per thread");
   static_assert(NB_MAX_ROWS <= 256, "ranking keys: 8-bit index");

@@ -837,7 +837,7 @@ void launch_nb(reax_ctx* c, int nt, cudaStream_t s) {
   }
   Timer t(c, 4, s);
   launch_k(c, k_nonbonded, c->nb_plan ? c->nb_umax : g.nblock * c->nsplit, NB_THREADS,
-           nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s, nt, g, w.cell_start, w.spos, w.stype, w.prm, w.nbr, w.nbr_len,
+           nb_smem(c->cap.window_cap, c->cap.row_cap, nt), s, nt, g, w.spos, w.prm, w.nbr, w.nbr_len,
            c->cap.row_cap, c->cap.window_cap, w.sf, w.erow, c->nsplit, w.st,
            c->nb_plan ? (const int*)w.units : nullptr, c->nb_plan ? (const int*)w.nunits : nullptr, w.blkrow,
            (const int*)w.wpack, (const int2*)w.wsinfo);
